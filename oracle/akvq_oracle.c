@@ -1,0 +1,570 @@
+/*
+ * akvq_oracle.c -- plain, slow, obviously-correct CPU oracle of the AKVQ-VL
+ * hot path (arXiv 2501.15021).  TEST INFRASTRUCTURE: see akvq_oracle.h for
+ * who may use it.  Shares nothing with the CUDA path.
+ *
+ * Build: gcc -O2 -std=c11 -fopenmp -ffp-contract=off -fPIC -shared
+ *        (no -ffast-math: the fp32 decisions must be plain IEEE single ops;
+ *         -ffp-contract=off forbids fusing a*b+c into an FMA).
+ *
+ * The method, in the paper's order:
+ *  1. Walsh-Hadamard matrix (Eq. 7) and the equivalent
+ *     transformation of Q/K after RoPE (Fig. 6) and of V/O
+ *     (Fig. 7; applied online here, R4).
+ *  2. Salient tokens: text tokens in TSA layers, pivot tokens in
+ *     PSA layers (top-k over accumulated attention column sums per
+ *     north_star BJ:5, R2), recent tokens always.
+ *  3. Pivot + recent tokens at the original 16-bit precision, text tokens at
+ *     4 bits, the rest at 2 bits, with Eqs. 3-6 and
+ *     clip ratios 0.8 / 1.0, group size G.  K per channel
+ *     over G-token blocks, V per token over G-channel groups (BJ:5, R1).
+ *  4. Decode attention over the cache (Eq. 2 "update the KV cache", P:112-119;
+ *     softmax(q K^T / sqrt d) V), computed as the plain definition on
+ *     the dequantized view.
+ */
+#include "akvq_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+struct orc_cache {
+  orc_config cfg;
+  int cap;        /* capacity rounded up to a multiple of G              */
+  int side_cap;   /* PSA: top_k; TSA: cap                                 */
+  int L, nq;      /* tokens stored; tokens in the quantized region        */
+  double *H;      /* normalized Walsh-Hadamard matrix, d x d (Eq. 7)      */
+  double *Hs;     /* +-1 Walsh-Hadamard matrix H_s = sqrt(d) H            */
+  uint16_t *K, *V;      /* [U][cap][d] original 16-bit rows, every token  */
+  uint8_t *sal;         /* [U][cap] salient flag                           */
+  float *xk, *xv;       /* [U][cap][d] fp32 K.H_s, V.H_s (decision inputs) */
+  uint8_t *kc, *vc;     /* [U][cap][d] unpacked 2-bit codes                */
+  float *ks32;          /* [U][cap/G][d] K scale (unnormalized units)      */
+  int32_t *kz;          /* [U][cap/G][d] K zero point                      */
+  float *vs32;          /* [U][cap][d/G] V scale (unnormalized units)      */
+  int32_t *vz;          /* [U][cap][d/G] V zero point                      */
+  int32_t *side_idx;    /* [U][side_cap] token index of each side entry    */
+  int32_t *side_cnt;    /* [U]                                             */
+  int32_t *side_pos;    /* [U][cap] side entry of token t (or -1)          */
+  uint8_t *s4c;         /* [U][side_cap][2][d] unpacked 4-bit codes (TSA)  */
+  float *s4s32;         /* [U][side_cap][2][d/G]                           */
+  int32_t *s4z;         /* [U][side_cap][2][d/G]                           */
+};
+
+static int is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+/* ------------------------------------------------------------------ */
+/* Eq. 7: H_1 = [1];                                        */
+/*   H_{2^k} = (1/sqrt 2) [[H_{2^(k-1)},  H_{2^(k-1)}],                 */
+/*                         [H_{2^(k-1)}, -H_{2^(k-1)}]].                */
+/* Built literally by the recursion, one doubling at a time.            */
+int orc_hadamard(int d, int normalized, double *H) {
+  if (!is_pow2(d)) return ORC_EINVAL;
+  const double f = normalized ? 1.0 / sqrt(2.0) : 1.0;
+  H[0] = 1.0;                                   /* H_1 = [1] */
+  for (int n = 1; n < d; n *= 2) {              /* H_n -> H_2n, in place */
+    /* copy H_n (stored with row stride d) into the four quadrants,
+     * bottom-right negated; go from the last row up so the top-left
+     * quadrant is read before it is overwritten. */
+    for (int i = n - 1; i >= 0; --i) {
+      for (int j = n - 1; j >= 0; --j) {
+        const double h = H[i * d + j];
+        H[i * d + j] = f * h;
+        H[i * d + j + n] = f * h;
+        H[(i + n) * d + j] = f * h;
+        H[(i + n) * d + j + n] = -f * h;
+      }
+    }
+  }
+  return ORC_OK;
+}
+
+/* y = x . H  (explicit vector-matrix product in fp64). */
+int orc_rotate(int d, int normalized, const double *x, double *y) {
+  if (!is_pow2(d)) return ORC_EINVAL;
+  double *H = (double *)malloc(sizeof(double) * d * d);
+  orc_hadamard(d, normalized, H);
+  for (int j = 0; j < d; ++j) {
+    double s = 0.0;
+    for (int i = 0; i < d; ++i) s += x[i] * H[i * d + j];
+    y[j] = s;
+  }
+  free(H);
+  return ORC_OK;
+}
+
+static void matvec(int d, const double *H, const double *x, double *y) {
+  for (int j = 0; j < d; ++j) {
+    double s = 0.0;
+    for (int i = 0; i < d; ++i) s += x[i] * H[i * d + j];
+    y[j] = s;
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* 16-bit inputs are widened exactly.                                   */
+double orc_half_to_double(uint16_t h, int dtype16) {
+  if (dtype16 == ORC_BF16) {
+    uint32_t u = (uint32_t)h << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return (double)f;
+  }
+  /* IEEE binary16: 1 sign, 5 exponent (bias 15), 10 mantissa bits. */
+  const int s = (h >> 15) & 1, e = (h >> 10) & 0x1f, m = h & 0x3ff;
+  double v;
+  if (e == 0) v = ldexp((double)m, -24);                 /* subnormal */
+  else if (e == 31) v = m ? NAN : INFINITY;
+  else v = ldexp((double)(m | 0x400), e - 25);           /* 1.m * 2^(e-15) */
+  return s ? -v : v;
+}
+
+/* ------------------------------------------------------------------ */
+/* Eqs. 3, 5, 6 on one group of n elements (stride apart).  */
+/*   clipped_max = clip * max, clipped_min = clip * min   (R3)   */
+/*   scale = (clipped_max - clipped_min) / (2^n - 1)           Eq. 5    */
+/*   zero  = -round(clipped_min / scale)                       Eq. 6    */
+/*   Q(X)  = clamp(round(X / scale) + zero, 0, 2^n - 1)        Eq. 3    */
+/* round = round-half-to-even (R7).  Degenerate group (clipped range <  */
+/* 1e-12): scale = the constant, zero 0, codes 1 (R8).  Empty    */
+/* group (all elements skipped): scale 0, zero 0, codes 0 (R8).         */
+/* Every step is an fp32 IEEE operation (R6); skipped elements get 0.   */
+void orc_quantize_group(const float *x, const uint8_t *skip, int n, int stride,
+                        int bits, float clip, float *scale, int32_t *zero,
+                        uint8_t *codes, int code_stride) {
+  const int levels = (1 << bits) - 1;
+  int any = 0;
+  float mx = 0.0f, mn = 0.0f;
+  for (int i = 0; i < n; ++i) {
+    if (skip && skip[i]) continue;
+    const float v = x[(long)i * stride];
+    if (!any) { mx = v; mn = v; any = 1; }
+    else { if (v > mx) mx = v; if (v < mn) mn = v; }
+  }
+  if (!any) {
+    *scale = 0.0f; *zero = 0;
+    for (int i = 0; i < n; ++i) codes[(long)i * code_stride] = 0;
+    return;
+  }
+  const float cmx = clip * mx;               /* clipped_max(X) */
+  const float cmn = clip * mn;               /* clipped_min(X) */
+  const float range = cmx - cmn;
+  if (range < 1e-12f) {                      /* degenerate constant group */
+    *scale = mx; *zero = 0;
+    for (int i = 0; i < n; ++i)
+      codes[(long)i * code_stride] = (skip && skip[i]) ? 0 : 1;
+    return;
+  }
+  const float s = range / (float)levels;     /* Eq. 5 */
+  const float zf = -rintf(cmn / s);          /* Eq. 6 */
+  for (int i = 0; i < n; ++i) {
+    if (skip && skip[i]) { codes[(long)i * code_stride] = 0; continue; }
+    const float r = rintf(x[(long)i * stride] / s);            /* Eq. 3 */
+    double q = (double)r + (double)zf;
+    if (q < 0.0) q = 0.0;
+    if (q > (double)levels) q = (double)levels;
+    codes[(long)i * code_stride] = (uint8_t)q;
+  }
+  *scale = s;
+  if (zf > 2147483520.0f) *zero = 2147483647;
+  else if (zf < -2147483648.0f) *zero = (int32_t)0x80000000u;
+  else *zero = (int32_t)zf;
+}
+
+/* 2-bit code i -> bits [2(i mod 4), 2(i mod 4)+1] of byte i/4;
+ *        4-bit code i -> low nibble of byte i/2 if i even, else high.   */
+void orc_pack(const uint8_t *codes, int n, int bits, uint8_t *out) {
+  const int per = 8 / bits;
+  memset(out, 0, (size_t)((n + per - 1) / per));
+  for (int i = 0; i < n; ++i)
+    out[i / per] |= (uint8_t)((codes[i] & ((1 << bits) - 1)) << (bits * (i % per)));
+}
+void orc_unpack(const uint8_t *in, int n, int bits, uint8_t *codes) {
+  const int per = 8 / bits;
+  for (int i = 0; i < n; ++i)
+    codes[i] = (in[i / per] >> (bits * (i % per))) & ((1 << bits) - 1);
+}
+
+/* ------------------------------------------------------------------ */
+/* Salient-token selection for one unit (BJ:5, R2).          */
+/*  TSA: salient = text tokens (type 1).                                */
+/*  PSA: score_t = sum_{j<g} colsum[j][t] (fp32, j ascending: R6), the   */
+/*       min(top_k, L0) tokens first in the order (score desc, t asc).   */
+static const float *g_sort_scores;
+static int cmp_desc_score_asc_idx(const void *a, const void *b) {
+  const int i = *(const int *)a, j = *(const int *)b;
+  const float si = g_sort_scores[i], sj = g_sort_scores[j];
+  if (si > sj) return -1;
+  if (si < sj) return 1;
+  return (i > j) - (i < j);
+}
+void orc_select_salient(int kind, int g, int L0, int top_k,
+                        const uint8_t *types, const float *colsum,
+                        uint8_t *salient) {
+  memset(salient, 0, (size_t)L0);
+  if (kind == ORC_TSA) {
+    for (int t = 0; t < L0; ++t) salient[t] = types[t] == 1;
+    return;
+  }
+  if (L0 <= 0) return;
+  float *score = (float *)malloc(sizeof(float) * L0);
+  int *order = (int *)malloc(sizeof(int) * L0);
+  for (int t = 0; t < L0; ++t) {
+    float s = 0.0f;
+    for (int j = 0; j < g; ++j) s += colsum[(long)j * L0 + t];
+    score[t] = s;
+    order[t] = t;
+  }
+  /* a library sort is a permitted step; qsort is not reentrant-safe with
+   * the global, so this runs under a critical section when threaded. */
+#ifdef _OPENMP
+#pragma omp critical(orc_sort)
+#endif
+  {
+    g_sort_scores = score;
+    qsort(order, (size_t)L0, sizeof(int), cmp_desc_score_asc_idx);
+  }
+  const int k = top_k < L0 ? top_k : L0;
+  for (int r = 0; r < k; ++r) salient[order[r]] = 1;
+  free(score);
+  free(order);
+}
+
+/* ------------------------------------------------------------------ */
+static long ROW(const orc_cache *c, int u, int t) {
+  return ((long)u * c->cap + t) * c->cfg.d;
+}
+
+orc_cache *orc_new(const orc_config *cfg, int *status) {
+  const int d = cfg->d, G = cfg->G;
+  if (!is_pow2(d) || d > 512 || !is_pow2(G) || G > d || cfg->U < 1 || cfg->g < 1 ||
+      cfg->R < 0 || cfg->capacity < 1 || cfg->top_k < 0 ||
+      !(cfg->clip2 > 0.0f && cfg->clip2 <= 1.0f) ||
+      !(cfg->clip4 > 0.0f && cfg->clip4 <= 1.0f) ||
+      (cfg->kind != ORC_TSA && cfg->kind != ORC_PSA)) {
+    if (status) *status = ORC_EINVAL;
+    return NULL;
+  }
+  orc_cache *c = (orc_cache *)calloc(1, sizeof(orc_cache));
+  c->cfg = *cfg;
+  c->cap = (cfg->capacity + G - 1) / G * G;
+  c->side_cap = cfg->kind == ORC_PSA ? cfg->top_k : c->cap;
+  const long U = cfg->U, cap = c->cap, sc = c->side_cap > 0 ? c->side_cap : 1;
+  c->H = (double *)malloc(sizeof(double) * d * d);
+  c->Hs = (double *)malloc(sizeof(double) * d * d);
+  orc_hadamard(d, 1, c->H);
+  orc_hadamard(d, 0, c->Hs);
+  c->K = (uint16_t *)calloc((size_t)(U * cap * d), 2);
+  c->V = (uint16_t *)calloc((size_t)(U * cap * d), 2);
+  c->sal = (uint8_t *)calloc((size_t)(U * cap), 1);
+  c->xk = (float *)calloc((size_t)(U * cap * d), 4);
+  c->xv = (float *)calloc((size_t)(U * cap * d), 4);
+  c->kc = (uint8_t *)calloc((size_t)(U * cap * d), 1);
+  c->vc = (uint8_t *)calloc((size_t)(U * cap * d), 1);
+  c->ks32 = (float *)calloc((size_t)(U * (cap / G) * d), 4);
+  c->kz = (int32_t *)calloc((size_t)(U * (cap / G) * d), 4);
+  c->vs32 = (float *)calloc((size_t)(U * cap * (d / G)), 4);
+  c->vz = (int32_t *)calloc((size_t)(U * cap * (d / G)), 4);
+  c->side_idx = (int32_t *)calloc((size_t)(U * sc), 4);
+  c->side_cnt = (int32_t *)calloc((size_t)U, 4);
+  c->side_pos = (int32_t *)malloc(sizeof(int32_t) * U * cap);
+  for (long i = 0; i < U * cap; ++i) c->side_pos[i] = -1;
+  c->s4c = (uint8_t *)calloc((size_t)(U * sc * 2 * d), 1);
+  c->s4s32 = (float *)calloc((size_t)(U * sc * 2 * (d / G)), 4);
+  c->s4z = (int32_t *)calloc((size_t)(U * sc * 2 * (d / G)), 4);
+  if (status) *status = ORC_OK;
+  return c;
+}
+
+void orc_free(orc_cache *c) {
+  if (!c) return;
+  free(c->H); free(c->Hs); free(c->K); free(c->V); free(c->sal);
+  free(c->xk); free(c->xv); free(c->kc); free(c->vc);
+  free(c->ks32); free(c->kz); free(c->vs32); free(c->vz);
+  free(c->side_idx); free(c->side_cnt); free(c->side_pos);
+  free(c->s4c); free(c->s4s32); free(c->s4z);
+  free(c);
+}
+
+int orc_L(const orc_cache *c) { return c->L; }
+int orc_nq(const orc_cache *c) { return c->nq; }
+int orc_cap_rounded(const orc_cache *c) { return c->cap; }
+int orc_side_cap(const orc_cache *c) { return c->side_cap; }
+int orc_nthreads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+/* x.H_s of a stored 16-bit row, exact in fp64, then rounded once to fp32
+ * (the decision precision, R5/R6). */
+static void rotate_row_fp32(const orc_cache *c, const uint16_t *row, float *out) {
+  const int d = c->cfg.d;
+  double x[512], y[512];
+  for (int i = 0; i < d; ++i) x[i] = orc_half_to_double(row[i], c->cfg.dtype16);
+  matvec(d, c->Hs, x, y);
+  for (int i = 0; i < d; ++i) out[i] = (float)y[i];
+}
+
+/* Quantize block j = tokens [jG, (j+1)G) of unit u (R1):     */
+/*  K: per channel c over the block's non-salient tokens (2-bit, clip2). */
+/*  V: per token over G-channel groups (2-bit, clip2); salient tokens    */
+/*     get codes 0 and meta (0, 0).                                      */
+/*  Salient tokens enter the side table in ascending token order:        */
+/*   PSA -> original 16-bit rows;                            */
+/*   TSA -> 4-bit per-token groups of K.H_s and V.H_s, clip4.    */
+static void quantize_block(orc_cache *c, int u, int j) {
+  const int d = c->cfg.d, G = c->cfg.G, t0 = j * G;
+  for (int t = t0; t < t0 + G; ++t) {
+    rotate_row_fp32(c, c->K + ROW(c, u, t), c->xk + ROW(c, u, t));
+    rotate_row_fp32(c, c->V + ROW(c, u, t), c->xv + ROW(c, u, t));
+  }
+  const uint8_t *skip = c->sal + (long)u * c->cap + t0;
+  const long mb = ((long)u * (c->cap / G) + j) * d;
+  for (int ch = 0; ch < d; ++ch)           /* K per channel over G tokens */
+    orc_quantize_group(c->xk + ROW(c, u, t0) + ch, skip, G, d, 2, c->cfg.clip2,
+                       &c->ks32[mb + ch], &c->kz[mb + ch],
+                       c->kc + ROW(c, u, t0) + ch, d);
+  const int ng = d / G;
+  for (int t = t0; t < t0 + G; ++t) {      /* V per token over G channels */
+    const long vm = ((long)u * c->cap + t) * ng;
+    for (int gi = 0; gi < ng; ++gi) {
+      if (c->sal[(long)u * c->cap + t]) {
+        c->vs32[vm + gi] = 0.0f; c->vz[vm + gi] = 0;
+        memset(c->vc + ROW(c, u, t) + gi * G, 0, (size_t)G);
+      } else {
+        orc_quantize_group(c->xv + ROW(c, u, t) + gi * G, NULL, G, 1, 2,
+                           c->cfg.clip2, &c->vs32[vm + gi], &c->vz[vm + gi],
+                           c->vc + ROW(c, u, t) + gi * G, 1);
+      }
+    }
+  }
+  for (int t = t0; t < t0 + G; ++t) {      /* side table, ascending t */
+    if (!c->sal[(long)u * c->cap + t]) continue;
+    const int e = c->side_cnt[u]++;
+    c->side_idx[(long)u * c->side_cap + e] = t;
+    c->side_pos[(long)u * c->cap + t] = e;
+    if (c->cfg.kind == ORC_TSA) {
+      for (int kv = 0; kv < 2; ++kv) {
+        const float *x = (kv == 0 ? c->xk : c->xv) + ROW(c, u, t);
+        const long base = (((long)u * c->side_cap + e) * 2 + kv);
+        for (int gi = 0; gi < ng; ++gi)
+          orc_quantize_group(x + gi * G, NULL, G, 1, 4, c->cfg.clip4,
+                             &c->s4s32[base * ng + gi], &c->s4z[base * ng + gi],
+                             c->s4c + base * d + gi * G, 1);
+      }
+    }
+  }
+}
+
+/* Prefill: store rows, select salient tokens,     */
+/* quantize blocks [0, n_q) with n_q = G floor(max(0, L0 - R)/G) (R9).    */
+int orc_prefill(orc_cache *c, const uint16_t *K, const uint16_t *V, int L0,
+                const uint8_t *types, const float *colsum) {
+  const orc_config *f = &c->cfg;
+  if (c->L != 0) return ORC_ESTATE;
+  if (L0 < 0) return ORC_EINVAL;
+  if (L0 > f->capacity) return ORC_ECAPACITY;
+  if (f->kind == ORC_PSA && L0 > 0 && !colsum) return ORC_EINVAL;
+  if (f->kind == ORC_TSA && L0 > 0 && !types) return ORC_EINVAL;
+  const int d = f->d;
+  const int nq = L0 > f->R ? (L0 - f->R) / f->G * f->G : 0;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic)
+#endif
+  for (int u = 0; u < f->U; ++u) {
+    for (int t = 0; t < L0; ++t) {
+      memcpy(c->K + ROW(c, u, t), K + ((long)u * L0 + t) * d, (size_t)d * 2);
+      memcpy(c->V + ROW(c, u, t), V + ((long)u * L0 + t) * d, (size_t)d * 2);
+    }
+    orc_select_salient(f->kind, f->g, L0, f->top_k,
+                       types ? types + (long)u * L0 : NULL,
+                       colsum ? colsum + (long)u * f->g * L0 : NULL,
+                       c->sal + (long)u * c->cap);
+    for (int j = 0; j < nq / f->G; ++j) quantize_block(c, u, j);
+  }
+  c->L = L0;
+  c->nq = nq;
+  return ORC_OK;
+}
+
+/* Append one decode token per unit (Eq. 2).        */
+/* The new token enters the 16-bit recent window; in TSA layers a text    */
+/* token is salient.  When L - R - n_q >= G the oldest block      */
+/* leaves the window and is quantized exactly as prefill would.   */
+int orc_append(orc_cache *c, const uint16_t *k, const uint16_t *v,
+               const uint8_t *types) {
+  const orc_config *f = &c->cfg;
+  if (c->L >= f->capacity) return ORC_ECAPACITY;
+  const int d = f->d, t = c->L;
+  for (int u = 0; u < f->U; ++u) {
+    memcpy(c->K + ROW(c, u, t), k + (long)u * d, (size_t)d * 2);
+    memcpy(c->V + ROW(c, u, t), v + (long)u * d, (size_t)d * 2);
+    c->sal[(long)u * c->cap + t] =
+        (f->kind == ORC_TSA && types && types[u] == 1) ? 1 : 0;
+  }
+  c->L = t + 1;
+  if (c->L - f->R - c->nq >= f->G) {
+    const int j = c->nq / f->G;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic)
+#endif
+    for (int u = 0; u < f->U; ++u) quantize_block(c, u, j);
+    c->nq += f->G;
+  }
+  return ORC_OK;
+}
+
+/* Dequantized row of token t in the rotated normalized basis (Eq. 4).   */
+static void view_row(const orc_cache *c, int u, int t, double *Kh, double *Vh) {
+  const int d = c->cfg.d, G = c->cfg.G, ng = d / G;
+  const double rs = 1.0 / sqrt((double)d);   /* stored scale = scale/sqrt d */
+  const int sal = c->sal[(long)u * c->cap + t];
+  if (t >= c->nq || (sal && c->cfg.kind == ORC_PSA)) {
+    /* 16-bit tier (recent window / PSA pivots): original row . H */
+    double x[512];
+    for (int i = 0; i < d; ++i)
+      x[i] = orc_half_to_double(c->K[ROW(c, u, t) + i], c->cfg.dtype16);
+    matvec(d, c->H, x, Kh);
+    for (int i = 0; i < d; ++i)
+      x[i] = orc_half_to_double(c->V[ROW(c, u, t) + i], c->cfg.dtype16);
+    matvec(d, c->H, x, Vh);
+    return;
+  }
+  if (sal) {                                 /* TSA text token, 4-bit */
+    const int e = c->side_pos[(long)u * c->cap + t];
+    for (int kv = 0; kv < 2; ++kv) {
+      const long base = ((long)u * c->side_cap + e) * 2 + kv;
+      double *out = kv == 0 ? Kh : Vh;
+      for (int i = 0; i < d; ++i) {
+        const double s = (double)c->s4s32[base * ng + i / G] * rs;
+        out[i] = s * ((double)c->s4c[base * d + i] - (double)c->s4z[base * ng + i / G]);
+      }
+    }
+    return;
+  }
+  const int j = t / G;                       /* 2-bit tier */
+  const long mb = ((long)u * (c->cap / G) + j) * d;
+  const long vm = ((long)u * c->cap + t) * ng;
+  for (int i = 0; i < d; ++i) {
+    Kh[i] = (double)c->ks32[mb + i] * rs *
+            ((double)c->kc[ROW(c, u, t) + i] - (double)c->kz[mb + i]);
+    Vh[i] = (double)c->vs32[vm + i / G] * rs *
+            ((double)c->vc[ROW(c, u, t) + i] - (double)c->vz[vm + i / G]);
+  }
+}
+
+int orc_view(const orc_cache *c, double *K, double *V) {
+  const int d = c->cfg.d, L = c->L;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic)
+#endif
+  for (int u = 0; u < c->cfg.U; ++u)
+    for (int t = 0; t < L; ++t)
+      view_row(c, u, t, K + ((long)u * L + t) * d, V + ((long)u * L + t) * d);
+  return ORC_OK;
+}
+
+/* Decode attention for one query per head: with q~ = q.H,     */
+/*   s_t = q~ . K^_t / sqrt(d),  p = softmax(s),  o' = sum_t p_t V^_t,      */
+/*   o = o' . H   (H symmetric orthonormal, so H^-1 = H; Fig. 7).    */
+/* GQA: the g query heads of unit u all read unit u's cache.        */
+int orc_decode(const orc_cache *c, const uint16_t *q, double *out,
+               int out_rotated, int unit_lo, int unit_hi) {
+  const orc_config *f = &c->cfg;
+  const int d = f->d, g = f->g, L = c->L;
+  if (L == 0) return ORC_ESTATE;
+  if (unit_lo < 0) unit_lo = 0;
+  if (unit_hi > f->U || unit_hi < 0) unit_hi = f->U;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic)
+#endif
+  for (int u = unit_lo; u < unit_hi; ++u) {
+    double *Kh = (double *)malloc(sizeof(double) * L * d);
+    double *Vh = (double *)malloc(sizeof(double) * L * d);
+    double *s = (double *)malloc(sizeof(double) * L);
+    double qx[512], qt[512], o[512];
+    for (int t = 0; t < L; ++t) view_row(c, u, t, Kh + (long)t * d, Vh + (long)t * d);
+    for (int h = 0; h < g; ++h) {
+      const uint16_t *qr = q + ((long)u * g + h) * d;
+      for (int i = 0; i < d; ++i) qx[i] = orc_half_to_double(qr[i], f->dtype16);
+      matvec(d, c->H, qx, qt);                              /* q~ = q.H */
+      double m = -INFINITY;
+      for (int t = 0; t < L; ++t) {
+        double a = 0.0;
+        for (int i = 0; i < d; ++i) a += qt[i] * Kh[(long)t * d + i];
+        s[t] = a / sqrt((double)d);
+        if (s[t] > m) m = s[t];
+      }
+      double Z = 0.0;
+      for (int t = 0; t < L; ++t) { s[t] = exp(s[t] - m); Z += s[t]; }
+      for (int i = 0; i < d; ++i) o[i] = 0.0;
+      for (int t = 0; t < L; ++t) {
+        const double p = s[t] / Z;
+        for (int i = 0; i < d; ++i) o[i] += p * Vh[(long)t * d + i];
+      }
+      double *dst = out + ((long)u * g + h) * d;
+      if (out_rotated) memcpy(dst, o, sizeof(double) * d);
+      else matvec(d, c->H, o, dst);                          /* o = o'.H */
+    }
+    free(Kh); free(Vh); free(s);
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ */
+int orc_export(const orc_cache *c, const orc_export_t *ex) {
+  const orc_config *f = &c->cfg;
+  const long U = f->U, cap = c->cap, d = f->d, G = f->G, ng = d / G;
+  const long sc = c->side_cap;
+  const double rs = 1.0 / sqrt((double)d);
+  for (long u = 0; u < U; ++u) {
+    for (long t = 0; t < cap; ++t) {
+      if (ex->kcodes) orc_pack(c->kc + ROW(c, (int)u, (int)t), (int)d, 2, ex->kcodes + (u * cap + t) * (d / 4));
+      if (ex->vcodes) orc_pack(c->vc + ROW(c, (int)u, (int)t), (int)d, 2, ex->vcodes + (u * cap + t) * (d / 4));
+      if (ex->salient) ex->salient[u * cap + t] = c->sal[u * cap + t];
+    }
+    if (ex->side_count) ex->side_count[u] = c->side_cnt[u];
+    for (long e = 0; e < sc; ++e) {
+      const int have = e < c->side_cnt[u];
+      const int t = have ? c->side_idx[u * sc + e] : -1;
+      if (ex->side_index) ex->side_index[u * sc + e] = t;
+      if (ex->side16) {
+        uint16_t *dst = ex->side16 + (u * sc + e) * 2 * d;
+        if (have) {
+          memcpy(dst, c->K + ROW(c, (int)u, t), (size_t)d * 2);
+          memcpy(dst + d, c->V + ROW(c, (int)u, t), (size_t)d * 2);
+        } else {
+          memset(dst, 0, (size_t)d * 4);
+        }
+      }
+      for (int kv = 0; kv < 2; ++kv) {
+        const long base = (u * sc + e) * 2 + kv;
+        if (ex->side4) orc_pack(c->s4c + base * d, (int)d, 4, ex->side4 + base * (d / 2));
+        for (long gi = 0; gi < ng; ++gi) {
+          if (ex->side4_scale) ex->side4_scale[base * ng + gi] = (double)c->s4s32[base * ng + gi] * rs;
+          if (ex->side4_zero) ex->side4_zero[base * ng + gi] = c->s4z[base * ng + gi];
+        }
+      }
+    }
+  }
+  const long nk = U * (cap / G) * d, nv = U * cap * ng;
+  for (long i = 0; i < nk; ++i) {
+    if (ex->kscale) ex->kscale[i] = (double)c->ks32[i] * rs;
+    if (ex->kscale32) ex->kscale32[i] = c->ks32[i];
+    if (ex->kzero) ex->kzero[i] = c->kz[i];
+  }
+  for (long i = 0; i < nv; ++i) {
+    if (ex->vscale) ex->vscale[i] = (double)c->vs32[i] * rs;
+    if (ex->vscale32) ex->vscale32[i] = c->vs32[i];
+    if (ex->vzero) ex->vzero[i] = c->vz[i];
+  }
+  if (ex->xs_k) memcpy(ex->xs_k, c->xk, sizeof(float) * U * cap * d);
+  if (ex->xs_v) memcpy(ex->xs_v, c->xv, sizeof(float) * U * cap * d);
+  return ORC_OK;
+}

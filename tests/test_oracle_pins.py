@@ -1,0 +1,451 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+Each test checks the oracle against something OTHER than itself: a value the
+paper prints (Eq. 7), a SPEC worked example (tests/golden/spec_examples.json,
+each with its citation), a closed form, an invariant, a library routine
+(scipy.linalg.hadamard, torch SDPA in fp64) or brute force on tiny inputs.
+A plausible mistake in the oracle -- a dropped term, a wrong sign or index, a
+transposed operand, a mis-rounded code -- fails at least one of them.
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg
+import torch
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _spec():
+    with open(os.path.join(GOLD, "spec_examples.json")) as f:
+        return json.load(f)
+
+
+def _f16_bits(x):
+    return np.asarray(x, np.float16).view(np.uint16)
+
+
+def _bf16_bits(x):
+    t = torch.tensor(np.asarray(x, np.float32)).to(torch.bfloat16)
+    return t.view(torch.int16).numpy().view(np.uint16)
+
+
+# ------------------------------------------------------------------ Eq. 7
+def test_h1_and_h2_as_printed(orc):
+    assert np.array_equal(orc.hadamard(1), np.array([[1.0]]))          # H_1 = [1]
+    rows = [list(map(float, l.split())) for l in open(os.path.join(GOLD, "eq7_hadamard_h2.txt"))
+            if l.strip() and not l.startswith("#")]
+    H2 = np.array(rows) / math.sqrt(2.0)
+    assert np.abs(orc.hadamard(2) - H2).max() <= 1e-15
+
+
+@pytest.mark.parametrize("d", [2, 4, 8, 16, 32, 64, 128, 256, 512])
+def test_hadamard_closed_form_and_library(orc, d):
+    H = orc.hadamard(d)
+    Hs = orc.hadamard(d, normalized=False)
+    i = np.arange(d)
+    pop = np.vectorize(lambda v: bin(int(v)).count("1"))(i[:, None] & i[None, :])
+    closed = (-1.0) ** pop
+    assert np.array_equal(Hs, closed)                                  # (-1)^popcount(i&j)
+    assert np.array_equal(Hs, scipy.linalg.hadamard(d).astype(np.float64))
+    assert np.abs(H * math.sqrt(d) - Hs).max() <= 1e-12
+    assert np.abs(H @ H.T - np.eye(d)).max() <= 1e-12                  # H H^T = I
+    assert np.abs(Hs @ Hs.T - d * np.eye(d)).max() <= 1e-9             # H_s H_s^T = d I (BJ:5)
+    assert np.abs(H @ H - np.eye(d)).max() <= 1e-12                    # involution
+
+
+def test_rotate_worked_examples(orc):
+    # d = 4, x = [1,2,3,4]: x.H = [5, -1, -2, 0] (exact arithmetic).
+    assert np.abs(orc.rotate([1, 2, 3, 4]) - [5, -1, -2, 0]).max() <= 1e-12
+    ex = _spec()["fwht"][0]
+    assert np.abs(orc.rotate(ex["x"]) * math.sqrt(2) - ex["y_times_sqrt_d"]).max() <= 1e-12
+    for d in (8, 64, 128):                                             # one-hot
+        for j in (0, d // 3, d - 1):
+            e = np.zeros(d); e[j] = 3.5
+            y = orc.rotate(e)
+            assert np.abs(np.abs(y) - 3.5 / math.sqrt(d)).max() <= 1e-12
+
+
+def test_rotation_invariants(orc):
+    rng = np.random.default_rng(0)
+    for d in (16, 64, 128):
+        q, k = rng.normal(size=d), rng.normal(size=d)
+        qt, kt = orc.rotate(q), orc.rotate(k)
+        assert abs(np.dot(qt, kt) - np.dot(q, k)) <= 1e-10            # q~.k~ = q.k
+        assert abs(np.linalg.norm(qt) - np.linalg.norm(q)) <= 1e-10   # energy
+        assert np.abs(orc.rotate(qt) - q).max() <= 1e-12              # invertible
+        # explicit matrix vs the library Hadamard
+        assert np.abs(orc.rotate(q, normalized=False) - q @ scipy.linalg.hadamard(d)).max() <= 1e-9
+
+
+def test_rotation_reduces_channel_outliers(orc):
+    # Fig. 5 analogue: one-hot channel -> uniform; hot channels spread.
+    rng = np.random.default_rng(1)
+    d = 128
+    X = rng.normal(size=(64, d)); X[:, [3, 17]] *= 20
+    Y = np.stack([orc.rotate(x) for x in X])
+    ratio = lambda T: np.abs(T).mean(0).max() / np.abs(T).mean(0).mean()
+    assert ratio(Y) < ratio(X)
+
+
+# ------------------------------------------------------------------ Eqs. 3-6
+def test_quantizer_spec_examples(orc):
+    for ex in _spec()["quantize"]:
+        s, z, c = orc.quantize_group(ex["x"], ex["bits"], ex["clip"])
+        assert s == pytest.approx(ex["scale"], rel=1e-7), ex["cite"]
+        assert z == ex["zero"], ex["cite"]
+        assert c.tolist() == ex["codes"], ex["cite"]
+
+
+def test_clipped_range_via_scale(orc):
+    # clipped range of [-10, 4] is (-10, 4) at 1.0 and (-8, 3.2) at 0.8;
+    # Eq. 5 then gives scale = (max - min) / 3 for 2 bits.
+    for ex in _spec()["clipped_range"]:
+        s, z, _ = orc.quantize_group(ex["x"], 2, ex["clip"])
+        assert s * 3 == pytest.approx(ex["max"] - ex["min"], rel=1e-6), ex["cite"]
+        assert z == -round(ex["min"] / ((ex["max"] - ex["min"]) / 3))
+
+
+def test_quantizer_hand_worked(orc):
+    # on-grid: scale is a power of two, zero an integer -> exact reconstruction.
+    x = [-0.5, 0, 0.5, 1, 1, -0.5, 0.5, 0]
+    s, z, c = orc.quantize_group(x, 2, 1.0)
+    assert (s, z, c.tolist()) == (0.5, 1, [0, 1, 2, 3, 3, 0, 2, 1])
+    assert np.array_equal(s * (c.astype(np.float64) - z), np.asarray(x, np.float64))
+    # clip 0.8, no ties: scale 32/15, zero 1 (cmn/scale = -1.125), codes [0,1,1,2,3].
+    s, z, c = orc.quantize_group([-3, -1, 0.25, 2, 5], 2, 0.8)
+    assert s == pytest.approx(32 / 15, rel=1e-6) and z == 1 and c.tolist() == [0, 1, 1, 2, 3]
+    # a skipped (salient) element is excluded from the statistics and coded 0.
+    s2, z2, c2 = orc.quantize_group([-3, -1, 100.0, 2, 5], 2, 0.8, skip=[0, 0, 1, 0, 0])
+    assert (s2, z2) == (s, z) and c2.tolist() == [0, 1, 0, 2, 3]
+    # all skipped: empty group -> (0, 0), codes 0.
+    s3, z3, c3 = orc.quantize_group([1.0, 2.0], 2, 0.8, skip=[1, 1])
+    assert (s3, z3, c3.tolist()) == (0.0, 0, [0, 0])
+
+
+@pytest.mark.parametrize("bits,clip", [(2, 0.8), (2, 1.0), (4, 0.8), (4, 1.0)])
+def test_quantizer_brute_force_and_bounds(orc, bits, clip):
+    """brute-force nearest code, error <= scale/2, monotone."""
+    rng = np.random.default_rng(bits * 10 + int(clip * 10))
+    levels = (1 << bits) - 1
+    for _ in range(300):
+        x = rng.uniform(-1, 1, size=128).astype(np.float32) * rng.uniform(0.1, 10)
+        s, z, c = orc.quantize_group(x, bits, clip)
+        assert c.max() <= levels
+        # brute force over every code q: argmin |x - s (q - z)|, ties -> even rounding
+        # of x/s (checked by excluding exact half-way points, which random data avoids)
+        grid = s * (np.arange(levels + 1)[None, :] - z)
+        best = np.abs(x.astype(np.float64)[:, None] - grid).argmin(1)
+        assert np.array_equal(best, c)
+        xr = s * (c.astype(np.float64) - z)
+        inclip = (x >= clip * x.min()) & (x <= clip * x.max())
+        assert np.all(np.abs(x[inclip] - xr[inclip]) <= s / 2 + 1e-6)
+        o = np.argsort(x, kind="stable")
+        assert np.all(np.diff(c[o].astype(int)) >= 0)
+
+
+def test_pack_examples_and_roundtrip(orc):
+    for ex in _spec()["pack"]:
+        assert orc.pack(ex["codes"], ex["bits"]).tolist() == ex["bytes"], ex["cite"]
+    assert orc.pack([0, 1, 1, 2], 2).tolist() == [0x94]
+    rng = np.random.default_rng(3)
+    for bits in (2, 4):
+        c = rng.integers(0, 1 << bits, size=1000).astype(np.uint8)
+        assert np.array_equal(orc.unpack(orc.pack(c, bits), 1000, bits), c)
+
+
+def test_half_decoding(orc):
+    vals = np.array([0.0, 1.0, -2.5, 65504.0, 6.1e-5, 5.96e-8, -1e-3], np.float16)
+    for v, b in zip(vals, vals.view(np.uint16)):
+        assert orc.half_to_double(int(b), orc.FP16) == float(v)
+    vb = np.array([1.0, -3.140625, 1e30, 1e-30], np.float32)
+    for v, b in zip(torch.tensor(vb).to(torch.bfloat16).float().numpy(), _bf16_bits(vb)):
+        assert orc.half_to_double(int(b), orc.BF16) == float(v)
+
+
+# ------------------------------------------------------------------ saliency
+def test_saliency_examples(orc):
+    cs = np.array([[0.1, 0.3, 0.3, 0.2]], np.float32)
+    assert np.flatnonzero(orc.select_salient(orc.PSA, colsum=cs, top_k=2)).tolist() == [1, 2]
+    assert np.flatnonzero(orc.select_salient(orc.PSA, colsum=cs, top_k=1)).tolist() == [1]
+    assert np.flatnonzero(orc.select_salient(orc.TSA, types=[1, 0, 0, 1])).tolist() == [0, 3]
+    # g > 1: scores are summed over the query heads of the unit
+    cs2 = np.array([[0.5, 0.0, 0.1], [0.0, 0.6, 0.1]], np.float32)
+    assert np.flatnonzero(orc.select_salient(orc.PSA, colsum=cs2, top_k=1)).tolist() == [1]
+    # k >= L0 selects everything
+    assert orc.select_salient(orc.PSA, colsum=cs, top_k=9).tolist() == [1, 1, 1, 1]
+
+
+def test_saliency_brute_force(orc):
+    """The selected set is the unique k-subset whose members all precede every
+    non-member in the order (score desc, index asc): checked over all subsets."""
+    rng = np.random.default_rng(4)
+    for trial in range(200):
+        L0, k = 8, int(rng.integers(1, 5))
+        sc = rng.integers(0, 4, size=(1, L0)).astype(np.float32)       # many ties
+        got = set(np.flatnonzero(orc.select_salient(orc.PSA, colsum=sc, top_k=k)))
+        wins = []
+        for sub in itertools.combinations(range(L0), k):
+            ok = all((sc[0, a] > sc[0, b]) or (sc[0, a] == sc[0, b] and a < b)
+                     for a in sub for b in range(L0) if b not in sub)
+            if ok:
+                wins.append(set(sub))
+        assert wins == [got]
+
+
+# ------------------------------------------------------------------ the cache
+def _cfg(orc, **kw):
+    base = dict(U=1, g=1, d=4, G=4, R=0, capacity=16, top_k=1, kind=orc.PSA,
+                dtype16=orc.FP16)
+    base.update(kw)
+    return orc.OracleConfig(**base)
+
+
+def _rows_with_rotation(target):
+    """fp16 rows K such that K.H_s = target exactly (H_s H_s = d I)."""
+    target = np.asarray(target, np.float64)
+    d = target.shape[-1]
+    K = target @ scipy.linalg.hadamard(d) / d
+    assert np.array_equal(K.astype(np.float16).astype(np.float64), K)
+    return _f16_bits(K)
+
+
+def test_per_channel_block_hand_worked(orc):
+    """G = 4 tokens, d = 4, 2-bit, clip 1.0 (pre-rotated targets)."""
+    # channel 0 = [0,1,2,3] -> (1,0,[0,1,2,3]); channel 1 = -1 const -> degenerate
+    # (-1, 0, 1); channels 2,3 = 0 -> degenerate (0, 0, 1).
+    Xs = np.array([[0, -1, 0, 0], [1, -1, 0, 0], [2, -1, 0, 0], [3, -1, 0, 0]], float)
+    K = _rows_with_rotation(Xs)[None]
+    for sal_tok in (None, 2):
+        c = orc.OracleCache(_cfg(orc, clip2=1.0, kind=orc.PSA,
+                                 top_k=0 if sal_tok is None else 1))
+        cs = np.zeros((1, 1, 4), np.float32)
+        if sal_tok is not None:
+            cs[0, 0, sal_tok] = 1.0
+        assert c.prefill(K, K, colsum=cs) == 0 and c.nq == 4
+        e = c.export()
+        assert np.allclose(e["kscale32"][0, 0], [1, -1, 0, 0]) and e["kzero"][0, 0].tolist() == [0] * 4
+        kb = e["kcodes"][0, :4, 0].tolist()
+        # byte of token t = code(ch0) | code(ch1) << 2 | code(ch2) << 4 | code(ch3) << 6
+        exp = [t | (1 << 2) | (1 << 4) | (1 << 6) for t in range(4)]
+        if sal_tok is not None:
+            exp[sal_tok] = 0
+            assert e["side_index"][0].tolist() == [sal_tok]
+            assert np.array_equal(e["side16"][0, 0, 0], K[0, sal_tok])
+        assert kb == exp
+        # stored (normalized) scale = decision scale / sqrt(d)
+        assert np.allclose(e["kscale"][0, 0], np.array([1, -1, 0, 0]) / 2)
+
+
+def test_tier_rule_examples(orc):
+    """S:332-333 tier examples, with G chosen so the block boundary equals L - R."""
+    L, R, d, G = 300, 128, 4, 4
+    rng = np.random.default_rng(5)
+    K = _f16_bits(rng.normal(size=(1, L, d)))
+    types = np.zeros((1, L), np.uint8); types[0, :100] = 1
+    c = orc.OracleCache(_cfg(orc, R=R, capacity=L, kind=orc.TSA))
+    assert c.prefill(K, K, types=types) == 0
+    assert c.nq == 172                                                 # 172..299 16-bit
+    e = c.export()
+    assert e["side_count"][0] == 100 and e["side_index"][0, :100].tolist() == list(range(100))
+    c2 = orc.OracleCache(_cfg(orc, R=R, capacity=L, kind=orc.PSA, top_k=2))
+    cs = np.full((1, 1, L), 1e-3, np.float32); cs[0, 0, [0, 57]] = 0.5
+    assert c2.prefill(K, K, colsum=cs) == 0
+    e2 = c2.export()
+    assert e2["side_index"][0].tolist() == [0, 57] and c2.nq == 172
+
+
+def test_schedule_boundaries(orc):
+    # tiny (BJ:7): n_q = 64 at L0 = 96 (G 32, R 8); flush at L = 104 -> 96.
+    c = orc.OracleCache(_cfg(orc, d=64, G=32, R=8, capacity=120, top_k=4))
+    rng = np.random.default_rng(6)
+    K = _f16_bits(rng.normal(size=(1, 96, 64)))
+    cs = rng.random((1, 1, 96)).astype(np.float32)
+    assert c.prefill(K, K, colsum=cs) == 0 and c.nq == 64
+    for L in range(97, 106):
+        k = _f16_bits(rng.normal(size=(1, 64)))
+        c.append(k, k)
+        assert c.L == L and c.nq == (96 if L >= 104 else 64)
+    # 7B (BJ:8): n_q = 512 at L0 = 671 (G 128, R 32); 640 at 672; next flush at 800.
+    c = orc.OracleCache(_cfg(orc, d=128, G=128, R=32, capacity=801, top_k=15,
+                             dtype16=orc.BF16))
+    K = _bf16_bits(rng.normal(size=(1, 671, 128)))
+    assert c.prefill(K, K, colsum=rng.random((1, 1, 671)).astype(np.float32)) == 0
+    assert c.nq == 512
+    k = _bf16_bits(rng.normal(size=(1, 128)))
+    for L in range(672, 802):
+        c.append(k, k)
+        assert c.nq == (512 if L < 672 else 640 if L < 800 else 768)
+    assert c.append(k, k) != 0 and c.L == 801                          # capacity error
+
+
+def test_prefill_equals_incremental_append(orc):
+    """prefill of T tokens == appending them one at a time (bit-exact)."""
+    rng = np.random.default_rng(7)
+    for kind in (orc.PSA, orc.TSA):
+        L0, d = 200, 64
+        K = _f16_bits(rng.normal(size=(2, L0, d)) * np.where(np.arange(d) == 5, 20, 1))
+        V = _f16_bits(rng.normal(size=(2, L0, d)))
+        types = (rng.random((2, L0)) < 0.3).astype(np.uint8)
+        cfg = _cfg(orc, U=2, d=d, G=32, R=16, capacity=L0, kind=kind, top_k=3)
+        a = orc.OracleCache(cfg)
+        a.prefill(K, V, types=types, colsum=np.zeros((2, 1, L0), np.float32) + 1)
+        b = orc.OracleCache(cfg)
+        b.prefill(K[:, :0], V[:, :0], types=types[:, :0], colsum=np.zeros((2, 1, 0), np.float32))
+        for t in range(L0):
+            b.append(K[:, t], V[:, t], types[:, t])
+        if kind == orc.PSA:            # pivots exist only for prompt tokens
+            continue
+        ea, eb = a.export(), b.export()
+        assert a.nq == b.nq and a.L == b.L
+        for key in ea:
+            assert np.array_equal(ea[key], eb[key]), key
+
+
+def test_region_partition_and_view_bounds(orc):
+    """Region partition, dequant error <= scale/2 (north_star), on-grid exact."""
+    rng = np.random.default_rng(8)
+    U, L0, d, G, R = 3, 150, 64, 32, 20
+    K = _f16_bits(rng.normal(size=(U, L0, d)))
+    V = _f16_bits(rng.normal(size=(U, L0, d)))
+    cfg = _cfg(orc, U=U, d=d, G=G, R=R, capacity=L0, kind=orc.PSA, top_k=4, clip2=1.0)
+    c = orc.OracleCache(cfg)
+    c.prefill(K, V, colsum=rng.random((U, 1, L0)).astype(np.float32))
+    e = c.export()
+    Kh, Vh = c.view()
+    H = scipy.linalg.hadamard(d) / math.sqrt(d)
+    Kf = K.view(np.float16).astype(np.float64) @ H
+    Vf = V.view(np.float16).astype(np.float64) @ H
+    nq = c.nq
+    assert nq == 128
+    for u in range(U):
+        sal = e["salient"][u, :L0].astype(bool)
+        assert sal.sum() == 4 and e["side_count"][u] == (sal[:nq]).sum()
+        # 16-bit tiers reproduce the input exactly (up to the fp64 rotation)
+        exact = np.zeros(L0, bool); exact[nq:] = True; exact[:nq] |= sal[:nq]
+        assert np.abs(Kh[u][exact] - Kf[u][exact]).max() <= 1e-12
+        # 2-bit tier: |x - x'| <= scale/2 with clip 1.0 (every element in-clip)
+        q = ~exact
+        ks = np.repeat(e["kscale"][u, : nq // G], G, axis=0)[:nq]
+        assert np.all(np.abs(Kh[u][q] - Kf[u][q]) <= ks[q[:nq]] / 2 * (1 + 1e-6) + 1e-12)
+        vs = np.repeat(e["vscale"][u, :nq], G, axis=1)
+        assert np.all(np.abs(Vh[u][q] - Vf[u][q]) <= vs[q[:nq]] / 2 * (1 + 1e-6) + 1e-12)
+    # inputs on the quantization grid reconstruct exactly: two-level channels
+    Xs = np.zeros((1, 32, 32)); Xs[0, :, :] = np.where(rng.random((32, 32)) < 0.5, 2.0, -1.0)
+    Xs[0, 0, :] = 2.0; Xs[0, 1, :] = -1.0         # every channel sees both levels
+    Kg = _rows_with_rotation(Xs)
+    cg = orc.OracleCache(_cfg(orc, d=32, G=32, R=0, capacity=32, top_k=0, clip2=1.0))
+    cg.prefill(Kg, Kg, colsum=np.zeros((1, 1, 32), np.float32))
+    Kh, _ = cg.view()
+    assert np.abs(Kh[0] - Xs[0] / math.sqrt(32)).max() <= 1e-12
+
+
+def _sdpa64(q, K, V):
+    return torch.nn.functional.scaled_dot_product_attention(
+        torch.tensor(q)[None, None], torch.tensor(K)[None, None], torch.tensor(V)[None, None]
+    )[0, 0].numpy()
+
+
+def test_decode_special_cases(orc):
+    rng = np.random.default_rng(9)
+    d = 64
+    # single cached token -> output = v
+    c = orc.OracleCache(_cfg(orc, d=d, G=32, R=8, capacity=8))
+    k = _f16_bits(rng.normal(size=(1, 1, d))); v = _f16_bits(rng.normal(size=(1, 1, d)))
+    c.prefill(k, v, colsum=np.ones((1, 1, 1), np.float32))
+    q = _f16_bits(rng.normal(size=(1, 1, d)))
+    out = c.decode(q)
+    assert np.abs(out[0, 0] - v[0, 0].view(np.float16)).max() <= 1e-12
+    # identical keys -> mean of values
+    c = orc.OracleCache(_cfg(orc, d=d, G=32, R=8, capacity=8))
+    K = np.repeat(k, 5, axis=1); V = _f16_bits(rng.normal(size=(1, 5, d)))
+    c.prefill(K, V, colsum=np.ones((1, 1, 5), np.float32))
+    assert np.abs(c.decode(q)[0, 0] - V[0].view(np.float16).astype(np.float64).mean(0)).max() <= 1e-12
+    # 2-token closed form
+    c = orc.OracleCache(_cfg(orc, d=d, G=32, R=8, capacity=8))
+    K2 = _f16_bits(rng.normal(size=(1, 2, d))); V2 = _f16_bits(rng.normal(size=(1, 2, d)))
+    c.prefill(K2, V2, colsum=np.ones((1, 1, 2), np.float32))
+    qf = q[0, 0].view(np.float16).astype(np.float64)
+    Kf, Vf = K2[0].view(np.float16).astype(np.float64), V2[0].view(np.float16).astype(np.float64)
+    s = Kf @ qf / math.sqrt(d)
+    p1 = 1.0 / (1.0 + math.exp(s[0] - s[1]))
+    assert np.abs(c.decode(q)[0, 0] - ((1 - p1) * Vf[0] + p1 * Vf[1])).max() <= 1e-12
+
+
+def test_decode_unquantized_matches_library_sdpa(orc):
+    """R >= L: nothing is quantized -> output = SDPA on the original rows (torch fp64),
+    which also pins the rotation equivalence q~.k~ = q.k and o = o'.H (Figs. 6-7)."""
+    rng = np.random.default_rng(10)
+    U, g, d, L0 = 2, 3, 64, 40
+    K = _bf16_bits(rng.normal(size=(U, L0, d))); V = _bf16_bits(rng.normal(size=(U, L0, d)))
+    c = orc.OracleCache(_cfg(orc, U=U, g=g, d=d, G=32, R=64, capacity=64, top_k=4,
+                             dtype16=orc.BF16))
+    c.prefill(K, V, colsum=rng.random((U, g, L0)).astype(np.float32))
+    q = _bf16_bits(rng.normal(size=(U, g, d)))
+    out = c.decode(q)
+    f = lambda a: torch.tensor(a.view(np.int16)).view(torch.bfloat16).double().numpy()
+    for u in range(U):
+        ref = _sdpa64(f(q[u]), f(K[u]), f(V[u]))
+        assert np.abs(out[u] - ref).max() <= 1e-12
+    outr = c.decode(q, out_rotated=True)
+    H = scipy.linalg.hadamard(d) / math.sqrt(d)
+    assert np.abs(outr @ H - out).max() <= 1e-12
+
+
+def test_decode_quantized_matches_library_sdpa_on_view(orc):
+    """With quantization: decode == SDPA(q.H, view K^, view V^) . H, using scipy's H
+    and torch's SDPA -- and outputs lie in the per-channel [min, max] of V^."""
+    rng = np.random.default_rng(11)
+    U, g, d, L0 = 2, 2, 64, 200
+    K = _f16_bits(rng.normal(size=(U, L0, d)) * np.where(np.arange(d) % 17 == 3, 20, 1))
+    V = _f16_bits(rng.normal(size=(U, L0, d)))
+    types = (rng.random((U, L0)) < 0.2).astype(np.uint8)
+    H = scipy.linalg.hadamard(d) / math.sqrt(d)
+    for kind in (orc.PSA, orc.TSA):
+        c = orc.OracleCache(_cfg(orc, U=U, g=g, d=d, G=32, R=24, capacity=L0, kind=kind,
+                                 top_k=4))
+        c.prefill(K, V, types=types, colsum=rng.random((U, g, L0)).astype(np.float32))
+        q = _f16_bits(rng.normal(size=(U, g, d)))
+        out = c.decode(q, out_rotated=True)
+        Kh, Vh = c.view()
+        for u in range(U):
+            qt = q[u].view(np.float16).astype(np.float64) @ H
+            ref = _sdpa64(qt, Kh[u], Vh[u])
+            assert np.abs(out[u] - ref).max() <= 1e-12
+            assert np.all(out[u] <= Vh[u].max(0) + 1e-12) and np.all(out[u] >= Vh[u].min(0) - 1e-12)
+
+
+def test_decode_error_and_degenerate_states(orc):
+    c = orc.OracleCache(_cfg(orc))
+    with pytest.raises(RuntimeError):
+        c.decode(np.zeros((1, 1, 4), np.uint16))                      # L == 0 -> ESTATE
+    assert c.prefill(np.zeros((1, 17, 4), np.uint16), np.zeros((1, 17, 4), np.uint16),
+                     colsum=np.zeros((1, 1, 17), np.float32)) != 0      # > capacity
+    # all-zero cache: every group degenerate at 0, output 0
+    c = orc.OracleCache(_cfg(orc, capacity=16))
+    z = np.zeros((1, 16, 4), np.uint16)
+    assert c.prefill(z, z, colsum=np.zeros((1, 1, 16), np.float32)) == 0
+    assert np.array_equal(c.decode(np.zeros((1, 1, 4), np.uint16)), np.zeros((1, 1, 4)))
+    with pytest.raises(ValueError):
+        orc.OracleCache(_cfg(orc, d=6))
+
+
+def test_codes_are_scale_invariant(orc):
+    """Reading R5: Eqs. 3,5,6 are homogeneous in X, so quantizing x.H_s (exact sums of
+    16-bit inputs) gives the codes of x.H = x.H_s/sqrt(d); only round-half ties can
+    differ, and those are excluded here by construction (|frac - 1/2| > 1e-4)."""
+    rng = np.random.default_rng(12)
+    for _ in range(500):
+        x = rng.normal(size=128).astype(np.float32)
+        s1, z1, c1 = orc.quantize_group(x, 2, 0.8)
+        xn = (x.astype(np.float64) / math.sqrt(128)).astype(np.float32)
+        s2, z2, c2 = orc.quantize_group(xn, 2, 0.8)
+        fr = np.abs(np.mod(x / s1, 1.0) - 0.5)
+        frz = abs((0.8 * x.min() / s1) % 1.0 - 0.5)
+        if fr.min() > 1e-4 and frz > 1e-4:
+            assert z1 == z2 and np.array_equal(c1, c2)
+            assert s2 == pytest.approx(s1 / math.sqrt(128), rel=1e-6)
