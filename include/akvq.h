@@ -1,0 +1,219 @@
+/*
+ * akvq.h -- C ABI of libakvq.so, the B200 (sm_100a) hot path of AKVQ-VL
+ * (arXiv 2501.15021): Walsh-Hadamard rotation, attention-aware saliency,
+ * 2-bit group quantize-and-pack of one attention layer's KV cache, and
+ * single-query decode attention that reads the packed cache directly.
+ *
+ * Citation keys: P:n = PAPER.md line n, S:n = SPEC.md line n, BJ:n =
+ * BASELINE.json line n; R1..R20 = DESIGN.md section 2 readings.
+ *
+ * Conventions shared by every call
+ *  - Plain C types only.  Pointers named dev_* / K, V, q, out, ws, types,
+ *    colsum are DEVICE pointers (cudaMalloc / torch CUDA storage) unless the
+ *    comment says host.  akvq_config, akvq_cache and akvq_mem_report are
+ *    HOST structs owned by the caller.
+ *  - Every call is asynchronous on the caller's stream (akvq_stream_t is the
+ *    CUDA runtime's cudaStream_t; NULL = legacy default stream).  The
+ *    library never allocates device memory and never synchronizes; the
+ *    caller owns every buffer.  Asynchronous faults surface at the caller's
+ *    next synchronization.
+ *  - Errors are returned, never thrown.  Argument/state errors are detected
+ *    on the host BEFORE any work is enqueued and leave the cache unchanged.
+ *    AKVQ_ECUDA reports cudaGetLastError() after a launch.
+ *  - A cache is single-writer: calls on one cache must be
+ *    ordered (same stream or explicit events).  Distinct caches are
+ *    independent.  Sharding across GPUs is invisible to the library: each
+ *    rank builds caches for its own unit range.
+ *  - Units: u = b * n_kv_heads + h (b-major).  All per-unit arrays are
+ *    row-major with the unit index outermost.
+ */
+#ifndef AKVQ_H
+#define AKVQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+struct CUstream_st;
+typedef struct CUstream_st *akvq_stream_t;   /* == cudaStream_t */
+
+typedef enum {
+  AKVQ_OK = 0,
+  AKVQ_EINVAL = 1,        /* bad argument: NULL pointer, non-power-of-two d/G,
+                             clip outside (0,1], negative sizes */
+  AKVQ_EUNSUPPORTED = 2,  /* valid per the paper but not built: d not in
+                             {64,128}; G not in {32,64,128} or G > d; top_k > 32;
+                             PSA prompt longer than AKVQ_MAX_PSA_PROMPT         */
+  AKVQ_ECAPACITY = 3,     /* buffer/workspace too small, L0 > capacity,
+                             append at L == capacity                            */
+  AKVQ_ESTATE = 4,        /* prefill on a non-empty cache, decode or
+                             view on an empty cache                             */
+  AKVQ_ECUDA = 5          /* a CUDA launch failed (cudaGetLastError)            */
+} akvq_status;
+
+typedef enum { AKVQ_TSA = 0, AKVQ_PSA = 1 } akvq_kind;        /* Table I */
+typedef enum { AKVQ_BF16 = 0, AKVQ_FP16 = 1 } akvq_dtype16;   /* R13 */
+
+/* decode flags */
+#define AKVQ_OUT_ROTATED 1u     /* return o' = sum p V^ in the rotated basis
+                                   (caller folded H into W_O, R4)      */
+
+#define AKVQ_MAX_PSA_PROMPT 49152   /* PSA top-k keeps the prompt's scores in
+                                       shared memory (192 KB)                 */
+
+/* One layer's cache configuration.  Per-channel K / per-token V (R1). */
+typedef struct {
+  int32_t n_units;    /* U = batch x kv heads (>= 1)                          */
+  int32_t q_per_kv;   /* g = query heads per kv head (GQA), 1..16      */
+  int32_t head_dim;   /* d, 64 or 128 (power of two, Eq. 7)                   */
+  int32_t group;      /* G: K token-block length = V channel-group length
+                         (P:408), 32/64/128, G <= d                           */
+  int32_t residual;   /* R: recent window kept 16-bit, >= 0    */
+  int32_t capacity;   /* max tokens per unit (prompt + decode), >= 1          */
+  int32_t top_k;      /* PSA pivots, 0..32; ignored for TSA           */
+  int32_t kind;       /* akvq_kind                                            */
+  int32_t dtype16;    /* akvq_dtype16 of K/V/q inputs and 16-bit tiers        */
+  float clip2;        /* 2-bit clip ratio, (0,1], paper 0.8           */
+  float clip4;        /* 4-bit clip ratio, (0,1], paper 1.0           */
+} akvq_config;
+
+/* Byte layout of the caller's cache buffer (all offsets from its base;
+ * every region 256-byte aligned).  cap = capacity rounded up to G;
+ * n_pages = cap / G; ng = d / G; slots = R + G.
+ *
+ *  pages   [U][n_pages][page_bytes]        one page = one G-token block:
+ *            +pg_kscale  f32 [d]     K scale per channel (normalized basis)
+ *            +pg_kzero   i32 [d]     K zero point per channel
+ *            +pg_kcodes  u8  [G][d/4] K codes, 4 per byte along channels
+ *            +pg_vscale  f32 [G][ng] V scale per token and channel group
+ *            +pg_vzero   i32 [G][ng]
+ *            +pg_vcodes  u8  [G][d/4]
+ *  ring    [U][slots][2][d] 16-bit     recent-window rows, ORIGINAL basis
+ *                                      (R10); token t lives in slot t % slots
+ *  bitmask [U][bitmask_words] u32      bit t = token t salient (R2, R11, R12)
+ *  side_idx [U][side_cap] i32          token index of each side entry,
+ *                                      ascending token order
+ *  side_cnt [U] i32                    entries in use
+ *  side    [U][side_cap][side_entry_bytes]
+ *            PSA: K row, V row, 16-bit, ORIGINAL basis (R10)
+ *            TSA: +0 kscale f32[ng], kzero i32[ng], vscale f32[ng],
+ *                 vzero i32[ng], then K codes u8[d/2], V codes u8[d/2]
+ *                 (4-bit, 2 per byte, low nibble first; clip4, R11)
+ *  side_cap = top_k (PSA) or cap (TSA).
+ */
+typedef struct {
+  uint64_t total_bytes;
+  uint64_t pages_off, page_bytes;
+  uint64_t pg_kscale, pg_kzero, pg_kcodes, pg_vscale, pg_vzero, pg_vcodes;
+  uint64_t ring_off, ring_unit_bytes;
+  uint64_t bitmask_off;
+  uint64_t side_idx_off, side_cnt_off;
+  uint64_t side_off, side_entry_bytes;
+  int32_t cap, n_pages, slots, bitmask_words, side_cap, ng;
+} akvq_layout;
+
+/* Caller-owned handle.  L and n_q are host mirrors of the (uniform across
+ * units) token count and quantized-region length n_q = G*floor(max(0,L-R)/G)
+ * (R9); the host needs them to schedule flushes without device->host syncs. */
+typedef struct {
+  akvq_config cfg;
+  akvq_layout lay;
+  void *base;          /* device buffer of lay.total_bytes bytes              */
+  int32_t L;
+  int32_t n_q;
+  int32_t sm_count;    /* filled at init, used to size decode grids           */
+  int32_t reserved;
+} akvq_cache;
+
+typedef struct {      /* memory_report, host arithmetic           */
+  double bytes_fp16, bytes_int4, bytes_int2, bytes_overhead;
+  double effective_bits_per_element, compression_ratio_vs_fp16;
+  uint64_t allocated_bytes;
+} akvq_mem_report;
+
+/* ---------------------------------------------------------------- layout */
+/* Layout of a cache for cfg.  Returns AKVQ_OK or the config error. */
+akvq_status akvq_cache_layout(const akvq_config *cfg, akvq_layout *out);
+/* Bytes the caller must provide for one cache; 0 if cfg is invalid. */
+size_t akvq_cache_bytes(const akvq_config *cfg);
+
+/* ---------------------------------------------------------------- init */
+/* cache_new: validates cfg, records dev_buf, enqueues zeroing of
+ * the bitmask and side counters on `stream`; L = n_q = 0.
+ * Errors: EINVAL, EUNSUPPORTED, ECAPACITY (bytes < akvq_cache_bytes). */
+akvq_status akvq_cache_init(akvq_cache *c, const akvq_config *cfg, void *dev_buf,
+                            size_t bytes, akvq_stream_t stream);
+
+/* ---------------------------------------------------------------- prefill */
+/* prefill: for every unit, select salient
+ * tokens (TSA: types[u][t] == 1; PSA: top-k of sum_j colsum[u][j][t]), then
+ * rotate (x.H_s, R5) and quantize blocks [0, n_q) -- K per channel over each
+ * G-token block, V per token over G-channel groups, 2 bits, clip2 -- with
+ * salient tokens moved to the side table, and copy tokens [n_q, L0) into the
+ * 16-bit ring.  Sets L = L0.
+ *   K, V    device [U][L0][d] 16-bit (cfg.dtype16), post-RoPE
+ *   types   device [U][L0] u8 (1 = text); required for TSA, may be NULL for PSA
+ *   colsum  device [U][g][L0] f32 accumulated attention column sums;
+ *           required for PSA, may be NULL for TSA
+ * Errors: ESTATE (L != 0), ECAPACITY (L0 > capacity), EINVAL (NULL input the
+ * layer kind needs, L0 < 0), EUNSUPPORTED (PSA with L0 > AKVQ_MAX_PSA_PROMPT). */
+akvq_status akvq_rotate_quantize(akvq_cache *c, const void *K, const void *V,
+                                 int32_t L0, const uint8_t *types,
+                                 const float *colsum, akvq_stream_t stream);
+
+/* ---------------------------------------------------------------- append */
+/* append_decode (Eq. 2): store each unit's new row in
+ * ring slot L % slots, mark it salient if TSA and types[u] == 1, L += 1; if
+ * L - R - n_q >= G, quantize block [n_q, n_q + G) from the ring exactly as
+ * prefill would and n_q += G.
+ *   k, v   device [U][d] 16-bit;  types device [U] u8 (NULL = all vision)
+ * Errors: ECAPACITY (L == capacity; nothing changes). */
+akvq_status akvq_append_token(akvq_cache *c, const void *k, const void *v,
+                              const uint8_t *types, akvq_stream_t stream);
+
+/* ---------------------------------------------------------------- decode */
+/* Workspace (device bytes) akvq_decode_attention needs for this cache's
+ * current L (grows with L; size it for capacity via the _max variant). */
+size_t akvq_decode_workspace_bytes(const akvq_cache *c);
+size_t akvq_decode_workspace_bytes_max(const akvq_cache *c);
+
+/* Single-query decode attention over the whole cache (R17):
+ *   out[u][j] = softmax_t(q~ . K^_t / sqrt d) . V^  then . H unless
+ *   flags & AKVQ_OUT_ROTATED, with q~ = q[u][j] . H, K^/V^ the dequantized
+ *   2-bit rows, 4-bit TSA side rows, and 16-bit ring / PSA side rows.
+ *   q    device [U][g][d] 16-bit;   out device [U][g][d] f32
+ *   ws   device scratch of >= akvq_decode_workspace_bytes(c) bytes
+ * Errors: ESTATE (L == 0), ECAPACITY (ws too small), EINVAL (NULL). */
+akvq_status akvq_decode_attention(const akvq_cache *c, const void *q, float *out,
+                                  void *ws, size_t ws_bytes, uint32_t flags,
+                                  akvq_stream_t stream);
+
+/* ---------------------------------------------------------------- hooks */
+/* Saliency only (classify_tokens): writes bitmask bits [0, L0).
+ * Test hook; akvq_rotate_quantize calls the same kernel.  Cache must be
+ * empty (ESTATE) and freshly initialised. */
+akvq_status akvq_select_salient(akvq_cache *c, const uint8_t *types,
+                                const float *colsum, int32_t L0,
+                                akvq_stream_t stream);
+
+/* dequantized_view: K^, V^ device f32 [U][L][d] in the rotated
+ * normalized basis (R5).  Test hook.  Errors: ESTATE (L == 0). */
+akvq_status akvq_dequantize_view(const akvq_cache *c, float *K, float *V,
+                                 akvq_stream_t stream);
+
+/* memory_report: host arithmetic over the current L, n_q and the
+ * given number of side entries per unit (host value; pass the count the
+ * caller read back, or -1 to use top_k for PSA / 0 for TSA). */
+akvq_status akvq_memory_report(const akvq_cache *c, int32_t side_entries,
+                               akvq_mem_report *host_out);
+
+const char *akvq_status_str(akvq_status s);
+const char *akvq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AKVQ_H */

@@ -1,0 +1,305 @@
+// api.cu -- the C ABI of libakvq.so (include/akvq.h): argument validation,
+// cache layout, host mirrors of L / n_q, decode split planning and launches.
+// Every entry point is asynchronous on the caller's stream, allocates no
+// device memory and never synchronizes.
+#include <math.h>
+#include <string.h>
+
+#include "akvq.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace akvq;
+
+namespace {
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+akvq_status check_config(const akvq_config *f) {
+  if (!f) return AKVQ_EINVAL;
+  if (f->n_units < 1 || f->q_per_kv < 1 || f->residual < 0 || f->capacity < 1 ||
+      f->top_k < 0 || !is_pow2(f->head_dim) || !is_pow2(f->group) ||
+      !(f->clip2 > 0.f && f->clip2 <= 1.f) || !(f->clip4 > 0.f && f->clip4 <= 1.f) ||
+      (f->kind != AKVQ_TSA && f->kind != AKVQ_PSA) ||
+      (f->dtype16 != AKVQ_BF16 && f->dtype16 != AKVQ_FP16))
+    return AKVQ_EINVAL;
+  if ((f->head_dim != 64 && f->head_dim != 128) || f->group < 32 || f->group > 128 ||
+      f->group > f->head_dim || f->q_per_kv > 16 || f->top_k > 32)
+    return AKVQ_EUNSUPPORTED;
+  return AKVQ_OK;
+}
+
+DevCache make_dev(const akvq_cache *c) {
+  const akvq_config &f = c->cfg;
+  const akvq_layout &y = c->lay;
+  uint8_t *b = static_cast<uint8_t *>(c->base);
+  DevCache d;
+  d.pages = b + y.pages_off;
+  d.ring = reinterpret_cast<uint16_t *>(b + y.ring_off);
+  d.bitmask = reinterpret_cast<uint32_t *>(b + y.bitmask_off);
+  d.side_idx = reinterpret_cast<int32_t *>(b + y.side_idx_off);
+  d.side_cnt = reinterpret_cast<int32_t *>(b + y.side_cnt_off);
+  d.side = b + y.side_off;
+  d.page_bytes = (uint32_t)y.page_bytes;
+  d.pg_kscale = (uint32_t)y.pg_kscale; d.pg_kzero = (uint32_t)y.pg_kzero;
+  d.pg_kcodes = (uint32_t)y.pg_kcodes; d.pg_vscale = (uint32_t)y.pg_vscale;
+  d.pg_vzero = (uint32_t)y.pg_vzero; d.pg_vcodes = (uint32_t)y.pg_vcodes;
+  d.side_entry = (uint32_t)y.side_entry_bytes;
+  d.n_pages = y.n_pages; d.slots = y.slots; d.bm_words = y.bitmask_words;
+  d.side_cap = y.side_cap;
+  d.U = f.n_units; d.g = f.q_per_kv; d.d = f.head_dim; d.G = f.group; d.R = f.residual;
+  d.ng = y.ng; d.kind = f.kind;
+  d.clip2 = f.clip2; d.clip4 = f.clip4;
+  d.inv_sqrt_d = (float)(1.0 / sqrt((double)f.head_dim));
+  return d;
+}
+
+akvq_status cuda_status(cudaError_t e) { return e == cudaSuccess ? AKVQ_OK : AKVQ_ECUDA; }
+
+DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
+  const akvq_config &f = c->cfg;
+  DecodePlan p;
+  p.L = L;
+  p.n_q = n_q;
+  p.n_pages = n_q / f.group;
+  const int sms = c->sm_count > 0 ? c->sm_count : 148;
+  const long target = 4L * sms;                       // CTAs to keep every SM busy
+  long pps = ((long)f.n_units * p.n_pages + target - 1) / target;
+  if (pps < 1) pps = 1;
+  if (pps > p.n_pages) pps = p.n_pages > 0 ? p.n_pages : 1;
+  p.pages_per_split = (int)pps;
+  p.n_page_splits = p.n_pages > 0 ? (p.n_pages + (int)pps - 1) / (int)pps : 0;
+  p.ring_per_split = 128;
+  p.n_ring_splits = (L - n_q + p.ring_per_split - 1) / p.ring_per_split;
+  if (f.kind == AKVQ_PSA) {
+    p.n_side_splits = (f.top_k > 0 && n_q > 0) ? 1 : 0;
+  } else {
+    const int bound = n_q;                            // side entries <= n_q
+    p.n_side_splits = bound > 0 ? (bound + 511) / 512 : 0;
+    if (p.n_side_splits > 8) p.n_side_splits = 8;
+  }
+  p.S = p.n_page_splits + p.n_ring_splits + p.n_side_splits;
+  return p;
+}
+
+size_t ws_bytes_for(const akvq_cache *c, const DecodePlan &p) {
+  return (size_t)c->cfg.n_units * p.S * c->cfg.q_per_kv * (c->cfg.head_dim + 2) * sizeof(float);
+}
+
+}  // namespace
+
+extern "C" {
+
+akvq_status akvq_cache_layout(const akvq_config *f, akvq_layout *y) {
+  const akvq_status st = check_config(f);
+  if (st != AKVQ_OK) return st;
+  if (!y) return AKVQ_EINVAL;
+  memset(y, 0, sizeof(*y));
+  const uint64_t U = f->n_units, d = f->head_dim, G = f->group;
+  const uint64_t ng = d / G;
+  y->cap = (int32_t)((f->capacity + G - 1) / G * G);
+  y->n_pages = (int32_t)(y->cap / G);
+  y->slots = (int32_t)(f->residual + G);
+  y->bitmask_words = y->cap / 32;
+  y->side_cap = f->kind == AKVQ_PSA ? f->top_k : y->cap;
+  y->ng = (int32_t)ng;
+  uint64_t o = 0;
+  y->pg_kscale = o; o = align_up(o + 4 * d, 16);
+  y->pg_kzero = o;  o = align_up(o + 4 * d, 16);
+  y->pg_kcodes = o; o = align_up(o + G * d / 4, 16);
+  y->pg_vscale = o; o = align_up(o + 4 * G * ng, 16);
+  y->pg_vzero = o;  o = align_up(o + 4 * G * ng, 16);
+  y->pg_vcodes = o; o = align_up(o + G * d / 4, 16);
+  y->page_bytes = align_up(o, 128);
+  uint64_t t = 0;
+  y->pages_off = t;    t = align_up(t + U * y->n_pages * y->page_bytes, 256);
+  y->ring_unit_bytes = (uint64_t)y->slots * 2 * d * 2;
+  y->ring_off = t;     t = align_up(t + U * y->ring_unit_bytes, 256);
+  y->bitmask_off = t;  t = align_up(t + U * y->bitmask_words * 4, 256);
+  y->side_idx_off = t; t = align_up(t + U * y->side_cap * 4, 256);
+  y->side_cnt_off = t; t = align_up(t + U * 4, 256);
+  y->side_entry_bytes = f->kind == AKVQ_PSA ? 4 * d : align_up(d + 16 * ng, 16);
+  y->side_off = t;     t = align_up(t + U * y->side_cap * y->side_entry_bytes, 256);
+  y->total_bytes = t;
+  return AKVQ_OK;
+}
+
+size_t akvq_cache_bytes(const akvq_config *f) {
+  akvq_layout y;
+  return akvq_cache_layout(f, &y) == AKVQ_OK ? (size_t)y.total_bytes : 0;
+}
+
+akvq_status akvq_cache_init(akvq_cache *c, const akvq_config *f, void *dev_buf, size_t bytes,
+                            akvq_stream_t stream) {
+  if (!c || !f || !dev_buf) return AKVQ_EINVAL;
+  akvq_layout y;
+  const akvq_status st = akvq_cache_layout(f, &y);
+  if (st != AKVQ_OK) return st;
+  if (bytes < y.total_bytes) return AKVQ_ECAPACITY;
+  memset(c, 0, sizeof(*c));
+  c->cfg = *f;
+  c->lay = y;
+  c->base = dev_buf;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  c->sm_count = sms;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t *b = static_cast<uint8_t *>(dev_buf);
+  cudaMemsetAsync(b + y.bitmask_off, 0, (size_t)f->n_units * y.bitmask_words * 4, s);
+  cudaMemsetAsync(b + y.side_cnt_off, 0, (size_t)f->n_units * 4, s);
+  if (y.side_cap > 0)
+    cudaMemsetAsync(b + y.side_idx_off, 0xff, (size_t)f->n_units * y.side_cap * 4, s);
+  return cuda_status(cudaGetLastError());
+}
+
+akvq_status akvq_select_salient(akvq_cache *c, const uint8_t *types, const float *colsum,
+                                int32_t L0, akvq_stream_t stream) {
+  if (!c || !c->base || L0 < 0) return AKVQ_EINVAL;
+  if (c->L != 0) return AKVQ_ESTATE;
+  if (L0 > c->cfg.capacity) return AKVQ_ECAPACITY;
+  if (L0 == 0) return AKVQ_OK;
+  if (c->cfg.kind == AKVQ_TSA && !types) return AKVQ_EINVAL;
+  if (c->cfg.kind == AKVQ_PSA) {
+    if (!colsum) return AKVQ_EINVAL;
+    if (L0 > AKVQ_MAX_PSA_PROMPT) return AKVQ_EUNSUPPORTED;
+  }
+  const DevCache d = make_dev(c);
+  return cuda_status(launch_salient(d, types, colsum, L0, c->cfg.top_k,
+                                    reinterpret_cast<cudaStream_t>(stream)));
+}
+
+akvq_status akvq_rotate_quantize(akvq_cache *c, const void *K, const void *V, int32_t L0,
+                                 const uint8_t *types, const float *colsum,
+                                 akvq_stream_t stream) {
+  if (!c || !c->base || L0 < 0) return AKVQ_EINVAL;
+  if (c->L != 0) return AKVQ_ESTATE;
+  if (L0 > c->cfg.capacity) return AKVQ_ECAPACITY;
+  if (L0 > 0 && (!K || !V)) return AKVQ_EINVAL;
+  akvq_status st = akvq_select_salient(c, types, colsum, L0, stream);
+  if (st != AKVQ_OK) return st;
+  const akvq_config &f = c->cfg;
+  const int n_q = L0 > f.residual ? (L0 - f.residual) / f.group * f.group : 0;   // R9
+  const DevCache d = make_dev(c);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  QuantSrc src;
+  src.K = static_cast<const uint16_t *>(K);
+  src.V = static_cast<const uint16_t *>(V);
+  src.unit_stride = (size_t)L0 * f.head_dim;
+  src.tok_stride = f.head_dim;
+  src.ring_slots = 0;
+  const int nb = n_q / f.group;
+  cudaError_t e = launch_quantize_blocks(d, f.dtype16, src, 0, nb, nb - 1, s);
+  if (e == cudaSuccess) e = launch_ring_fill(d, K, V, L0, n_q, L0, s);
+  if (e != cudaSuccess) return AKVQ_ECUDA;
+  c->L = L0;
+  c->n_q = n_q;
+  return AKVQ_OK;
+}
+
+akvq_status akvq_append_token(akvq_cache *c, const void *k, const void *v,
+                              const uint8_t *types, akvq_stream_t stream) {
+  if (!c || !c->base || !k || !v) return AKVQ_EINVAL;
+  const akvq_config &f = c->cfg;
+  if (c->L >= f.capacity) return AKVQ_ECAPACITY;
+  const DevCache d = make_dev(c);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_append(d, k, v, types, c->L, s);
+  if (e != cudaSuccess) return AKVQ_ECUDA;
+  c->L += 1;
+  if (c->L - f.residual - c->n_q >= f.group) {        // block leaves the window (R9)
+    QuantSrc src;
+    src.K = d.ring;
+    src.V = d.ring + f.head_dim;
+    src.unit_stride = (size_t)d.slots * 2 * f.head_dim;
+    src.tok_stride = (size_t)2 * f.head_dim;
+    src.ring_slots = d.slots;
+    const int j = c->n_q / f.group;
+    e = launch_quantize_blocks(d, f.dtype16, src, j, 1, j, s);
+    if (e != cudaSuccess) return AKVQ_ECUDA;
+    c->n_q += f.group;
+  }
+  return AKVQ_OK;
+}
+
+size_t akvq_decode_workspace_bytes(const akvq_cache *c) {
+  if (!c) return 0;
+  return ws_bytes_for(c, plan_decode(c, c->L, c->n_q));
+}
+
+size_t akvq_decode_workspace_bytes_max(const akvq_cache *c) {
+  if (!c) return 0;
+  size_t best = 0;
+  const akvq_config &f = c->cfg;
+  for (int L = 1; L <= f.capacity; L += (L < f.capacity - f.group ? f.group : 1)) {
+    const int n_q = L > f.residual ? (L - f.residual) / f.group * f.group : 0;
+    const size_t b = ws_bytes_for(c, plan_decode(c, L, n_q));
+    if (b > best) best = b;
+  }
+  const int n_q = f.capacity > f.residual ? (f.capacity - f.residual) / f.group * f.group : 0;
+  const size_t b = ws_bytes_for(c, plan_decode(c, f.capacity, n_q));
+  return b > best ? b : best;
+}
+
+akvq_status akvq_decode_attention(const akvq_cache *c, const void *q, float *out, void *ws,
+                                  size_t ws_bytes, uint32_t flags, akvq_stream_t stream) {
+  if (!c || !c->base || !q || !out || !ws) return AKVQ_EINVAL;
+  if (c->L == 0) return AKVQ_ESTATE;
+  const DecodePlan p = plan_decode(c, c->L, c->n_q);
+  if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
+  const DevCache d = make_dev(c);
+  return cuda_status(launch_decode(d, c->cfg.dtype16, p, q, out, ws, flags,
+                                   reinterpret_cast<cudaStream_t>(stream)));
+}
+
+akvq_status akvq_dequantize_view(const akvq_cache *c, float *K, float *V, akvq_stream_t stream) {
+  if (!c || !c->base || !K || !V) return AKVQ_EINVAL;
+  if (c->L == 0) return AKVQ_ESTATE;
+  const DevCache d = make_dev(c);
+  return cuda_status(launch_view(d, c->cfg.dtype16, c->L, c->n_q, K, V,
+                                 reinterpret_cast<cudaStream_t>(stream)));
+}
+
+// memory_report: bytes per tier over the current contents.
+//  16-bit: ring tokens [n_q, L) and PSA side rows, 2 B/element;
+//  4-bit : TSA side rows, 0.5 B/element + 8 B per group (scale, zero);
+//  2-bit : the quantized region [n_q) minus side rows, 0.25 B/element;
+//  overhead: K meta 8 B per channel per block, V meta 8 B per group per token.
+// The 1-bit-per-token salient bitmask is not counted (allocated_bytes is).
+akvq_status akvq_memory_report(const akvq_cache *c, int32_t side_entries, akvq_mem_report *r) {
+  if (!c || !r) return AKVQ_EINVAL;
+  const akvq_config &f = c->cfg;
+  const double U = f.n_units, d = f.head_dim, G = f.group, ng = d / G;
+  int se = side_entries;
+  if (se < 0) se = f.kind == AKVQ_PSA ? (f.top_k < c->n_q ? f.top_k : c->n_q) : 0;
+  const double ring = (double)(c->L - c->n_q);
+  const double quant = (double)c->n_q - se;
+  memset(r, 0, sizeof(*r));
+  r->bytes_fp16 = U * 2 * d * 2 * (ring + (f.kind == AKVQ_PSA ? se : 0));
+  r->bytes_int4 = f.kind == AKVQ_TSA ? U * se * 2 * (d * 0.5 + 8 * ng) : 0;
+  r->bytes_int2 = U * quant * 2 * d * 0.25;
+  r->bytes_overhead = U * ((double)c->n_q / G * d * 8 + (double)c->n_q * ng * 8);
+  const double total = r->bytes_fp16 + r->bytes_int4 + r->bytes_int2 + r->bytes_overhead;
+  const double elems = U * (double)c->L * 2 * d;
+  r->effective_bits_per_element = elems > 0 ? 8 * total / elems : 0;
+  r->compression_ratio_vs_fp16 = elems > 0 ? 16.0 / r->effective_bits_per_element : 1.0;
+  r->allocated_bytes = c->lay.total_bytes;
+  return AKVQ_OK;
+}
+
+const char *akvq_status_str(akvq_status s) {
+  switch (s) {
+    case AKVQ_OK: return "ok";
+    case AKVQ_EINVAL: return "invalid argument";
+    case AKVQ_EUNSUPPORTED: return "unsupported configuration";
+    case AKVQ_ECAPACITY: return "capacity exceeded";
+    case AKVQ_ESTATE: return "invalid cache state";
+    case AKVQ_ECUDA: return "CUDA launch error";
+  }
+  return "unknown status";
+}
+
+const char *akvq_version(void) { return "akvq-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,136 @@
+// common.cuh -- device-side helpers shared by the libakvq.so kernels (sm_100a).
+// AKVQ-VL (arXiv 2501.15021).  Nothing here is shared with oracle/.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "akvq.h"
+
+namespace akvq {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// Device view of one layer's cache (pointers resolved on the host from
+// akvq_layout; see include/akvq.h for the byte layout).
+struct DevCache {
+  uint8_t *pages;          // [U][n_pages][page_bytes]
+  uint16_t *ring;          // [U][slots][2][d]
+  uint32_t *bitmask;       // [U][bm_words]
+  int32_t *side_idx;       // [U][side_cap]
+  int32_t *side_cnt;       // [U]
+  uint8_t *side;           // [U][side_cap][side_entry]
+  uint32_t page_bytes, pg_kscale, pg_kzero, pg_kcodes, pg_vscale, pg_vzero, pg_vcodes;
+  uint32_t side_entry;
+  int32_t n_pages, slots, bm_words, side_cap;
+  int32_t U, g, d, G, R, ng, kind;
+  float clip2, clip4, inv_sqrt_d;
+};
+
+__device__ __forceinline__ uint8_t *page_ptr(const DevCache &c, int u, int p) {
+  return c.pages + ((size_t)u * c.n_pages + p) * c.page_bytes;
+}
+__device__ __forceinline__ uint16_t *ring_row(const DevCache &c, int u, int slot) {
+  return c.ring + ((size_t)u * c.slots + slot) * 2 * c.d;   // K row; V row at +d
+}
+__device__ __forceinline__ uint8_t *side_ptr(const DevCache &c, int u, int e) {
+  return c.side + ((size_t)u * c.side_cap + e) * c.side_entry;
+}
+
+// ---- 16-bit element types --------------------------------------------------
+template <int DT> struct H16;
+template <> struct H16<AKVQ_BF16> {
+  static __device__ __forceinline__ float to_f(uint16_t h) {
+    return __uint_as_float((uint32_t)h << 16);
+  }
+};
+template <> struct H16<AKVQ_FP16> {
+  static __device__ __forceinline__ float to_f(uint16_t h) {
+    return __half2float(__ushort_as_half(h));
+  }
+};
+
+// Unpack 8 16-bit values held in a uint4.
+template <int DT>
+__device__ __forceinline__ void cvt8(const uint4 v, float *o) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[2 * i] = H16<DT>::to_f((uint16_t)(w[i] & 0xffff));
+    o[2 * i + 1] = H16<DT>::to_f((uint16_t)(w[i] >> 16));
+  }
+}
+
+// Load a row of D 16-bit values into fp32 registers.
+template <int D, int DT>
+__device__ __forceinline__ void load_row(const uint16_t *__restrict__ src, float (&x)[D]) {
+  const uint4 *s = reinterpret_cast<const uint4 *>(src);
+#pragma unroll
+  for (int i = 0; i < D / 8; ++i) cvt8<DT>(__ldg(s + i), x + 8 * i);
+}
+
+// In-register fast Walsh-Hadamard transform: x <- x . H_s, the +-1
+// Sylvester matrix in natural order (Eq. 7 without the 1/sqrt2 factors, R5).
+template <int D>
+__device__ __forceinline__ void fwht_reg(float (&x)[D]) {
+#pragma unroll
+  for (int h = 1; h < D; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < D; i += 2 * h) {
+#pragma unroll
+      for (int j = i; j < i + h; ++j) {
+        const float a = x[j], b = x[j + h];
+        x[j] = __fadd_rn(a, b);
+        x[j + h] = __fsub_rn(a, b);
+      }
+    }
+  }
+}
+
+// ---- Eqs. 3, 5, 6 with fp32 decisions (R3, R6, R7, R8) ------
+struct QMeta {
+  float s;    // scale in x.H_s units (normal), constant (degenerate), 0 (empty)
+  float zf;   // zero point as an integer-valued float
+  int mode;   // 0 normal, 1 degenerate (codes 1), 2 empty (codes 0)
+};
+
+// IEEE single operations only (explicit _rn intrinsics: no FMA contraction).
+__device__ __forceinline__ QMeta q_meta(float mn, float mx, bool any, float clip,
+                                        float levels) {
+  QMeta m;
+  if (!any) { m.s = 0.f; m.zf = 0.f; m.mode = 2; return m; }
+  const float cmx = __fmul_rn(clip, mx);            // clipped_max(X)
+  const float cmn = __fmul_rn(clip, mn);            // clipped_min(X)
+  const float range = __fsub_rn(cmx, cmn);
+  if (range < 1e-12f) { m.s = mx; m.zf = 0.f; m.mode = 1; return m; }
+  m.s = __fdiv_rn(range, levels);                   // Eq. 5
+  m.zf = -rintf(__fdiv_rn(cmn, m.s));               // Eq. 6
+  m.mode = 0;
+  return m;
+}
+
+__device__ __forceinline__ uint32_t q_code(float x, const QMeta &m, float levels) {
+  if (m.mode == 2) return 0u;
+  if (m.mode == 1) return 1u;
+  const float r = rintf(__fdiv_rn(x, m.s));         // Eq. 3
+  float q = __fadd_rn(r, m.zf);
+  q = fminf(fmaxf(q, 0.f), levels);
+  return (uint32_t)q;
+}
+
+__device__ __forceinline__ int32_t zero_i32(float zf) { return __float2int_rz(zf); }
+
+// ---- warp helpers --------------------------------------------------------
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace akvq

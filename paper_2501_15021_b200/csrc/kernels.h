@@ -1,0 +1,41 @@
+// kernels.h -- host launchers of the libakvq.so kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace akvq {
+
+struct DevCache;
+
+// Source rows of a quantize launch: prefill inputs [U][L0][d] or the ring.
+struct QuantSrc {
+  const uint16_t *K, *V;
+  size_t unit_stride;   // elements between units
+  size_t tok_stride;    // elements between tokens (slots in ring mode)
+  int ring_slots;       // 0: linear token index; >0: slot = token % ring_slots
+};
+
+// Decode split plan (host-computed, uniform across units).
+struct DecodePlan {
+  int L, n_q;
+  int n_pages;           // quantized pages in use = n_q / G
+  int pages_per_split, n_page_splits;
+  int ring_per_split, n_ring_splits;
+  int n_side_splits;     // side entries are shared equally among these splits
+  int S;                 // total splits
+};
+
+cudaError_t launch_salient(const DevCache &c, const uint8_t *types, const float *colsum,
+                           int L0, int top_k, cudaStream_t st);
+cudaError_t launch_quantize_blocks(const DevCache &c, int dtype16, const QuantSrc &src,
+                                   int block0, int nblocks, int last_block, cudaStream_t st);
+cudaError_t launch_ring_fill(const DevCache &c, const void *K, const void *V, int L0, int t0,
+                             int t1, cudaStream_t st);
+cudaError_t launch_append(const DevCache &c, const void *k, const void *v,
+                          const uint8_t *types, int L, cudaStream_t st);
+cudaError_t launch_decode(const DevCache &c, int dtype16, const DecodePlan &p, const void *q,
+                          float *out, void *ws, uint32_t flags, cudaStream_t st);
+cudaError_t launch_view(const DevCache &c, int dtype16, int L, int n_q, float *K, float *V,
+                        cudaStream_t st);
+
+}  // namespace akvq

@@ -1,0 +1,218 @@
+"""GPU parity: libakvq.so (through the C ABI) vs the CPU oracle, element by element
+on the same seeded inputs (-m gpu).  Agreement rules: DESIGN.md section 4 (BJ:5).
+
+Sizes: the tiny config (BJ:7) and the 7B shape (BJ:8) in full; the sweep, video and
+Qwen shapes (BJ:9-11) at full size on the GPU with sampled units checked against
+the oracle (first, middle, last unit), in the launch configuration bench.py uses.
+"""
+import numpy as np
+import pytest
+import torch
+
+from parity import GpuState, compare_ring, compare_state, f16_bits
+
+pytestmark = pytest.mark.gpu
+
+OUT_TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def ak():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2501_15021_b200 import akvq
+    akvq.lib()
+    return akvq
+
+
+@pytest.fixture(scope="module")
+def sy():
+    from paper_2501_15021_b200 import synth
+    return synth
+
+
+def _configs(ak, orc, w, layer, units_n, kind=None, cap=None):
+    kind = w.kind(layer) if kind is None else kind
+    dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
+    cap = w.capacity if cap is None else cap
+    gcfg = ak.make_config(units_n, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4)
+    ocfg = orc.OracleConfig(units_n, w.g, w.d, w.G, w.R, cap, w.top_k, kind,
+                            orc.BF16 if dt == ak.AKVQ_BF16 else orc.FP16, w.clip2, w.clip4)
+    return gcfg, ocfg
+
+
+def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every=1,
+              flags=0, report=None):
+    """Prefill + `steps` decode steps on the GPU for all units; the oracle runs the
+    sampled `units` (default all).  Compares state after prefill and after every
+    flush, outputs every `check_every` steps."""
+    U = w.U
+    us = list(range(U)) if units is None else list(units)
+    gcfg, _ = _configs(ak, orc, w, layer, U, kind)
+    _, ocfg = _configs(ak, orc, w, layer, len(us), kind)
+    dev = "cuda"
+    inp = sy.layer_inputs(w, layer, device=dev)
+    lc = ak.LayerCache(gcfg)
+    lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
+    oc = orc.OracleCache(ocfg)
+    inp_o = sy.layer_inputs(w, layer, units=us, device="cpu")
+    # the CPU-generated sampled units are the GPU's units (counter-based generator)
+    assert torch.equal(inp_o["K"], inp["K"][us].cpu())
+    assert oc.prefill(f16_bits(inp_o["K"]), f16_bits(inp_o["V"]), inp_o["types"].numpy(),
+                      inp_o["colsum"].numpy()) == 0
+    rows_k = [f16_bits(inp_o["K"])]
+    rows_v = [f16_bits(inp_o["V"])]
+    gs = GpuState(lc)
+    assert (gs.L, gs.n_q) == (oc.L, oc.nq)
+    compare_state(gs, oc.export(), gcfg, report, units=us)
+    compare_ring(gs, np.concatenate(rows_k, 1), np.concatenate(rows_v, 1), gs.ring.shape[1], us)
+    worst = 0.0
+    for step in range(steps):
+        di = sy.decode_inputs(w, layer, step, device=dev)
+        nq_before = lc.n_q
+        lc.append(di["k"], di["v"], di["types"])
+        out = lc.decode(di["q"], flags=flags)
+        do = sy.decode_inputs(w, layer, step, units=us, device="cpu")
+        oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
+        rows_k.append(f16_bits(do["k"])[:, None])
+        rows_v.append(f16_bits(do["v"])[:, None])
+        assert (lc.L, lc.n_q) == (oc.L, oc.nq)
+        if lc.n_q != nq_before:
+            gs = GpuState(lc)
+            compare_state(gs, oc.export(), gcfg, report, units=us)
+            compare_ring(gs, np.concatenate(rows_k, 1), np.concatenate(rows_v, 1),
+                         gs.ring.shape[1], us)
+        if step % check_every == 0 or step == steps - 1:
+            ref = oc.decode(f16_bits(do["q"]), out_rotated=bool(flags & ak.AKVQ_OUT_ROTATED))
+            got = out[us].double().cpu().numpy()
+            err = np.abs(got - ref).max()
+            worst = max(worst, err)
+            assert err <= OUT_TOL, f"step {step}: max-abs {err}"
+    return lc, oc, worst
+
+
+# ----------------------------------------------------------------- tiny (BJ:7)
+@pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
+def test_tiny_prefill_decode_and_flush(ak, orc, sy, kind):
+    """Quantize once, 4 decode steps, extended to 16 steps across the L = 104 flush."""
+    w = sy.TINY
+    lc, oc, worst = _run_case(ak, orc, sy, w, 0, kind=kind, steps=16)
+    assert lc.L == 112 and lc.n_q == 96
+
+
+def test_tiny_view_and_rotated_output(ak, orc, sy):
+    w = sy.TINY
+    lc, oc, _ = _run_case(ak, orc, sy, w, 0, kind=1, steps=9, flags=ak.AKVQ_OUT_ROTATED)
+    K, V = lc.view()
+    Ko, Vo = oc.view()
+    for a, b in ((K, Ko), (V, Vo)):
+        a = a.double().cpu().numpy()
+        assert np.all(np.abs(a - b) <= 1e-6 * np.maximum(np.abs(b), np.abs(b).max(-1, keepdims=True)) + 1e-7)
+
+
+# ----------------------------------------------------------------- 7B shape (BJ:8)
+@pytest.mark.parametrize("layer", [0, 2], ids=["TSA-L0", "PSA-L2"])
+def test_llava7b_layer_full(ak, orc, sy, layer):
+    """All 32 units; decode across the L = 672 flush (n_q 512 -> 640)."""
+    w = sy.LLAVA7B
+    rep = {}
+    lc, oc, worst = _run_case(ak, orc, sy, w, layer, steps=3, report=rep)
+    assert lc.n_q == 640
+    print("ties", rep, "worst", worst)
+
+
+# ----------------------------------------------------------------- sampled, full size
+@pytest.mark.parametrize("name,layer", [("sweep@b16", 2), ("video13b", 3), ("qwen_gqa", 5),
+                                        ("qwen_gqa", 1)])
+def test_full_size_sampled_units(ak, orc, sy, name, layer):
+    w = sy.get(name)
+    U = w.U
+    _run_case(ak, orc, sy, w, layer, steps=2, units=[0, U // 2, U - 1])
+
+
+# ----------------------------------------------------------------- edge cases
+def _mini(sy, **kw):
+    base = dict(name="edge", n_layers=1, batch=1, hq=2, hkv=2, d=128, G=128, R=8, top_k=3,
+                dtype="bf16", segments=((1, 20), (0, 200), (1, 30)), tsa_layers=(0,),
+                n_outlier_ch=2, outlier_gain=15.0, pivots_random_vision=2, decode_steps=40)
+    base.update(kw)
+    return sy.Workload(**base)
+
+
+@pytest.mark.parametrize("kw", [
+    dict(),                                                         # TSA, ragged tail
+    dict(tsa_layers=()),                                            # PSA
+    dict(d=64, G=64, segments=((1, 7), (0, 100))),                  # d 64
+    dict(G=32, segments=((0, 77),), R=0, tsa_layers=()),            # G 32, R 0, PSA
+    dict(G=64, hq=14, hkv=2, segments=((1, 5), (0, 190)), tsa_layers=()),   # GQA g = 7
+    dict(segments=((1, 5),), R=16, decode_steps=30),                # L0 < R: nothing quantized
+    dict(segments=((1, 300),)),                                     # TSA all text: empty K groups
+    dict(segments=((0, 136),), R=8, top_k=0, tsa_layers=()),        # L0 = G + R exactly, k = 0
+    dict(top_k=32, segments=((0, 40),), R=0, G=32, d=64, tsa_layers=()),    # k = L0 > G
+], ids=["tsa", "psa", "d64", "g32r0", "gqa7", "short", "alltext", "exact", "k32"])
+def test_edge_cases(ak, orc, sy, kw):
+    w = _mini(sy, **kw)
+    _run_case(ak, orc, sy, w, 0, steps=w.decode_steps)
+
+
+def test_empty_prefill_then_appends(ak, orc, sy):
+    """append to an empty cache; prefill of 0 tokens then 150 appends."""
+    w = _mini(sy, segments=((1, 1),), decode_steps=150)
+    gcfg, ocfg = _configs(ak, orc, w, 0, w.U)
+    lc = ak.LayerCache(gcfg)
+    with pytest.raises(ak.AkvqError) as e:
+        lc.decode(torch.zeros((w.U, w.g, w.d), dtype=torch.bfloat16, device="cuda"))
+    assert e.value.status == ak.AKVQ_ESTATE
+    oc = orc.OracleCache(ocfg)
+    for step in range(150):
+        di = sy.decode_inputs(w, 0, step, device="cuda")
+        lc.append(di["k"], di["v"], di["types"])
+        oc.append(f16_bits(di["k"]), f16_bits(di["v"]), di["types"].cpu().numpy())
+        if step % 37 == 0 or step == 149:
+            out = lc.decode(di["q"]).double().cpu().numpy()
+            assert np.abs(out - oc.decode(f16_bits(di["q"]))).max() <= OUT_TOL
+    compare_state(GpuState(lc), oc.export(), gcfg)
+
+
+def test_degenerate_constant_rows(ak, orc):
+    """Constant K/V rows -> degenerate groups (R8) reconstruct exactly."""
+    U, d, G, L0 = 2, 128, 128, 300
+    gcfg = ak.make_config(U, 1, d, G, 0, L0 + 4, 2, 1, ak.AKVQ_BF16)
+    ocfg = orc.OracleConfig(U, 1, d, G, 0, L0 + 4, 2, 1, orc.BF16)
+    K = torch.full((U, L0, d), 0.75, dtype=torch.bfloat16)
+    K[:, :, 0] = 3.0                      # rotated rows are not constant, channels are
+    V = torch.zeros((U, L0, d), dtype=torch.bfloat16)
+    V[:, :, 5] = -2.0                     # rotated V rows = +-2/sqrt(d): two levels
+    cs = torch.rand((U, 1, L0), generator=torch.Generator().manual_seed(0))
+    lc = ak.LayerCache(gcfg)
+    lc.prefill(K.cuda(), V.cuda(), None, cs.cuda())
+    oc = orc.OracleCache(ocfg)
+    oc.prefill(f16_bits(K), f16_bits(V), None, cs.numpy())
+    compare_state(GpuState(lc), oc.export(), gcfg)
+    q = torch.randn((U, 1, d), generator=torch.Generator().manual_seed(1)).to(torch.bfloat16)
+    out = lc.decode(q.cuda()).double().cpu().numpy()
+    assert np.abs(out - oc.decode(f16_bits(q))).max() <= OUT_TOL
+
+
+def test_determinism_and_errors(ak, orc, sy):
+    w = _mini(sy, tsa_layers=())
+    gcfg, _ = _configs(ak, orc, w, 0, w.U)
+    inp = sy.layer_inputs(w, 0, device="cuda")
+    lc = ak.LayerCache(gcfg)
+    lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
+    with pytest.raises(ak.AkvqError) as e:          # prefill on a non-empty cache
+        lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
+    assert e.value.status == ak.AKVQ_ESTATE
+    di = sy.decode_inputs(w, 0, 0, device="cuda")
+    a = lc.decode(di["q"])
+    b = lc.decode(di["q"])
+    assert torch.equal(a, b)                         # bit-identical
+    small = torch.empty(1, dtype=torch.float32, device="cuda")
+    with pytest.raises(ak.AkvqError) as e:
+        ak.akvq_decode_attention(lc.handle, di["q"], a, small)
+    assert e.value.status == ak.AKVQ_ECAPACITY
+    for _ in range(w.capacity - lc.L):
+        lc.append(di["k"], di["v"], di["types"])
+    with pytest.raises(ak.AkvqError) as e:
+        lc.append(di["k"], di["v"], di["types"])
+    assert e.value.status == ak.AKVQ_ECAPACITY
