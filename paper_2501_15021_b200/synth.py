@@ -184,7 +184,7 @@ def pivot_positions(w: Workload, batch_row: int) -> List[int]:
     """Planted pivot tokens of one batch row (BJ:7-11)."""
     types = token_types(w)
     vis = torch.nonzero(types == VISION).flatten().tolist()
-    piv = [p for p in w.pivots_fixed]
+    piv = [p for p in w.pivots_fixed if p < w.L0]
     keys = torch.tensor([_key(w.seed, batch_row, _KIND["piv"])], dtype=torch.int64)
     h = _uniform_bits(keys, 64, "cpu")[0].tolist()
     if w.pivots_per_frame:
@@ -197,8 +197,9 @@ def pivot_positions(w: Workload, batch_row: int) -> List[int]:
         for i, (s, c) in enumerate(frames):
             piv.append(s + int(h[i]) % c)
     else:
+        want = len(w.pivots_fixed) + min(w.pivots_random_vision, len(vis))
         i = 0
-        while len(piv) < len(w.pivots_fixed) + w.pivots_random_vision:
+        while len(piv) < want and i < len(h):
             p = vis[int(h[i]) % len(vis)]
             i += 1
             if p not in piv:
