@@ -1,0 +1,429 @@
+#!/usr/bin/env python3
+"""bench.py -- 2-bit-KV decode throughput of the AKVQ-VL hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl akvq|reference]
+
+One "step" = one decode step of the whole model for the whole batch: for every
+layer, append the new token's K/V (flushing a G-block to 2 bits when it leaves the
+window) and run single-query decode attention over that layer's packed cache
+(SURVEY 8(a) rows a2-a7), plus the all-gather of outputs across ranks (a8).
+Prompts are quantized (rows a2-a5, incl. saliency) before timing; that prefill is
+timed separately and reported under "prefill".
+
+Default workload: BJ:9's batch sweep at LLaVA-1.5-7B shape, batch 64 ("sweep@b64":
+32 layers, 32 MHA heads, d 128, 3-image prompt of 1848 tokens), the largest
+configuration BASELINE.json's metric is quoted on that fits one GPU.  Synthetic
+inputs (paper_2501_15021_b200/synth.py) stand in for MileBench prompts.
+
+Multi-GPU: launched by torchrun; rank r owns a contiguous slice of the global
+units (batch x kv-head, BJ:5), so the global batch is fixed ("strong" scaling);
+outputs are all-gathered with NCCL every layer.  Timing: CUDA events on the
+launching stream with a barrier + synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2501_15021_b200 import synth  # noqa: E402
+
+METRIC = "2-bit-KV decode tokens/s and attention HBM GB/s vs peak at 1/2/4/8 B200"
+
+
+def _peaks():
+    p = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md: 6.65 TB/s)"}
+    f = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(f):
+        with open(f) as fh:
+            j = json.load(fh)
+        p = {"hbm_gbs": float(j["hbm_gbs"]), "src": "measured (MEASURED_PEAKS.json)",
+             "sm_max_mhz": j.get("sm_max_mhz")}
+    return p
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+# ----------------------------------------------------------------- byte model
+def decode_bytes_per_unit(w, kind, L, n_q, side):
+    """Algorithmic bytes one decode reads/writes for one unit:
+    2-bit codes + K meta (8 B/channel/block) + V meta (8 B/group/token) + bitmask
+    for [0, n_q); 16-bit ring rows; side rows; q in, fp32 out."""
+    d, G = w.d, w.G
+    ng = d // G
+    b = n_q * (2 * d / 4 + 8 * d / G + 8 * ng + 1 / 8)
+    b += (L - n_q) * 4 * d
+    b += side * (4 * d if kind == 1 else d + 16 * ng)
+    b += w.g * d * (2 + 4)
+    return b
+
+
+def prefill_bytes_per_unit(w, kind, L0):
+    """Prefill quantize: read K,V rows (16-bit) + types/colsum; write packed pages,
+    ring rows and side rows."""
+    d, G = w.d, w.G
+    ng = d // G
+    n_q = (L0 - w.R) // G * G if L0 > w.R else 0
+    rd = L0 * 4 * d + (L0 * 4 * w.g if kind == 1 else L0)
+    wr = n_q * (2 * d / 4 + 8 * d / G + 8 * ng) + (L0 - n_q) * 4 * d
+    return rd + wr
+
+
+# ----------------------------------------------------------------- CPU oracle leg
+class OracleSample:
+    """The oracle (as it stands, never tuned) on the host cores, on a bounded sample
+    of the workload: `n_units` units of one PSA layer, prefilled once; each step is
+    one decode step (append + attention) of those units, extrapolated to the whole
+    batch and all layers (tokens/s)."""
+
+    def __init__(self, w, n_units=16, layer=2):
+        import oracle
+        oracle.build()
+        self.oracle, self.w, self.layer = oracle, w, layer
+        U = w.U
+        self.units = sorted(set(int(round(i * (U - 1) / max(1, n_units - 1)))
+                                for i in range(n_units)))
+        kind = w.kind(layer)
+        ocfg = oracle.OracleConfig(len(self.units), w.g, w.d, w.G, w.R, w.capacity, w.top_k,
+                                   kind, oracle.BF16 if w.dtype == "bf16" else oracle.FP16,
+                                   w.clip2, w.clip4)
+        self.oc = oracle.OracleCache(ocfg)
+        inp = synth.layer_inputs(w, layer, units=self.units, device="cpu")
+        self.oc.prefill(synth.to_u16(inp["K"]), synth.to_u16(inp["V"]), inp["types"].numpy(),
+                        inp["colsum"].numpy())
+        self.steps, self.t_tot = 0, 0.0
+
+    def step(self) -> float:
+        """One timed oracle decode step; returns the extrapolated tokens/s."""
+        w = self.w
+        if self.oc.L >= w.capacity:
+            raise RuntimeError("oracle sample ran out of capacity")
+        di = synth.decode_inputs(w, self.layer, self.steps, units=self.units, device="cpu")
+        k, v, q = synth.to_u16(di["k"]), synth.to_u16(di["v"]), synth.to_u16(di["q"])
+        t0 = time.perf_counter()
+        self.oc.append(k, v, di["types"].numpy())
+        self.oc.decode(q)
+        dt = time.perf_counter() - t0
+        self.steps += 1
+        self.t_tot += dt
+        return w.batch / (dt / len(self.units) * w.U * w.n_layers)
+
+    def describe(self) -> str:
+        w = self.w
+        return (f"oracle decode steps (append + attention) of {len(self.units)} of {w.U} "
+                f"units of layer {self.layer}, {self.steps} steps in {self.t_tot:.3f} s; "
+                f"extrapolated x{w.U}/{len(self.units)} units x{w.n_layers} layers")
+
+    @property
+    def cores(self) -> int:
+        return self.oracle.nthreads()
+
+
+def oracle_baseline(w, seconds=12.0, max_steps=60):
+    """cpu_baseline leg of the GPU run: ~10-30 s of oracle work."""
+    smp = OracleSample(w)
+    vals = []
+    while smp.steps < max_steps and smp.t_tot < seconds and smp.oc.L < w.capacity:
+        vals.append(smp.step())
+    val = len(vals) / sum(1.0 / v for v in vals)
+    return {"value": val, "unit": "tokens/s", "cores": smp.cores, "kind": "oracle",
+            "sample": smp.describe()}
+
+
+def run_reference(args, w, rank):
+    """--impl reference: the oracle as the reference arm, rank 0 only."""
+    if rank != 0:
+        return
+    smp = OracleSample(w, n_units=8)
+    n = min(args.warmup + args.steps, w.capacity - smp.oc.L)
+    times = []
+    for i in range(n):
+        v = smp.step()
+        if i >= args.warmup:
+            times.append(1.0 / v)
+    val = len(times) / sum(times)
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+            "ms_per_step": 1000.0 * w.batch / val, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": smp.cores,
+                             "kind": "oracle", "sample": smp.describe()},
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="sweep@b64")
+    ap.add_argument("--impl", default="akvq", choices=["akvq", "reference"])
+    ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    w = synth.get(args.workload)
+
+    if args.impl == "reference":
+        run_reference(args, w, rank)
+        return
+
+    from paper_2501_15021_b200 import akvq as ak
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    n_layers = args.layers or w.n_layers
+    U = w.U
+    if U % world:
+        raise SystemExit(f"units {U} not divisible by {world} ranks")
+    Ul = U // world
+    units = list(range(rank * Ul, (rank + 1) * Ul))
+    dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
+    need_steps = args.warmup + 2 * args.steps
+    cap = w.L0 + max(w.decode_steps, need_steps)
+    stream = torch.cuda.current_stream()
+
+    # ---------------- prefill every layer (timed separately)
+    caches, pre_ms, pre_bytes = [], 0.0, 0.0
+    for layer in range(n_layers):
+        kind = w.kind(layer)
+        cfg = ak.make_config(Ul, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4)
+        lc = ak.LayerCache(cfg, device=dev)
+        inp = synth.layer_inputs(w, layer, units=units, device=dev)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
+        e1.record()
+        torch.cuda.synchronize()
+        pre_ms += e0.elapsed_time(e1)
+        pre_bytes += Ul * prefill_bytes_per_unit(w, kind, w.L0)
+        del inp
+        caches.append(lc)
+    torch.cuda.empty_cache()
+
+    # ---------------- decode-step inputs, resident in HBM before timing
+    def step_inputs(step, device):
+        qs, ks, vs = [], [], []
+        for layer in range(n_layers):
+            di = synth.decode_inputs(w, layer, step, units=units, device=device)
+            qs.append(di["q"]); ks.append(di["k"]); vs.append(di["v"])
+        return torch.stack(qs), torch.stack(ks), torch.stack(vs), di["types"]
+
+    inputs = [step_inputs(s, dev) for s in range(args.warmup + args.steps)]
+    outs = torch.empty((n_layers, Ul, w.g, w.d), dtype=torch.float32, device=dev)
+    gath = torch.empty((n_layers, U, w.g, w.d), dtype=torch.float32, device=dev) if world > 1 else None
+    launches = [0]
+
+    def one_step(q, k, v, types, ev=None):
+        for layer, lc in enumerate(caches):
+            nq = lc.n_q
+            lc.append(k[layer], v[layer], types)
+            launches[0] += 1 + (lc.n_q != nq)
+            if ev is not None:
+                ev[layer][0].record()
+            lc.decode(q[layer], out=outs[layer])
+            if ev is not None:
+                ev[layer][1].record()
+            launches[0] += 2
+            if gath is not None:
+                dist.all_gather_into_tensor(gath[layer], outs[layer])
+
+    for s in range(args.warmup):
+        one_step(*inputs[s])
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+
+    # ---------------- timed region (device)
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(n_layers)]
+           for _ in range(args.steps)]
+    L_at = [caches[2 % n_layers].L]
+    nq_at = [caches[2 % n_layers].n_q]
+    sampler = ClockSampler(local)
+    launches[0] = 0
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    with sampler:
+        t0.record()
+        for s in range(args.steps):
+            one_step(*inputs[args.warmup + s], ev=evs[s])
+            L_at.append(caches[2 % n_layers].L)
+            nq_at.append(caches[2 % n_layers].n_q)
+        t1.record()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    n_launch = launches[0]
+    ms = t0.elapsed_time(t1) / args.steps
+    dec_ms = sum(evs[s][l][0].elapsed_time(evs[s][l][1]) for s in range(args.steps)
+                 for l in range(n_layers)) / (args.steps * n_layers)
+    if dist:
+        t = torch.tensor([ms, dec_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, dec_ms = float(t[0]), float(t[1])
+    clocks = sampler.summary()
+
+    # algorithmic bytes of one decode launch (per layer, this rank), averaged
+    side_psa = w.top_k
+    text_prefix = [0]
+    for t in synth.token_types(w).tolist():
+        text_prefix.append(text_prefix[-1] + (t == 1))
+    bytes_layers = []
+    for s in range(args.steps):
+        L, nq = L_at[s + 1], nq_at[s + 1]
+        for layer in range(n_layers):
+            kind = w.kind(layer)
+            if kind == 1:
+                side = side_psa
+            else:
+                side = text_prefix[min(nq, w.L0)] + max(0, nq - w.L0)
+            bytes_layers.append(Ul * decode_bytes_per_unit(w, kind, L, nq, side))
+    dec_bytes = sum(bytes_layers) / len(bytes_layers)
+    peaks = _peaks()
+    achieved = dec_bytes / (dec_ms * 1e-3) / 1e9
+    tokens_per_s = w.batch / (ms * 1e-3)
+
+    # ---------------- end to end through the C ABI with host buffers
+    e2e_steps = args.steps
+    host_in = []
+    for s in range(e2e_steps):
+        q, k, v, ty = step_inputs(args.warmup + args.steps + s, "cpu")
+        host_in.append((q.pin_memory(), k.pin_memory(), v.pin_memory(), ty.pin_memory()))
+    host_out = torch.empty((n_layers, U if world > 1 else Ul, w.g, w.d), dtype=torch.float32).pin_memory()
+    dq = torch.empty_like(inputs[0][0]); dk = torch.empty_like(inputs[0][1])
+    dv = torch.empty_like(inputs[0][2]); dty = torch.empty_like(inputs[0][3])
+    h2d = sum(t.numel() * t.element_size() for t in host_in[0])
+    d2h = host_out.numel() * host_out.element_size()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for s in range(e2e_steps):
+        q, k, v, ty = host_in[s]
+        dq.copy_(q, non_blocking=True); dk.copy_(k, non_blocking=True)
+        dv.copy_(v, non_blocking=True); dty.copy_(ty, non_blocking=True)
+        one_step(dq, dk, dv, dty)
+        host_out.copy_(gath if gath is not None else outs, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+        dist.barrier()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_baseline(w)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": w.name, "source": "BJ:9 batch sweep at LLaVA-1.5-7B shape",
+                       "layers": n_layers, "global_batch": w.batch, "heads": w.hq,
+                       "kv_heads": w.hkv, "head_dim": w.d, "prompt_tokens": w.L0,
+                       "group": w.G, "residual": w.R, "top_k": w.top_k,
+                       "tsa_layers": list(w.tsa_layers), "kv_bits": 2,
+                       "parallelism": f"units (batch x kv-head) sharded over {world} GPU(s)",
+                       "l2": "no flush: per-step working set "
+                             f"{sum(bytes_layers[:n_layers]) / 1e9:.2f} GB/rank >> 126 MB L2"},
+            "attention_gbs": achieved,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                         "traffic": None, "kernel": "k_decode_split + k_combine",
+                         "bytes_per_launch": dec_bytes, "launch_ms": dec_ms,
+                         "peak_src": peaks["src"]},
+            "prefill": {"ms_all_layers": pre_ms, "quantize_gbs": pre_bytes / (pre_ms * 1e-3) / 1e9,
+                        "frac": pre_bytes / (pre_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "e2e": {"value": w.batch / (e2e_ms * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": n_launch,
+            "clocks": clocks,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
