@@ -125,8 +125,12 @@ typedef struct {
   int32_t L;
   int32_t n_q;
   int32_t sm_count;    /* filled at init, used to size decode grids           */
-  int32_t reserved;
+  int32_t options;     /* AKVQ_OPT_* bits, 0 by default (set after init)      */
 } akvq_cache;
+
+/* akvq_cache.options: route 2-bit pages through the generic split-K kernel
+ * instead of the persistent dp4a page kernel (test hook for cross-checks). */
+#define AKVQ_OPT_GENERIC_PAGES 1
 
 typedef struct {      /* memory_report, host arithmetic           */
   double bytes_fp16, bytes_int4, bytes_int2, bytes_overhead;

@@ -20,6 +20,7 @@ AKVQ_OK, AKVQ_EINVAL, AKVQ_EUNSUPPORTED, AKVQ_ECAPACITY, AKVQ_ESTATE, AKVQ_ECUDA
 AKVQ_TSA, AKVQ_PSA = 0, 1
 AKVQ_BF16, AKVQ_FP16 = 0, 1
 AKVQ_OUT_ROTATED = 1
+AKVQ_OPT_GENERIC_PAGES = 1
 AKVQ_MAX_PSA_PROMPT = 49152
 
 # every symbol include/akvq.h declares
@@ -55,7 +56,7 @@ class akvq_layout(C.Structure):
 class akvq_cache(C.Structure):
     _fields_ = [("cfg", akvq_config), ("lay", akvq_layout), ("base", C.c_void_p),
                 ("L", C.c_int32), ("n_q", C.c_int32), ("sm_count", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("options", C.c_int32)]
 
 
 class akvq_mem_report(C.Structure):
@@ -205,12 +206,13 @@ def akvq_memory_report(cache, side_entries: int = -1) -> akvq_mem_report:
 class LayerCache:
     """One layer's packed cache in a torch-owned device buffer."""
 
-    def __init__(self, cfg: akvq_config, device="cuda", stream=None):
+    def __init__(self, cfg: akvq_config, device="cuda", stream=None, options: int = 0):
         self.cfg = cfg
         self.layout = akvq_cache_layout(cfg)
         self.buf = torch.empty(int(self.layout.total_bytes), dtype=torch.uint8, device=device)
         self.handle = akvq_cache()
         akvq_cache_init(self.handle, cfg, self.buf, stream)
+        self.handle.options = options
         self.ws = torch.empty(max(1, akvq_decode_workspace_bytes_max(self.handle)) // 4 + 1,
                               dtype=torch.float32, device=device)
 

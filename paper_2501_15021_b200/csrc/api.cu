@@ -79,12 +79,28 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
     p.n_side_splits = bound > 0 ? (bound + 511) / 512 : 0;
     if (p.n_side_splits > 8) p.n_side_splits = 8;
   }
+  // fast path: the quantized pages go through the persistent dp4a page kernel
+  p.fast = 0;
+  p.pp.T = 0; p.pp.W = 0; p.pp.n_pages = p.n_pages; p.pp.maxseg = 0;
+  if (p.n_pages > 0 && !(c->options & AKVQ_OPT_GENERIC_PAGES) &&
+      pages_fast_supported(f.head_dim, f.group, f.q_per_kv)) {
+    p.fast = 1;
+    p.n_page_splits = 0;
+    p.pp.T = (long long)f.n_units * p.n_pages;
+    const long long wmax = (long long)sms * 2 * pages_warps_per_cta();
+    p.pp.W = p.pp.T < wmax ? p.pp.T : wmax;
+    const long long per = (p.pp.T + p.pp.W - 1) / p.pp.W;
+    p.pp.maxseg = (int)((per + p.n_pages - 1) / p.n_pages + 1);
+  }
   p.S = p.n_page_splits + p.n_ring_splits + p.n_side_splits;
   return p;
 }
 
 size_t ws_bytes_for(const akvq_cache *c, const DecodePlan &p) {
-  return (size_t)c->cfg.n_units * p.S * c->cfg.q_per_kv * (c->cfg.head_dim + 2) * sizeof(float);
+  const size_t per = (size_t)c->cfg.q_per_kv * (c->cfg.head_dim + 2) * sizeof(float);
+  size_t b = (size_t)c->cfg.n_units * p.S * per;
+  if (p.fast) b += (size_t)p.pp.W * p.pp.maxseg * per;
+  return b;
 }
 
 }  // namespace

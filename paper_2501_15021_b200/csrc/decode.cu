@@ -360,17 +360,37 @@ __global__ void __launch_bounds__(kThreads) k_decode_split(DevCache c, DecodePla
 }
 
 // Merge the splits (log-sum-exp) and apply the output H (Fig. 7, R4).
+// Partials: k_decode_split's S splits per unit, then (fast path) the page
+// kernel's per-(warp, unit) segments.
 template <int D>
 __global__ void __launch_bounds__(D) k_combine(DevCache c, DecodePlan p, const float *__restrict__ ws_m,
                                                const float *__restrict__ ws_l,
-                                               const float *__restrict__ ws_o, float *__restrict__ out,
-                                               uint32_t flags) {
+                                               const float *__restrict__ ws_o,
+                                               const float *__restrict__ pg_m,
+                                               const float *__restrict__ pg_l,
+                                               const float *__restrict__ pg_o,
+                                               float *__restrict__ out, uint32_t flags) {
   __shared__ float buf[D];
   const int u = blockIdx.x, ch = threadIdx.x, g = c.g;
   const bool side_rot = c.kind == AKVQ_TSA;
+  // page-kernel warps covering unit u: items [u*P, (u+1)*P)
+  long long w_lo = 0, w_hi = -1;
+  const long long P = p.pp.n_pages, T = p.pp.T, W = p.pp.W;
+  if (p.fast && T > 0) {
+    const long long i0 = (long long)u * P, i1 = i0 + P;
+    w_lo = i0 * W / T;
+    while (w_lo > 0 && w_lo * T / W > i0) --w_lo;
+    while ((w_lo + 1) * T / W <= i0) ++w_lo;
+    w_hi = w_lo;
+    while (w_hi + 1 < W && (w_hi + 1) * T / W < i1) ++w_hi;
+  }
   for (int h = 0; h < g; ++h) {
     float M = -INFINITY;
     for (int s = 0; s < p.S; ++s) M = fmaxf(M, ws_m[((size_t)u * p.S + s) * g + h]);
+    for (long long w = w_lo; w <= w_hi; ++w) {
+      const size_t slot = (size_t)(w * p.pp.maxseg + (u - (w * T / W) / P));
+      M = fmaxf(M, pg_m[slot * g + h]);
+    }
     float rot = 0.f, org = 0.f, lsum = 0.f;
     for (int s = 0; s < p.S; ++s) {
       const size_t b = ((size_t)u * p.S + s) * g + h;
@@ -382,6 +402,14 @@ __global__ void __launch_bounds__(D) k_combine(DevCache c, DecodePlan p, const f
       const bool is_rot = s < p.n_page_splits ||
                           (s >= p.n_page_splits + p.n_ring_splits && side_rot);
       if (is_rot) rot += v; else org += v;
+    }
+    for (long long w = w_lo; w <= w_hi; ++w) {
+      const size_t slot = (size_t)(w * p.pp.maxseg + (u - (w * T / W) / P));
+      const float ms = pg_m[slot * g + h];
+      if (ms == -INFINITY) continue;
+      const float f = exp2f(ms - M);
+      lsum += f * pg_l[slot * g + h];
+      rot += f * pg_o[(slot * g + h) * D + ch];
     }
     const bool out_rot = flags & AKVQ_OUT_ROTATED;
     buf[ch] = out_rot ? org : rot;          // the part that needs a basis change
@@ -408,12 +436,22 @@ static cudaError_t launch_dec(const DevCache &c, const DecodePlan &p, const void
   float *ws_m = reinterpret_cast<float *>(ws);
   float *ws_l = ws_m + (size_t)c.U * p.S * c.g;
   float *ws_o = ws_l + (size_t)c.U * p.S * c.g;
-  const size_t smem = Smem<D>::floats(c.g) * sizeof(float);
-  auto kern = k_decode_split<D, G, DT, MAXG>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid(p.S, c.U);
-  kern<<<grid, kThreads, smem, st>>>(c, p, (const uint16_t *)q, ws_m, ws_l, ws_o);
-  k_combine<D><<<c.U, D, 0, st>>>(c, p, ws_m, ws_l, ws_o, out, flags);
+  const size_t nslot = p.fast ? (size_t)p.pp.W * p.pp.maxseg * c.g : 0;
+  float *pg_m = ws_o + (size_t)c.U * p.S * c.g * D;
+  float *pg_l = pg_m + nslot;
+  float *pg_o = pg_l + nslot;
+  if (p.S > 0) {
+    const size_t smem = Smem<D>::floats(c.g) * sizeof(float);
+    auto kern = k_decode_split<D, G, DT, MAXG>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid(p.S, c.U);
+    kern<<<grid, kThreads, smem, st>>>(c, p, (const uint16_t *)q, ws_m, ws_l, ws_o);
+  }
+  if (p.fast) {
+    const cudaError_t e = launch_decode_pages(c, DT, p.pp, q, pg_m, pg_l, pg_o, st);
+    if (e != cudaSuccess) return e;
+  }
+  k_combine<D><<<c.U, D, 0, st>>>(c, p, ws_m, ws_l, ws_o, pg_m, pg_l, pg_o, out, flags);
   return cudaGetLastError();
 }
 

@@ -15,6 +15,16 @@ struct QuantSrc {
   int ring_slots;       // 0: linear token index; >0: slot = token % ring_slots
 };
 
+// Persistent page-kernel plan: T = U * n_pages flattened (unit, page) items,
+// W warps each owning items [w*T/W, (w+1)*T/W); a warp writes one partial per
+// unit it touches into slot w*maxseg + (u - first unit of w).
+struct PagePlan {
+  long long T;
+  long long W;
+  int n_pages;
+  int maxseg;
+};
+
 // Decode split plan (host-computed, uniform across units).
 struct DecodePlan {
   int L, n_q;
@@ -22,7 +32,9 @@ struct DecodePlan {
   int pages_per_split, n_page_splits;
   int ring_per_split, n_ring_splits;
   int n_side_splits;     // side entries are shared equally among these splits
-  int S;                 // total splits
+  int S;                 // total splits of k_decode_split (ring / side / fallback pages)
+  int fast;              // 1: pages go through k_decode_pages
+  PagePlan pp;
 };
 
 cudaError_t launch_salient(const DevCache &c, const uint8_t *types, const float *colsum,
@@ -35,6 +47,11 @@ cudaError_t launch_append(const DevCache &c, const void *k, const void *v,
                           const uint8_t *types, int L, cudaStream_t st);
 cudaError_t launch_decode(const DevCache &c, int dtype16, const DecodePlan &p, const void *q,
                           float *out, void *ws, uint32_t flags, cudaStream_t st);
+cudaError_t launch_decode_pages(const DevCache &c, int dtype16, const PagePlan &pp, const void *q,
+                                float *ws_m, float *ws_l, float *ws_o, cudaStream_t st);
+int pages_fast_supported(int d, int G, int g);
+int pages_warps_per_cta();
+size_t pages_smem_bytes(int d, int G, int g, size_t page_bytes);
 cudaError_t launch_view(const DevCache &c, int dtype16, int L, int n_q, float *K, float *V,
                         cudaStream_t st);
 

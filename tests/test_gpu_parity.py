@@ -42,7 +42,7 @@ def _configs(ak, orc, w, layer, units_n, kind=None, cap=None):
 
 
 def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every=1,
-              flags=0, report=None):
+              flags=0, report=None, options=0):
     """Prefill + `steps` decode steps on the GPU for all units; the oracle runs the
     sampled `units` (default all).  Compares state after prefill and after every
     flush, outputs every `check_every` steps."""
@@ -52,7 +52,7 @@ def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every
     _, ocfg = _configs(ak, orc, w, layer, len(us), kind)
     dev = "cuda"
     inp = sy.layer_inputs(w, layer, device=dev)
-    lc = ak.LayerCache(gcfg)
+    lc = ak.LayerCache(gcfg, options=options)
     lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
     oc = orc.OracleCache(ocfg)
     inp_o = sy.layer_inputs(w, layer, units=us, device="cpu")
@@ -92,11 +92,12 @@ def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every
 
 
 # ----------------------------------------------------------------- tiny (BJ:7)
+@pytest.mark.parametrize("options", [0, 1], ids=["dp4a-pages", "generic-pages"])
 @pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
-def test_tiny_prefill_decode_and_flush(ak, orc, sy, kind):
+def test_tiny_prefill_decode_and_flush(ak, orc, sy, kind, options):
     """Quantize once, 4 decode steps, extended to 16 steps across the L = 104 flush."""
     w = sy.TINY
-    lc, oc, worst = _run_case(ak, orc, sy, w, 0, kind=kind, steps=16)
+    lc, oc, worst = _run_case(ak, orc, sy, w, 0, kind=kind, steps=16, options=options)
     assert lc.L == 112 and lc.n_q == 96
 
 
@@ -111,12 +112,13 @@ def test_tiny_view_and_rotated_output(ak, orc, sy):
 
 
 # ----------------------------------------------------------------- 7B shape (BJ:8)
+@pytest.mark.parametrize("options", [0, 1], ids=["dp4a-pages", "generic-pages"])
 @pytest.mark.parametrize("layer", [0, 2], ids=["TSA-L0", "PSA-L2"])
-def test_llava7b_layer_full(ak, orc, sy, layer):
+def test_llava7b_layer_full(ak, orc, sy, layer, options):
     """All 32 units; decode across the L = 672 flush (n_q 512 -> 640)."""
     w = sy.LLAVA7B
     rep = {}
-    lc, oc, worst = _run_case(ak, orc, sy, w, layer, steps=3, report=rep)
+    lc, oc, worst = _run_case(ak, orc, sy, w, layer, steps=3, report=rep, options=options)
     assert lc.n_q == 640
     print("ties", rep, "worst", worst)
 
