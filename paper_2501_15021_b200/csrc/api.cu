@@ -79,18 +79,41 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
     p.n_side_splits = bound > 0 ? (bound + 511) / 512 : 0;
     if (p.n_side_splits > 8) p.n_side_splits = 8;
   }
-  // fast path: the quantized pages go through the persistent dp4a page kernel
+  // fast path: 2-bit pages through the persistent dp4a page kernel, 16-bit /
+  // 4-bit rows through the persistent row kernel, warp-per-unit combine
   p.fast = 0;
-  p.pp.T = 0; p.pp.W = 0; p.pp.n_pages = p.n_pages; p.pp.maxseg = 0;
-  if (p.n_pages > 0 && !(c->options & AKVQ_OPT_GENERIC_PAGES) &&
+  memset(&p.pp, 0, sizeof(p.pp));
+  memset(&p.rp, 0, sizeof(p.rp));
+  p.pp.n_pages = p.n_pages > 0 ? p.n_pages : 1;
+  p.rp.items_per_unit = 1;
+  if (!(c->options & AKVQ_OPT_GENERIC_PAGES) &&
       pages_fast_supported(f.head_dim, f.group, f.q_per_kv)) {
     p.fast = 1;
-    p.n_page_splits = 0;
-    p.pp.T = (long long)f.n_units * p.n_pages;
-    const long long wmax = (long long)sms * 2 * pages_warps_per_cta();
-    p.pp.W = p.pp.T < wmax ? p.pp.T : wmax;
-    const long long per = (p.pp.T + p.pp.W - 1) / p.pp.W;
-    p.pp.maxseg = (int)((per + p.n_pages - 1) / p.n_pages + 1);
+    if (p.n_pages > 0) {
+      p.pp.T = (long long)f.n_units * p.n_pages;
+      const long long wmax = (long long)sms * 2 * pages_warps_per_cta();
+      p.pp.W = p.pp.T < wmax ? p.pp.T : wmax;
+      const long long per = (p.pp.T + p.pp.W - 1) / p.pp.W;
+      p.pp.maxseg = (int)((per + p.n_pages - 1) / p.n_pages + 1);
+    }
+    const int ch = rows_chunk();
+    p.rp.L = L;
+    p.rp.n_q = n_q;
+    p.rp.n_ring_chunks = (L - n_q + ch - 1) / ch;
+    if (f.kind == AKVQ_PSA) p.rp.n_side_splits = (f.top_k > 0 && n_q > 0) ? 1 : 0;
+    else p.rp.n_side_splits = n_q > 0 ? (n_q + 1023) / 1024 : 0;
+    if (p.rp.n_side_splits > 8) p.rp.n_side_splits = 8;
+    p.rp.items_per_unit = p.rp.n_ring_chunks + p.rp.n_side_splits;
+    if (p.rp.items_per_unit > 0) {
+      p.rp.T = (long long)f.n_units * p.rp.items_per_unit;
+      const long long wmax = (long long)sms * 3 * rows_warps_per_cta();
+      p.rp.W = p.rp.T < wmax ? p.rp.T : wmax;
+      const long long per = (p.rp.T + p.rp.W - 1) / p.rp.W;
+      p.rp.maxseg = (int)((per + p.rp.items_per_unit - 1) / p.rp.items_per_unit + 1);
+    } else {
+      p.rp.items_per_unit = 1;
+    }
+    p.n_page_splits = p.n_ring_splits = p.n_side_splits = 0;
   }
   p.S = p.n_page_splits + p.n_ring_splits + p.n_side_splits;
   return p;
@@ -99,7 +122,10 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
 size_t ws_bytes_for(const akvq_cache *c, const DecodePlan &p) {
   const size_t per = (size_t)c->cfg.q_per_kv * (c->cfg.head_dim + 2) * sizeof(float);
   size_t b = (size_t)c->cfg.n_units * p.S * per;
-  if (p.fast) b += (size_t)p.pp.W * p.pp.maxseg * per;
+  if (p.fast) {
+    b += (size_t)p.pp.W * p.pp.maxseg * per;
+    b += (size_t)p.rp.W * p.rp.maxseg * (per + (size_t)c->cfg.q_per_kv * c->cfg.head_dim * 4);
+  }
   return b;
 }
 
@@ -248,7 +274,7 @@ size_t akvq_decode_workspace_bytes_max(const akvq_cache *c) {
   if (!c) return 0;
   size_t best = 0;
   const akvq_config &f = c->cfg;
-  for (int L = 1; L <= f.capacity; L += (L < f.capacity - f.group ? f.group : 1)) {
+  for (int L = 1; L <= f.capacity; ++L) {     // plans are cheap; the size is not monotone in L
     const int n_q = L > f.residual ? (L - f.residual) / f.group * f.group : 0;
     const size_t b = ws_bytes_for(c, plan_decode(c, L, n_q));
     if (b > best) best = b;

@@ -430,6 +430,103 @@ __global__ void __launch_bounds__(D) k_combine(DevCache c, DecodePlan p, const f
   }
 }
 
+// Warp-per-unit combine for the fast path: merges the page kernel's segments
+// (rotated basis) and the row kernel's segments (original + rotated basis) by
+// log-sum-exp, then applies the output H with an in-register / shuffle FWHT.
+__device__ __forceinline__ void seg_range(long long T, long long W, long long P, int u,
+                                          long long &w_lo, long long &w_hi) {
+  w_lo = 0; w_hi = -1;
+  if (T <= 0) return;
+  const long long i0 = (long long)u * P, i1 = i0 + P;
+  w_lo = i0 * W / T;
+  while (w_lo > 0 && w_lo * T / W > i0) --w_lo;
+  while ((w_lo + 1) * T / W <= i0) ++w_lo;
+  w_hi = w_lo;
+  while (w_hi + 1 < W && (w_hi + 1) * T / W < i1) ++w_hi;
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) k_combine_fast(DevCache c, DecodePlan p,
+                                                      const float *__restrict__ pg_m,
+                                                      const float *__restrict__ pg_l,
+                                                      const float *__restrict__ pg_o,
+                                                      const float *__restrict__ rw_m,
+                                                      const float *__restrict__ rw_l,
+                                                      const float *__restrict__ rw_o,
+                                                      float *__restrict__ out, uint32_t flags) {
+  constexpr int CPL = D / 32;                    // channels per lane (contiguous)
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (u >= c.U) return;
+  const int g = c.g;
+  long long pw0, pw1, rw0, rw1;
+  seg_range(p.pp.T, p.pp.W, p.pp.n_pages, u, pw0, pw1);
+  seg_range(p.rp.T, p.rp.W, p.rp.items_per_unit, u, rw0, rw1);
+  for (int h = 0; h < g; ++h) {
+    float M = -INFINITY;
+    for (long long w = pw0; w <= pw1; ++w) {
+      const size_t slot = (size_t)(w * p.pp.maxseg + (u - (w * p.pp.T / p.pp.W) / p.pp.n_pages));
+      M = fmaxf(M, pg_m[slot * g + h]);
+    }
+    for (long long w = rw0; w <= rw1; ++w) {
+      const size_t slot = (size_t)(w * p.rp.maxseg + (u - (w * p.rp.T / p.rp.W) / p.rp.items_per_unit));
+      M = fmaxf(M, rw_m[slot * g + h]);
+    }
+    float rot[CPL], org[CPL], lsum = 0.f;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) { rot[k] = 0.f; org[k] = 0.f; }
+    for (long long w = pw0; w <= pw1; ++w) {
+      const size_t slot = (size_t)(w * p.pp.maxseg + (u - (w * p.pp.T / p.pp.W) / p.pp.n_pages));
+      const float ms = pg_m[slot * g + h];
+      if (ms == -INFINITY) continue;
+      const float f = exp2f(ms - M);
+      lsum += f * pg_l[slot * g + h];
+      const float *src = pg_o + (slot * g + h) * D + CPL * lane;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) rot[k] = fmaf(f, src[k], rot[k]);
+    }
+    for (long long w = rw0; w <= rw1; ++w) {
+      const size_t slot = (size_t)(w * p.rp.maxseg + (u - (w * p.rp.T / p.rp.W) / p.rp.items_per_unit));
+      const float ms = rw_m[slot * g + h];
+      if (ms == -INFINITY) continue;
+      const float f = exp2f(ms - M);
+      lsum += f * rw_l[slot * g + h];
+      const float *src = rw_o + (slot * g + h) * 2 * D + CPL * lane;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        org[k] = fmaf(f, src[k], org[k]);
+        rot[k] = fmaf(f, src[D + k], rot[k]);
+      }
+    }
+    const bool out_rot = flags & AKVQ_OUT_ROTATED;
+    float x[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) x[k] = out_rot ? org[k] : rot[k];
+    // FWHT over D channels: lane holds channels CPL*lane .. CPL*lane+CPL-1
+#pragma unroll
+    for (int hs = 1; hs < CPL; hs <<= 1)
+#pragma unroll
+      for (int k = 0; k < CPL; ++k)
+        if (!(k & hs)) { const float a = x[k], b = x[k + hs]; x[k] = a + b; x[k + hs] = a - b; }
+#pragma unroll
+    for (int lm = 1; lm < 32; lm <<= 1) {
+      const bool upper = lane & lm;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        const float o = __shfl_xor_sync(0xffffffffu, x[k], lm);
+        x[k] = upper ? o - x[k] : x[k] + o;
+      }
+    }
+    const float inv = 1.f / lsum;
+    float *dst = out + ((size_t)u * g + h) * D + CPL * lane;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const float tr = x[k] * c.inv_sqrt_d;
+      dst[k] = (out_rot ? rot[k] + tr : tr + org[k]) * inv;
+    }
+  }
+}
+
 template <int D, int G, int DT, int MAXG>
 static cudaError_t launch_dec(const DevCache &c, const DecodePlan &p, const void *q, float *out,
                               void *ws, uint32_t flags, cudaStream_t st) {
@@ -448,8 +545,16 @@ static cudaError_t launch_dec(const DevCache &c, const DecodePlan &p, const void
     kern<<<grid, kThreads, smem, st>>>(c, p, (const uint16_t *)q, ws_m, ws_l, ws_o);
   }
   if (p.fast) {
-    const cudaError_t e = launch_decode_pages(c, DT, p.pp, q, pg_m, pg_l, pg_o, st);
+    const size_t rslot = (size_t)p.rp.W * p.rp.maxseg * c.g;
+    float *rw_m = pg_o + nslot * D;
+    float *rw_l = rw_m + rslot;
+    float *rw_o = rw_l + rslot;
+    cudaError_t e = launch_decode_rows(c, DT, p.rp, q, rw_m, rw_l, rw_o, st);
+    if (e == cudaSuccess) e = launch_decode_pages(c, DT, p.pp, q, pg_m, pg_l, pg_o, st);
     if (e != cudaSuccess) return e;
+    k_combine_fast<D><<<(c.U + 3) / 4, 128, 0, st>>>(c, p, pg_m, pg_l, pg_o, rw_m, rw_l, rw_o, out,
+                                                    flags);
+    return cudaGetLastError();
   }
   k_combine<D><<<c.U, D, 0, st>>>(c, p, ws_m, ws_l, ws_o, pg_m, pg_l, pg_o, out, flags);
   return cudaGetLastError();

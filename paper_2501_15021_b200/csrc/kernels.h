@@ -25,6 +25,19 @@ struct PagePlan {
   int maxseg;
 };
 
+// Persistent row-kernel plan: per unit, n_ring_chunks items of 16 ring tokens
+// then n_side_splits items sharing the unit's side entries; same segment /
+// partial-slot scheme as PagePlan (partials hold o_org and o_rot).
+struct RowPlan {
+  long long T;
+  long long W;
+  int items_per_unit;
+  int n_ring_chunks;
+  int n_side_splits;
+  int maxseg;
+  int L, n_q;
+};
+
 // Decode split plan (host-computed, uniform across units).
 struct DecodePlan {
   int L, n_q;
@@ -33,8 +46,9 @@ struct DecodePlan {
   int ring_per_split, n_ring_splits;
   int n_side_splits;     // side entries are shared equally among these splits
   int S;                 // total splits of k_decode_split (ring / side / fallback pages)
-  int fast;              // 1: pages go through k_decode_pages
+  int fast;              // 1: pages through k_decode_pages, rows through k_decode_rows
   PagePlan pp;
+  RowPlan rp;
 };
 
 cudaError_t launch_salient(const DevCache &c, const uint8_t *types, const float *colsum,
@@ -50,6 +64,10 @@ cudaError_t launch_decode(const DevCache &c, int dtype16, const DecodePlan &p, c
 cudaError_t launch_decode_pages(const DevCache &c, int dtype16, const PagePlan &pp, const void *q,
                                 float *ws_m, float *ws_l, float *ws_o, cudaStream_t st);
 int pages_fast_supported(int d, int G, int g);
+cudaError_t launch_decode_rows(const DevCache &c, int dtype16, const RowPlan &rp, const void *q,
+                               float *ws_m, float *ws_l, float *ws_o, cudaStream_t st);
+int rows_chunk();
+int rows_warps_per_cta();
 int pages_warps_per_cta();
 size_t pages_smem_bytes(int d, int G, int g, size_t page_bytes);
 cudaError_t launch_view(const DevCache &c, int dtype16, int L, int n_q, float *K, float *V,
