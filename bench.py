@@ -288,14 +288,14 @@ def main():
     def one_step(q, k, v, types, ev=None):
         for layer, lc in enumerate(caches):
             nq = lc.n_q
-            lc.append(k[layer], v[layer], types)
-            launches[0] += 1 + (lc.n_q != nq)
             if ev is not None:
                 ev[layer][0].record()
-            lc.decode(q[layer], out=outs[layer])
+            # append + decode attention through the C ABI (one fused launch when
+            # no block flush is due; append + quantize + decode when it is)
+            lc.step(k[layer], v[layer], q[layer], types, out=outs[layer])
             if ev is not None:
                 ev[layer][1].record()
-            launches[0] += 2
+            launches[0] += 1 if lc.n_q == nq else 3
             if gath is not None:
                 dist.all_gather_into_tensor(gath[layer], outs[layer])
 
@@ -408,7 +408,7 @@ def main():
             "attention_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                         "traffic": None, "kernel": "k_decode_split + k_combine",
+                         "traffic": None, "kernel": "k_decode_fused (append + attention + merge)",
                          "bytes_per_launch": dec_bytes, "launch_ms": dec_ms,
                          "peak_src": peaks["src"]},
             "prefill": {"ms_all_layers": pre_ms, "quantize_gbs": pre_bytes / (pre_ms * 1e-3) / 1e9,

@@ -102,6 +102,8 @@ typedef struct {
  *            TSA: +0 kscale f32[ng], kzero i32[ng], vscale f32[ng],
  *                 vzero i32[ng], then K codes u8[d/2], V codes u8[d/2]
  *                 (4-bit, 2 per byte, low nibble first; clip4, R11)
+ *  ticket  [U] u32                     per-unit merge tickets of the fused
+ *                                      decode (zeroed at init, self-resetting)
  *  side_cap = top_k (PSA) or cap (TSA).
  */
 typedef struct {
@@ -112,6 +114,7 @@ typedef struct {
   uint64_t bitmask_off;
   uint64_t side_idx_off, side_cnt_off;
   uint64_t side_off, side_entry_bytes;
+  uint64_t ticket_off;
   int32_t cap, n_pages, slots, bitmask_words, side_cap, ng;
 } akvq_layout;
 
@@ -194,6 +197,16 @@ size_t akvq_decode_workspace_bytes_max(const akvq_cache *c);
 akvq_status akvq_decode_attention(const akvq_cache *c, const void *q, float *out,
                                   void *ws, size_t ws_bytes, uint32_t flags,
                                   akvq_stream_t stream);
+
+/* One decode step = append (Eq. 2) + attention, fused into one launch when
+ * no block flush is due (akvq_append_token + akvq_decode_attention otherwise;
+ * results are identical).  k, v [U][d], types [U] (NULL = vision), q
+ * [U][g][d] 16-bit; out [U][g][d] f32; ws >= akvq_decode_workspace_bytes_max.
+ * Errors: ECAPACITY (L == capacity or ws too small; nothing changes), EINVAL. */
+akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v,
+                             const uint8_t *types, const void *q, float *out,
+                             void *ws, size_t ws_bytes, uint32_t flags,
+                             akvq_stream_t stream);
 
 /* ---------------------------------------------------------------- hooks */
 /* Saliency only (classify_tokens): writes bitmask bits [0, L0).

@@ -28,7 +28,7 @@ EXPORTS = (
     "akvq_cache_layout", "akvq_cache_bytes", "akvq_cache_init", "akvq_rotate_quantize",
     "akvq_append_token", "akvq_decode_workspace_bytes", "akvq_decode_workspace_bytes_max",
     "akvq_decode_attention", "akvq_select_salient", "akvq_dequantize_view",
-    "akvq_memory_report", "akvq_status_str", "akvq_version",
+    "akvq_memory_report", "akvq_status_str", "akvq_version", "akvq_decode_step",
 )
 
 
@@ -49,7 +49,7 @@ class akvq_layout(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "total_bytes", "pages_off", "page_bytes", "pg_kscale", "pg_kzero", "pg_kcodes",
         "pg_vscale", "pg_vzero", "pg_vcodes", "ring_off", "ring_unit_bytes", "bitmask_off",
-        "side_idx_off", "side_cnt_off", "side_off", "side_entry_bytes")] + [
+        "side_idx_off", "side_cnt_off", "side_off", "side_entry_bytes", "ticket_off")] + [
         (n, C.c_int32) for n in ("cap", "n_pages", "slots", "bitmask_words", "side_cap", "ng")]
 
 
@@ -97,6 +97,9 @@ def lib() -> C.CDLL:
         L.akvq_decode_attention.argtypes = [C.POINTER(akvq_cache), P, P, P, C.c_size_t,
                                             C.c_uint32, P]
         L.akvq_decode_attention.restype = S
+        L.akvq_decode_step.argtypes = [C.POINTER(akvq_cache), P, P, P, P, P, P, C.c_size_t,
+                                       C.c_uint32, P]
+        L.akvq_decode_step.restype = S
         L.akvq_select_salient.argtypes = [C.POINTER(akvq_cache), P, P, C.c_int32, P]
         L.akvq_select_salient.restype = S
         L.akvq_dequantize_view.argtypes = [C.POINTER(akvq_cache), P, P, P]
@@ -185,6 +188,12 @@ def akvq_decode_attention(cache, q, out, ws, flags=0, stream=None):
                                        _stream(stream)), "akvq_decode_attention")
 
 
+def akvq_decode_step(cache, k, v, types, q, out, ws, flags=0, stream=None):
+    _check(lib().akvq_decode_step(C.byref(cache), _ptr(k), _ptr(v), _ptr(types), _ptr(q),
+                                  _ptr(out), _ptr(ws), ws.numel() * ws.element_size(), int(flags),
+                                  _stream(stream)), "akvq_decode_step")
+
+
 def akvq_select_salient(cache, types, colsum, L0, stream=None):
     _check(lib().akvq_select_salient(C.byref(cache), _ptr(types), _ptr(colsum), int(L0),
                                      _stream(stream)), "akvq_select_salient")
@@ -234,6 +243,13 @@ class LayerCache:
         if out is None:
             out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
         akvq_decode_attention(self.handle, q, out, self.ws, flags, stream)
+        return out
+
+    def step(self, k, v, q, types=None, out=None, flags=0, stream=None):
+        """append (k, v) then attend with q, fused into one launch when possible"""
+        if out is None:
+            out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+        akvq_decode_step(self.handle, k, v, types, q, out, self.ws, flags, stream)
         return out
 
     def view(self, stream=None):

@@ -41,6 +41,7 @@ DevCache make_dev(const akvq_cache *c) {
   d.side_idx = reinterpret_cast<int32_t *>(b + y.side_idx_off);
   d.side_cnt = reinterpret_cast<int32_t *>(b + y.side_cnt_off);
   d.side = b + y.side_off;
+  d.ticket = reinterpret_cast<uint32_t *>(b + y.ticket_off);
   d.page_bytes = (uint32_t)y.page_bytes;
   d.pg_kscale = (uint32_t)y.pg_kscale; d.pg_kzero = (uint32_t)y.pg_kzero;
   d.pg_kcodes = (uint32_t)y.pg_kcodes; d.pg_vscale = (uint32_t)y.pg_vscale;
@@ -79,40 +80,40 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
     p.n_side_splits = bound > 0 ? (bound + 511) / 512 : 0;
     if (p.n_side_splits > 8) p.n_side_splits = 8;
   }
-  // fast path: 2-bit pages through the persistent dp4a page kernel, 16-bit /
-  // 4-bit rows through the persistent row kernel, warp-per-unit combine
-  p.fast = 0;
-  memset(&p.pp, 0, sizeof(p.pp));
-  memset(&p.rp, 0, sizeof(p.rp));
-  p.pp.n_pages = p.n_pages > 0 ? p.n_pages : 1;
-  p.rp.items_per_unit = 1;
+  // fused path: the whole decode in one persistent kernel (k_decode_fused)
+  p.fused = 0;
+  memset(&p.fp, 0, sizeof(p.fp));
   if (!(c->options & AKVQ_OPT_GENERIC_PAGES) &&
-      pages_fast_supported(f.head_dim, f.group, f.q_per_kv)) {
-    p.fast = 1;
-    if (p.n_pages > 0) {
-      p.pp.T = (long long)f.n_units * p.n_pages;
-      const long long wmax = (long long)sms * 2 * pages_warps_per_cta();
-      p.pp.W = p.pp.T < wmax ? p.pp.T : wmax;
-      const long long per = (p.pp.T + p.pp.W - 1) / p.pp.W;
-      p.pp.maxseg = (int)((per + p.n_pages - 1) / p.n_pages + 1);
-    }
-    const int ch = rows_chunk();
-    p.rp.L = L;
-    p.rp.n_q = n_q;
-    p.rp.n_ring_chunks = (L - n_q + ch - 1) / ch;
-    if (f.kind == AKVQ_PSA) p.rp.n_side_splits = (f.top_k > 0 && n_q > 0) ? 1 : 0;
-    else p.rp.n_side_splits = n_q > 0 ? (n_q + 1023) / 1024 : 0;
-    if (p.rp.n_side_splits > 8) p.rp.n_side_splits = 8;
-    p.rp.items_per_unit = p.rp.n_ring_chunks + p.rp.n_side_splits;
-    if (p.rp.items_per_unit > 0) {
-      p.rp.T = (long long)f.n_units * p.rp.items_per_unit;
-      const long long wmax = (long long)sms * 3 * rows_warps_per_cta();
-      p.rp.W = p.rp.T < wmax ? p.rp.T : wmax;
-      const long long per = (p.rp.T + p.rp.W - 1) / p.rp.W;
-      p.rp.maxseg = (int)((per + p.rp.items_per_unit - 1) / p.rp.items_per_unit + 1);
-    } else {
-      p.rp.items_per_unit = 1;
-    }
+      fused_supported(f.head_dim, f.group, f.q_per_kv)) {
+    const akvq_layout &y = c->lay;
+    FusedPlan &fp = p.fp;
+    const int RC = FusedPlan::kRowChunk;
+    fp.L = L;
+    fp.n_q = n_q;
+    fp.P = p.n_pages;
+    fp.NR = (L - n_q + RC - 1) / RC;
+    if (f.kind == AKVQ_PSA) fp.NS = (f.top_k > 0 && n_q > 0) ? 1 : 0;
+    else fp.NS = n_q > 0 ? ((n_q + 1023) / 1024 < 8 ? (n_q + 1023) / 1024 : 8) : 0;
+    // costs ~ bytes / 512 of each item's loads
+    fp.cp = (int)((y.page_bytes + 511) / 512);
+    fp.cr = (int)((RC * 4 * f.head_dim + 511) / 512);
+    fp.cs = f.kind == AKVQ_PSA ? fp.cr * ((f.top_k + RC - 1) / RC) : 2 * fp.cr;
+    if (fp.cp < 1) fp.cp = 1;
+    if (fp.cr < 1) fp.cr = 1;
+    if (fp.cs < 1) fp.cs = 1;
+    fp.cost_unit = fp.P * fp.cp + fp.NR * fp.cr + fp.NS * fp.cs;
+    if (fp.cost_unit < 1) fp.cost_unit = 1;
+    fp.T = (long long)f.n_units * fp.cost_unit;
+    const long long items = (long long)f.n_units * (fp.P + fp.NR + fp.NS);
+    long long W = (long long)sms * 3 * fused_warps_per_cta();
+    if (W > items) W = items > 0 ? items : 1;
+    if (W > fp.T) W = fp.T;
+    fp.W = W;
+    const long long per = (fp.T + W - 1) / W;
+    fp.maxseg = (int)((per + fp.cost_unit - 1) / fp.cost_unit + 1);
+    fp.stage_bytes = fused_stage_bytes(f.head_dim, f.group, y.page_bytes, y.pg_vscale,
+                                       y.side_entry_bytes);
+    p.fused = 1;
     p.n_page_splits = p.n_ring_splits = p.n_side_splits = 0;
   }
   p.S = p.n_page_splits + p.n_ring_splits + p.n_side_splits;
@@ -120,13 +121,9 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
 }
 
 size_t ws_bytes_for(const akvq_cache *c, const DecodePlan &p) {
-  const size_t per = (size_t)c->cfg.q_per_kv * (c->cfg.head_dim + 2) * sizeof(float);
-  size_t b = (size_t)c->cfg.n_units * p.S * per;
-  if (p.fast) {
-    b += (size_t)p.pp.W * p.pp.maxseg * per;
-    b += (size_t)p.rp.W * p.rp.maxseg * (per + (size_t)c->cfg.q_per_kv * c->cfg.head_dim * 4);
-  }
-  return b;
+  const size_t g = c->cfg.q_per_kv, d = c->cfg.head_dim;
+  if (p.fused) return (size_t)p.fp.W * p.fp.maxseg * g * (2 * d + 4) * sizeof(float);
+  return (size_t)c->cfg.n_units * p.S * g * (d + 2) * sizeof(float);
 }
 
 }  // namespace
@@ -163,6 +160,7 @@ akvq_status akvq_cache_layout(const akvq_config *f, akvq_layout *y) {
   y->side_cnt_off = t; t = align_up(t + U * 4, 256);
   y->side_entry_bytes = f->kind == AKVQ_PSA ? 4 * d : align_up(d + 16 * ng, 16);
   y->side_off = t;     t = align_up(t + U * y->side_cap * y->side_entry_bytes, 256);
+  y->ticket_off = t;   t = align_up(t + U * 4, 256);
   y->total_bytes = t;
   return AKVQ_OK;
 }
@@ -191,6 +189,7 @@ akvq_status akvq_cache_init(akvq_cache *c, const akvq_config *f, void *dev_buf, 
   uint8_t *b = static_cast<uint8_t *>(dev_buf);
   cudaMemsetAsync(b + y.bitmask_off, 0, (size_t)f->n_units * y.bitmask_words * 4, s);
   cudaMemsetAsync(b + y.side_cnt_off, 0, (size_t)f->n_units * 4, s);
+  cudaMemsetAsync(b + y.ticket_off, 0, (size_t)f->n_units * 4, s);
   if (y.side_cap > 0)
     cudaMemsetAsync(b + y.side_idx_off, 0xff, (size_t)f->n_units * y.side_cap * 4, s);
   return cuda_status(cudaGetLastError());
@@ -291,8 +290,35 @@ akvq_status akvq_decode_attention(const akvq_cache *c, const void *q, float *out
   const DecodePlan p = plan_decode(c, c->L, c->n_q);
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
   const DevCache d = make_dev(c);
-  return cuda_status(launch_decode(d, c->cfg.dtype16, p, q, out, ws, flags,
-                                   reinterpret_cast<cudaStream_t>(stream)));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (p.fused)
+    return cuda_status(launch_decode_fused(d, c->cfg.dtype16, p.fp, q, nullptr, nullptr, nullptr,
+                                           static_cast<float *>(ws), out, flags, s));
+  return cuda_status(launch_decode(d, c->cfg.dtype16, p, q, out, ws, flags, s));
+}
+
+akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const uint8_t *types,
+                             const void *q, float *out, void *ws, size_t ws_bytes, uint32_t flags,
+                             akvq_stream_t stream) {
+  if (!c || !c->base || !k || !v || !q || !out || !ws) return AKVQ_EINVAL;
+  const akvq_config &f = c->cfg;
+  if (c->L >= f.capacity) return AKVQ_ECAPACITY;
+  const int L1 = c->L + 1;
+  const bool flush = L1 - f.residual - c->n_q >= f.group;
+  const DecodePlan p = plan_decode(c, L1, flush ? c->n_q + f.group : c->n_q);
+  if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
+  if (flush || !p.fused) {              // flush step (every G tokens) or generic path
+    akvq_status st = akvq_append_token(c, k, v, types, stream);
+    if (st != AKVQ_OK) return st;
+    return akvq_decode_attention(c, q, out, ws, ws_bytes, flags, stream);
+  }
+  const DevCache d = make_dev(c);
+  const cudaError_t e = launch_decode_fused(d, f.dtype16, p.fp, q, k, v, types,
+                                            static_cast<float *>(ws), out, flags,
+                                            reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return AKVQ_ECUDA;
+  c->L = L1;
+  return AKVQ_OK;
 }
 
 akvq_status akvq_dequantize_view(const akvq_cache *c, float *K, float *V, akvq_stream_t stream) {

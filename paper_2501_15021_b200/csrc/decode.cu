@@ -359,38 +359,19 @@ __global__ void __launch_bounds__(kThreads) k_decode_split(DevCache c, DecodePla
   }
 }
 
-// Merge the splits (log-sum-exp) and apply the output H (Fig. 7, R4).
-// Partials: k_decode_split's S splits per unit, then (fast path) the page
-// kernel's per-(warp, unit) segments.
+// Merge the splits of k_decode_split (log-sum-exp) and apply the output H
+// (Fig. 7, R4).  Generic path (k_decode_fused merges in-kernel).
 template <int D>
 __global__ void __launch_bounds__(D) k_combine(DevCache c, DecodePlan p, const float *__restrict__ ws_m,
                                                const float *__restrict__ ws_l,
-                                               const float *__restrict__ ws_o,
-                                               const float *__restrict__ pg_m,
-                                               const float *__restrict__ pg_l,
-                                               const float *__restrict__ pg_o,
-                                               float *__restrict__ out, uint32_t flags) {
+                                               const float *__restrict__ ws_o, float *__restrict__ out,
+                                               uint32_t flags) {
   __shared__ float buf[D];
   const int u = blockIdx.x, ch = threadIdx.x, g = c.g;
   const bool side_rot = c.kind == AKVQ_TSA;
-  // page-kernel warps covering unit u: items [u*P, (u+1)*P)
-  long long w_lo = 0, w_hi = -1;
-  const long long P = p.pp.n_pages, T = p.pp.T, W = p.pp.W;
-  if (p.fast && T > 0) {
-    const long long i0 = (long long)u * P, i1 = i0 + P;
-    w_lo = i0 * W / T;
-    while (w_lo > 0 && w_lo * T / W > i0) --w_lo;
-    while ((w_lo + 1) * T / W <= i0) ++w_lo;
-    w_hi = w_lo;
-    while (w_hi + 1 < W && (w_hi + 1) * T / W < i1) ++w_hi;
-  }
   for (int h = 0; h < g; ++h) {
     float M = -INFINITY;
     for (int s = 0; s < p.S; ++s) M = fmaxf(M, ws_m[((size_t)u * p.S + s) * g + h]);
-    for (long long w = w_lo; w <= w_hi; ++w) {
-      const size_t slot = (size_t)(w * p.pp.maxseg + (u - (w * T / W) / P));
-      M = fmaxf(M, pg_m[slot * g + h]);
-    }
     float rot = 0.f, org = 0.f, lsum = 0.f;
     for (int s = 0; s < p.S; ++s) {
       const size_t b = ((size_t)u * p.S + s) * g + h;
@@ -403,22 +384,13 @@ __global__ void __launch_bounds__(D) k_combine(DevCache c, DecodePlan p, const f
                           (s >= p.n_page_splits + p.n_ring_splits && side_rot);
       if (is_rot) rot += v; else org += v;
     }
-    for (long long w = w_lo; w <= w_hi; ++w) {
-      const size_t slot = (size_t)(w * p.pp.maxseg + (u - (w * T / W) / P));
-      const float ms = pg_m[slot * g + h];
-      if (ms == -INFINITY) continue;
-      const float f = exp2f(ms - M);
-      lsum += f * pg_l[slot * g + h];
-      rot += f * pg_o[(slot * g + h) * D + ch];
-    }
     const bool out_rot = flags & AKVQ_OUT_ROTATED;
     buf[ch] = out_rot ? org : rot;          // the part that needs a basis change
     __syncthreads();
     for (int hs = 1; hs < D; hs <<= 1) {
-      float v = 0.f;
       const int i = ch & ~hs;
       const float a = buf[i], b2 = buf[i | hs];
-      v = (ch & hs) ? a - b2 : a + b2;
+      const float v = (ch & hs) ? a - b2 : a + b2;
       __syncthreads();
       buf[ch] = v;
       __syncthreads();
@@ -430,133 +402,18 @@ __global__ void __launch_bounds__(D) k_combine(DevCache c, DecodePlan p, const f
   }
 }
 
-// Warp-per-unit combine for the fast path: merges the page kernel's segments
-// (rotated basis) and the row kernel's segments (original + rotated basis) by
-// log-sum-exp, then applies the output H with an in-register / shuffle FWHT.
-__device__ __forceinline__ void seg_range(long long T, long long W, long long P, int u,
-                                          long long &w_lo, long long &w_hi) {
-  w_lo = 0; w_hi = -1;
-  if (T <= 0) return;
-  const long long i0 = (long long)u * P, i1 = i0 + P;
-  w_lo = i0 * W / T;
-  while (w_lo > 0 && w_lo * T / W > i0) --w_lo;
-  while ((w_lo + 1) * T / W <= i0) ++w_lo;
-  w_hi = w_lo;
-  while (w_hi + 1 < W && (w_hi + 1) * T / W < i1) ++w_hi;
-}
-
-template <int D>
-__global__ void __launch_bounds__(128) k_combine_fast(DevCache c, DecodePlan p,
-                                                      const float *__restrict__ pg_m,
-                                                      const float *__restrict__ pg_l,
-                                                      const float *__restrict__ pg_o,
-                                                      const float *__restrict__ rw_m,
-                                                      const float *__restrict__ rw_l,
-                                                      const float *__restrict__ rw_o,
-                                                      float *__restrict__ out, uint32_t flags) {
-  constexpr int CPL = D / 32;                    // channels per lane (contiguous)
-  const int lane = threadIdx.x & 31;
-  const int u = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (u >= c.U) return;
-  const int g = c.g;
-  long long pw0, pw1, rw0, rw1;
-  seg_range(p.pp.T, p.pp.W, p.pp.n_pages, u, pw0, pw1);
-  seg_range(p.rp.T, p.rp.W, p.rp.items_per_unit, u, rw0, rw1);
-  for (int h = 0; h < g; ++h) {
-    float M = -INFINITY;
-    for (long long w = pw0; w <= pw1; ++w) {
-      const size_t slot = (size_t)(w * p.pp.maxseg + (u - (w * p.pp.T / p.pp.W) / p.pp.n_pages));
-      M = fmaxf(M, pg_m[slot * g + h]);
-    }
-    for (long long w = rw0; w <= rw1; ++w) {
-      const size_t slot = (size_t)(w * p.rp.maxseg + (u - (w * p.rp.T / p.rp.W) / p.rp.items_per_unit));
-      M = fmaxf(M, rw_m[slot * g + h]);
-    }
-    float rot[CPL], org[CPL], lsum = 0.f;
-#pragma unroll
-    for (int k = 0; k < CPL; ++k) { rot[k] = 0.f; org[k] = 0.f; }
-    for (long long w = pw0; w <= pw1; ++w) {
-      const size_t slot = (size_t)(w * p.pp.maxseg + (u - (w * p.pp.T / p.pp.W) / p.pp.n_pages));
-      const float ms = pg_m[slot * g + h];
-      if (ms == -INFINITY) continue;
-      const float f = exp2f(ms - M);
-      lsum += f * pg_l[slot * g + h];
-      const float *src = pg_o + (slot * g + h) * D + CPL * lane;
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) rot[k] = fmaf(f, src[k], rot[k]);
-    }
-    for (long long w = rw0; w <= rw1; ++w) {
-      const size_t slot = (size_t)(w * p.rp.maxseg + (u - (w * p.rp.T / p.rp.W) / p.rp.items_per_unit));
-      const float ms = rw_m[slot * g + h];
-      if (ms == -INFINITY) continue;
-      const float f = exp2f(ms - M);
-      lsum += f * rw_l[slot * g + h];
-      const float *src = rw_o + (slot * g + h) * 2 * D + CPL * lane;
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) {
-        org[k] = fmaf(f, src[k], org[k]);
-        rot[k] = fmaf(f, src[D + k], rot[k]);
-      }
-    }
-    const bool out_rot = flags & AKVQ_OUT_ROTATED;
-    float x[CPL];
-#pragma unroll
-    for (int k = 0; k < CPL; ++k) x[k] = out_rot ? org[k] : rot[k];
-    // FWHT over D channels: lane holds channels CPL*lane .. CPL*lane+CPL-1
-#pragma unroll
-    for (int hs = 1; hs < CPL; hs <<= 1)
-#pragma unroll
-      for (int k = 0; k < CPL; ++k)
-        if (!(k & hs)) { const float a = x[k], b = x[k + hs]; x[k] = a + b; x[k + hs] = a - b; }
-#pragma unroll
-    for (int lm = 1; lm < 32; lm <<= 1) {
-      const bool upper = lane & lm;
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) {
-        const float o = __shfl_xor_sync(0xffffffffu, x[k], lm);
-        x[k] = upper ? o - x[k] : x[k] + o;
-      }
-    }
-    const float inv = 1.f / lsum;
-    float *dst = out + ((size_t)u * g + h) * D + CPL * lane;
-#pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-      const float tr = x[k] * c.inv_sqrt_d;
-      dst[k] = (out_rot ? rot[k] + tr : tr + org[k]) * inv;
-    }
-  }
-}
-
 template <int D, int G, int DT, int MAXG>
 static cudaError_t launch_dec(const DevCache &c, const DecodePlan &p, const void *q, float *out,
                               void *ws, uint32_t flags, cudaStream_t st) {
   float *ws_m = reinterpret_cast<float *>(ws);
   float *ws_l = ws_m + (size_t)c.U * p.S * c.g;
   float *ws_o = ws_l + (size_t)c.U * p.S * c.g;
-  const size_t nslot = p.fast ? (size_t)p.pp.W * p.pp.maxseg * c.g : 0;
-  float *pg_m = ws_o + (size_t)c.U * p.S * c.g * D;
-  float *pg_l = pg_m + nslot;
-  float *pg_o = pg_l + nslot;
-  if (p.S > 0) {
-    const size_t smem = Smem<D>::floats(c.g) * sizeof(float);
-    auto kern = k_decode_split<D, G, DT, MAXG>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid(p.S, c.U);
-    kern<<<grid, kThreads, smem, st>>>(c, p, (const uint16_t *)q, ws_m, ws_l, ws_o);
-  }
-  if (p.fast) {
-    const size_t rslot = (size_t)p.rp.W * p.rp.maxseg * c.g;
-    float *rw_m = pg_o + nslot * D;
-    float *rw_l = rw_m + rslot;
-    float *rw_o = rw_l + rslot;
-    cudaError_t e = launch_decode_rows(c, DT, p.rp, q, rw_m, rw_l, rw_o, st);
-    if (e == cudaSuccess) e = launch_decode_pages(c, DT, p.pp, q, pg_m, pg_l, pg_o, st);
-    if (e != cudaSuccess) return e;
-    k_combine_fast<D><<<(c.U + 3) / 4, 128, 0, st>>>(c, p, pg_m, pg_l, pg_o, rw_m, rw_l, rw_o, out,
-                                                    flags);
-    return cudaGetLastError();
-  }
-  k_combine<D><<<c.U, D, 0, st>>>(c, p, ws_m, ws_l, ws_o, pg_m, pg_l, pg_o, out, flags);
+  const size_t smem = Smem<D>::floats(c.g) * sizeof(float);
+  auto kern = k_decode_split<D, G, DT, MAXG>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(p.S, c.U);
+  kern<<<grid, kThreads, smem, st>>>(c, p, (const uint16_t *)q, ws_m, ws_l, ws_o);
+  k_combine<D><<<c.U, D, 0, st>>>(c, p, ws_m, ws_l, ws_o, out, flags);
   return cudaGetLastError();
 }
 

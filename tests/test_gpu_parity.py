@@ -42,7 +42,7 @@ def _configs(ak, orc, w, layer, units_n, kind=None, cap=None):
 
 
 def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every=1,
-              flags=0, report=None, options=0):
+              flags=0, report=None, options=0, fused_step=None):
     """Prefill + `steps` decode steps on the GPU for all units; the oracle runs the
     sampled `units` (default all).  Compares state after prefill and after every
     flush, outputs every `check_every` steps."""
@@ -70,8 +70,12 @@ def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every
     for step in range(steps):
         di = sy.decode_inputs(w, layer, step, device=dev)
         nq_before = lc.n_q
-        lc.append(di["k"], di["v"], di["types"])
-        out = lc.decode(di["q"], flags=flags)
+        # alternate the fused append+decode call and the two separate calls
+        if (step % 2 == 1) if fused_step is None else fused_step:
+            out = lc.step(di["k"], di["v"], di["q"], di["types"], flags=flags)
+        else:
+            lc.append(di["k"], di["v"], di["types"])
+            out = lc.decode(di["q"], flags=flags)
         do = sy.decode_inputs(w, layer, step, units=us, device="cpu")
         oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
         rows_k.append(f16_bits(do["k"])[:, None])
