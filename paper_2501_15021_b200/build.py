@@ -20,8 +20,8 @@ OUT = os.path.join(PKG, "libakvq.so")
 BUILD = os.path.join(PKG, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["api.cu", "quantize.cu", "decode.cu", "decode_fused.cu"]
-HEADERS = ["common.cuh", "kernels.h"]
+SOURCES = ["api.cu", "quantize.cu", "decode.cu", "decode_pages.cu", "decode_rows.cu"]
+HEADERS = ["common.cuh", "kernels.h", "decode_common.cuh"]
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

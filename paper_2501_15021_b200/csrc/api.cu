@@ -80,40 +80,42 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
     p.n_side_splits = bound > 0 ? (bound + 511) / 512 : 0;
     if (p.n_side_splits > 8) p.n_side_splits = 8;
   }
-  // fused path: the whole decode in one persistent kernel (k_decode_fused)
-  p.fused = 0;
-  memset(&p.fp, 0, sizeof(p.fp));
+  // fast path: 16-bit / 4-bit rows through the persistent row kernel (which
+  // also appends the new token), then 2-bit pages through the persistent dp4a
+  // page kernel (programmatic dependent launch); the last warp of each unit
+  // merges its segments and writes the output row.
+  p.fast = 0;
+  memset(&p.pp, 0, sizeof(p.pp));
+  memset(&p.rp, 0, sizeof(p.rp));
+  p.pp.n_pages = p.n_pages > 0 ? p.n_pages : 1;
+  p.rp.items_per_unit = 1;
   if (!(c->options & AKVQ_OPT_GENERIC_PAGES) &&
-      fused_supported(f.head_dim, f.group, f.q_per_kv)) {
-    const akvq_layout &y = c->lay;
-    FusedPlan &fp = p.fp;
-    const int RC = FusedPlan::kRowChunk;
-    fp.L = L;
-    fp.n_q = n_q;
-    fp.P = p.n_pages;
-    fp.NR = (L - n_q + RC - 1) / RC;
-    if (f.kind == AKVQ_PSA) fp.NS = (f.top_k > 0 && n_q > 0) ? 1 : 0;
-    else fp.NS = n_q > 0 ? ((n_q + 1023) / 1024 < 8 ? (n_q + 1023) / 1024 : 8) : 0;
-    // costs ~ bytes / 512 of each item's loads
-    fp.cp = (int)((y.page_bytes + 511) / 512);
-    fp.cr = (int)((RC * 4 * f.head_dim + 511) / 512);
-    fp.cs = f.kind == AKVQ_PSA ? fp.cr * ((f.top_k + RC - 1) / RC) : 2 * fp.cr;
-    if (fp.cp < 1) fp.cp = 1;
-    if (fp.cr < 1) fp.cr = 1;
-    if (fp.cs < 1) fp.cs = 1;
-    fp.cost_unit = fp.P * fp.cp + fp.NR * fp.cr + fp.NS * fp.cs;
-    if (fp.cost_unit < 1) fp.cost_unit = 1;
-    fp.T = (long long)f.n_units * fp.cost_unit;
-    const long long items = (long long)f.n_units * (fp.P + fp.NR + fp.NS);
-    long long W = (long long)sms * 3 * fused_warps_per_cta();
-    if (W > items) W = items > 0 ? items : 1;
-    if (W > fp.T) W = fp.T;
-    fp.W = W;
-    const long long per = (fp.T + W - 1) / W;
-    fp.maxseg = (int)((per + fp.cost_unit - 1) / fp.cost_unit + 1);
-    fp.stage_bytes = fused_stage_bytes(f.head_dim, f.group, y.page_bytes, y.pg_vscale,
-                                       y.side_entry_bytes);
-    p.fused = 1;
+      pages_fast_supported(f.head_dim, f.group, f.q_per_kv)) {
+    p.fast = 1;
+    if (p.n_pages > 0) {
+      p.pp.T = (long long)f.n_units * p.n_pages;
+      const long long wmax = (long long)sms * 2 * pages_warps_per_cta();
+      p.pp.W = p.pp.T < wmax ? p.pp.T : wmax;
+      const long long per = (p.pp.T + p.pp.W - 1) / p.pp.W;
+      p.pp.maxseg = (int)((per + p.n_pages - 1) / p.n_pages + 1);
+    }
+    const int ch = rows_chunk();
+    p.rp.L = L;
+    p.rp.n_q = n_q;
+    p.rp.n_ring_chunks = (L - n_q + ch - 1) / ch;
+    if (f.kind == AKVQ_PSA) p.rp.n_side_splits = (f.top_k > 0 && n_q > 0) ? 1 : 0;
+    else p.rp.n_side_splits = n_q > 0 ? (n_q + 1023) / 1024 : 0;
+    if (p.rp.n_side_splits > 8) p.rp.n_side_splits = 8;
+    p.rp.items_per_unit = p.rp.n_ring_chunks + p.rp.n_side_splits;
+    if (p.rp.items_per_unit > 0) {
+      p.rp.T = (long long)f.n_units * p.rp.items_per_unit;
+      const long long wmax = (long long)sms * 3 * rows_warps_per_cta();
+      p.rp.W = p.rp.T < wmax ? p.rp.T : wmax;
+      const long long per = (p.rp.T + p.rp.W - 1) / p.rp.W;
+      p.rp.maxseg = (int)((per + p.rp.items_per_unit - 1) / p.rp.items_per_unit + 1);
+    } else {
+      p.rp.items_per_unit = 1;
+    }
     p.n_page_splits = p.n_ring_splits = p.n_side_splits = 0;
   }
   p.S = p.n_page_splits + p.n_ring_splits + p.n_side_splits;
@@ -122,8 +124,25 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
 
 size_t ws_bytes_for(const akvq_cache *c, const DecodePlan &p) {
   const size_t g = c->cfg.q_per_kv, d = c->cfg.head_dim;
-  if (p.fused) return (size_t)p.fp.W * p.fp.maxseg * g * (2 * d + 4) * sizeof(float);
+  if (p.fast)
+    return ((size_t)p.pp.W * p.pp.maxseg * g * (d + 4) +
+            (size_t)p.rp.W * p.rp.maxseg * g * (2 * d + 4)) * sizeof(float);
   return (size_t)c->cfg.n_units * p.S * g * (d + 2) * sizeof(float);
+}
+
+// Fast-path launch: rows kernel (+ append when k != NULL), then page kernel.
+akvq_status launch_fast(const akvq_cache *c, const DecodePlan &p, const void *q, const void *k,
+                        const void *v, const uint8_t *types, float *out, void *ws,
+                        uint32_t flags, cudaStream_t s) {
+  const DevCache d = make_dev(c);
+  const size_t g = c->cfg.q_per_kv, dd = c->cfg.head_dim;
+  float *pg_part = static_cast<float *>(ws);
+  float *rw_part = pg_part + (size_t)p.pp.W * p.pp.maxseg * g * (dd + 4);
+  cudaError_t e = launch_decode_rows(d, c->cfg.dtype16, p.rp, p.pp, q, k, v, types, rw_part,
+                                     pg_part, out, flags, s);
+  if (e == cudaSuccess)
+    e = launch_decode_pages(d, c->cfg.dtype16, p.pp, p.rp, q, pg_part, rw_part, out, flags, s);
+  return cuda_status(e);
 }
 
 }  // namespace
@@ -291,9 +310,7 @@ akvq_status akvq_decode_attention(const akvq_cache *c, const void *q, float *out
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
   const DevCache d = make_dev(c);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (p.fused)
-    return cuda_status(launch_decode_fused(d, c->cfg.dtype16, p.fp, q, nullptr, nullptr, nullptr,
-                                           static_cast<float *>(ws), out, flags, s));
+  if (p.fast) return launch_fast(c, p, q, nullptr, nullptr, nullptr, out, ws, flags, s);
   return cuda_status(launch_decode(d, c->cfg.dtype16, p, q, out, ws, flags, s));
 }
 
@@ -307,16 +324,14 @@ akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const 
   const bool flush = L1 - f.residual - c->n_q >= f.group;
   const DecodePlan p = plan_decode(c, L1, flush ? c->n_q + f.group : c->n_q);
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
-  if (flush || !p.fused) {              // flush step (every G tokens) or generic path
+  if (flush || !p.fast || p.rp.T <= 0) {   // flush step (every G tokens) or generic path
     akvq_status st = akvq_append_token(c, k, v, types, stream);
     if (st != AKVQ_OK) return st;
     return akvq_decode_attention(c, q, out, ws, ws_bytes, flags, stream);
   }
-  const DevCache d = make_dev(c);
-  const cudaError_t e = launch_decode_fused(d, f.dtype16, p.fp, q, k, v, types,
-                                            static_cast<float *>(ws), out, flags,
-                                            reinterpret_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return AKVQ_ECUDA;
+  const akvq_status st = launch_fast(c, p, q, k, v, types, out, ws, flags,
+                                     reinterpret_cast<cudaStream_t>(stream));
+  if (st != AKVQ_OK) return st;
   c->L = L1;
   return AKVQ_OK;
 }

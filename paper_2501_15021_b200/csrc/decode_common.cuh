@@ -1,0 +1,181 @@
+// decode_common.cuh -- pieces shared by the two persistent decode kernels
+// (k_decode_rows, k_decode_pages): TMA bulk / mbarrier / dp4a wrappers, the
+// partial-record layouts, the (warp, unit) segment mapping and the per-unit
+// merge (log-sum-exp over segments, output Walsh-Hadamard, Fig. 7 / R4).
+#pragma once
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace akvq {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(s));
+  return r;
+}
+__device__ __forceinline__ int dp4a_uu(uint32_t a, uint32_t b, int c) {
+  int r;
+  asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {   // a unsigned, b signed
+  int r;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+// Programmatic dependent launch (PDL) controls.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Partial records (floats), 16-byte aligned per head:
+//   page segment: [o_rot D][m][l][pad 2]
+//   row segment:  [o_org D][o_rot D][m][l][pad 2]
+template <int D> struct Rec {
+  static constexpr int P = D + 4;
+  static constexpr int R = 2 * D + 4;
+};
+
+// Warps of a persistent plan (T work, W warps, per = work per unit) whose
+// ranges [w*T/W, (w+1)*T/W) intersect unit u's [u*per, (u+1)*per).
+__device__ __forceinline__ void seg_range(long long T, long long W, long long per, int u,
+                                          long long &w_lo, long long &w_hi) {
+  w_lo = 0;
+  w_hi = -1;
+  if (T <= 0 || W <= 0) return;
+  const long long i0 = (long long)u * per, i1 = i0 + per;
+  w_lo = i0 * W / T;
+  while (w_lo > 0 && w_lo * T / W > i0) --w_lo;
+  while ((w_lo + 1) * T / W <= i0) ++w_lo;
+  w_hi = w_lo;
+  while (w_hi + 1 < W && (w_hi + 1) * T / W < i1) ++w_hi;
+}
+__device__ __forceinline__ size_t seg_slot(long long T, long long W, long long per, int maxseg,
+                                           long long w, int u) {
+  const long long u_first = (w * T / W) / per;
+  return (size_t)(w * maxseg + (u - u_first));
+}
+
+// Per-unit merge by one warp: log-sum-exp over all page and row segments of
+// unit u, then out = (o_rot . H + o_org) / l (or o_rot + o_org . H with
+// AKVQ_OUT_ROTATED).  Partials are read with ld.global.cg (written by other
+// SMs in this or the preceding grid).
+template <int D, int NH>
+__device__ void merge_unit(const DevCache &c, const PagePlan &pp, const RowPlan &rp,
+                           const float *pg_part, const float *rw_part, int u, float *out,
+                           uint32_t flags, int lane) {
+  constexpr int CPL = D / 32;
+  long long pw0, pw1, rw0, rw1;
+  seg_range(pp.T, pp.W, pp.n_pages, u, pw0, pw1);
+  seg_range(rp.T, rp.W, rp.items_per_unit, u, rw0, rw1);
+  const bool out_rot = flags & AKVQ_OUT_ROTATED;
+#pragma unroll
+  for (int h = 0; h < NH; ++h) {
+    float M = -INFINITY;
+    for (long long w = pw0; w <= pw1; ++w) {
+      const float *r = pg_part + (seg_slot(pp.T, pp.W, pp.n_pages, pp.maxseg, w, u) * NH + h) * Rec<D>::P;
+      M = fmaxf(M, __ldcg(r + D));
+    }
+    for (long long w = rw0; w <= rw1; ++w) {
+      const float *r = rw_part + (seg_slot(rp.T, rp.W, rp.items_per_unit, rp.maxseg, w, u) * NH + h) * Rec<D>::R;
+      M = fmaxf(M, __ldcg(r + 2 * D));
+    }
+    float rot[CPL], org[CPL], lsum = 0.f;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) { rot[k] = 0.f; org[k] = 0.f; }
+    if (M != -INFINITY) {
+      for (long long w = pw0; w <= pw1; ++w) {
+        const float *r = pg_part + (seg_slot(pp.T, pp.W, pp.n_pages, pp.maxseg, w, u) * NH + h) * Rec<D>::P;
+        const float ms = __ldcg(r + D);
+        if (ms == -INFINITY) continue;
+        const float f = exp2f(ms - M);
+        lsum += f * __ldcg(r + D + 1);
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) rot[k] = fmaf(f, __ldcg(r + CPL * lane + k), rot[k]);
+      }
+      for (long long w = rw0; w <= rw1; ++w) {
+        const float *r = rw_part + (seg_slot(rp.T, rp.W, rp.items_per_unit, rp.maxseg, w, u) * NH + h) * Rec<D>::R;
+        const float ms = __ldcg(r + 2 * D);
+        if (ms == -INFINITY) continue;
+        const float f = exp2f(ms - M);
+        lsum += f * __ldcg(r + 2 * D + 1);
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          org[k] = fmaf(f, __ldcg(r + CPL * lane + k), org[k]);
+          rot[k] = fmaf(f, __ldcg(r + D + CPL * lane + k), rot[k]);
+        }
+      }
+    }
+    float x[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) x[k] = out_rot ? org[k] : rot[k];
+    // FWHT over D channels: lane holds channels CPL*lane .. CPL*lane + CPL - 1
+#pragma unroll
+    for (int hs = 1; hs < CPL; hs <<= 1)
+#pragma unroll
+      for (int k = 0; k < CPL; ++k)
+        if (!(k & hs)) { const float a = x[k], b = x[k + hs]; x[k] = a + b; x[k + hs] = a - b; }
+#pragma unroll
+    for (int lm = 1; lm < 32; lm <<= 1) {
+      const bool upper = lane & lm;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        const float o = __shfl_xor_sync(0xffffffffu, x[k], lm);
+        x[k] = upper ? o - x[k] : x[k] + o;
+      }
+    }
+    const float inv = 1.f / lsum;
+    float *dst = out + ((size_t)u * c.g + h) * D + CPL * lane;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const float tr = x[k] * c.inv_sqrt_d;
+      dst[k] = (out_rot ? rot[k] + tr : tr + org[k]) * inv;
+    }
+  }
+}
+
+// Ticket: called by every warp that wrote a segment of unit u; returns true
+// in exactly one warp (the last of `expected`), which then merges.
+__device__ __forceinline__ bool take_ticket(const DevCache &c, int u, int expected, int lane) {
+  __threadfence();
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) last = atomicAdd(&c.ticket[u], 1u) == (unsigned)(expected - 1);
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last) __threadfence();
+  return last;
+}
+
+}  // namespace akvq

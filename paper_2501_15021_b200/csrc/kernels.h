@@ -15,16 +15,27 @@ struct QuantSrc {
   int ring_slots;       // 0: linear token index; >0: slot = token % ring_slots
 };
 
-// Fused decode plan (k_decode_fused): per unit, items [P pages][NR ring chunks]
-// [NS side splits] with start costs k*cp, P*cp + r*cr, P*cp + NR*cr + s*cs;
-// warp w of W owns the items whose start cost lies in [w*T/W, (w+1)*T/W),
-// T = U * cost_unit.  Partials: W * maxseg slots.
-struct FusedPlan {
-  static constexpr int kRowChunk = 8;   // 16-bit / 4-bit rows per sub-load
-  long long T, W;
-  int cost_unit, P, NR, NS, cp, cr, cs, maxseg;
+// Persistent page-kernel plan: T = U * n_pages flattened (unit, page) items,
+// W warps each owning items [w*T/W, (w+1)*T/W); a warp writes one partial per
+// unit it touches into slot w*maxseg + (u - first unit of w).
+struct PagePlan {
+  long long T;
+  long long W;
+  int n_pages;
+  int maxseg;
+};
+
+// Persistent row-kernel plan: per unit, n_ring_chunks items of 16 ring tokens
+// then n_side_splits items sharing the unit's side entries; same segment /
+// partial-slot scheme as PagePlan (partials hold o_org and o_rot).
+struct RowPlan {
+  long long T;
+  long long W;
+  int items_per_unit;
+  int n_ring_chunks;
+  int n_side_splits;
+  int maxseg;
   int L, n_q;
-  size_t stage_bytes;
 };
 
 // Decode split plan (host-computed, uniform across units).
@@ -35,8 +46,9 @@ struct DecodePlan {
   int ring_per_split, n_ring_splits;
   int n_side_splits;     // side entries are shared equally among these splits
   int S;                 // total splits of k_decode_split (ring / side / fallback pages)
-  int fused;             // 1: the whole decode runs in k_decode_fused
-  FusedPlan fp;
+  int fast;              // 1: k_decode_rows then k_decode_pages (PDL), merged in-kernel
+  PagePlan pp;
+  RowPlan rp;
 };
 
 cudaError_t launch_salient(const DevCache &c, const uint8_t *types, const float *colsum,
@@ -49,13 +61,17 @@ cudaError_t launch_append(const DevCache &c, const void *k, const void *v,
                           const uint8_t *types, int L, cudaStream_t st);
 cudaError_t launch_decode(const DevCache &c, int dtype16, const DecodePlan &p, const void *q,
                           float *out, void *ws, uint32_t flags, cudaStream_t st);
-cudaError_t launch_decode_fused(const DevCache &c, int dtype16, const FusedPlan &fp, const void *q,
-                                const void *k, const void *v, const uint8_t *types, float *part,
-                                float *out, uint32_t flags, cudaStream_t st);
-int fused_supported(int d, int G, int g);
-int fused_warps_per_cta();
-size_t fused_stage_bytes(int d, int G, size_t page_bytes, size_t pg_vscale, size_t side_entry);
-size_t fused_smem_bytes(int d, int G, int g, size_t stage_bytes);
+cudaError_t launch_decode_rows(const DevCache &c, int dtype16, const RowPlan &rp, const PagePlan &pp,
+                               const void *q, const void *k, const void *v, const uint8_t *types,
+                               float *rw_part, const float *pg_part, float *out, uint32_t flags,
+                               cudaStream_t st);
+cudaError_t launch_decode_pages(const DevCache &c, int dtype16, const PagePlan &pp,
+                                const RowPlan &rp, const void *q, float *pg_part,
+                                const float *rw_part, float *out, uint32_t flags, cudaStream_t st);
+int pages_fast_supported(int d, int G, int g);
+int pages_warps_per_cta();
+int rows_chunk();
+int rows_warps_per_cta();
 cudaError_t launch_view(const DevCache &c, int dtype16, int L, int n_q, float *K, float *V,
                         cudaStream_t st);
 
