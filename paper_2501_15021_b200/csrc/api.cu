@@ -94,7 +94,7 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
     p.fast = 1;
     if (p.n_pages > 0) {
       p.pp.T = (long long)f.n_units * p.n_pages;
-      const long long wmax = (long long)sms * 2 * pages_warps_per_cta();
+      const long long wmax = (long long)sms * 3 * pages_warps_per_cta();
       p.pp.W = p.pp.T < wmax ? p.pp.T : wmax;
       const long long per = (p.pp.T + p.pp.W - 1) / p.pp.W;
       p.pp.maxseg = (int)((per + p.n_pages - 1) / p.n_pages + 1);

@@ -68,73 +68,101 @@ template <int D> struct Rec {
   static constexpr int R = 2 * D + 4;
 };
 
-// Warps of a persistent plan (T work, W warps, per = work per unit) whose
-// ranges [w*T/W, (w+1)*T/W) intersect unit u's [u*per, (u+1)*per).
-__device__ __forceinline__ void seg_range(long long T, long long W, long long per, int u,
-                                          long long &w_lo, long long &w_hi) {
+// Warps of a persistent plan (T work items, W warps, per = items per unit)
+// whose ranges [w*T/W, (w+1)*T/W) intersect unit u's [u*per, (u+1)*per).
+// 32-bit arithmetic: the host guarantees T * W < 2^31 is not needed because
+// products are formed in 64 bits and divided by a 32-bit W (see seg_begin).
+__device__ __forceinline__ int seg_begin(int T, int W, int w) {
+  return (int)(((unsigned long long)w * (unsigned)T) / (unsigned)W);   // 64/32 division
+}
+__device__ __forceinline__ void seg_range(int T, int W, int per, int u, int &w_lo, int &w_hi) {
   w_lo = 0;
   w_hi = -1;
   if (T <= 0 || W <= 0) return;
-  const long long i0 = (long long)u * per, i1 = i0 + per;
-  w_lo = i0 * W / T;
-  while (w_lo > 0 && w_lo * T / W > i0) --w_lo;
-  while ((w_lo + 1) * T / W <= i0) ++w_lo;
+  const int i0 = u * per, i1 = i0 + per;
+  // first warp whose range ends after i0: ceil((i0 + 1) * W / T) - 1
+  w_lo = (int)((((unsigned long long)(i0 + 1)) * (unsigned)W + (unsigned)T - 1) / (unsigned)T) - 1;
+  if (w_lo < 0) w_lo = 0;
+  while (w_lo > 0 && seg_begin(T, W, w_lo) > i0) --w_lo;
+  while (seg_begin(T, W, w_lo + 1) <= i0) ++w_lo;
   w_hi = w_lo;
-  while (w_hi + 1 < W && (w_hi + 1) * T / W < i1) ++w_hi;
-}
-__device__ __forceinline__ size_t seg_slot(long long T, long long W, long long per, int maxseg,
-                                           long long w, int u) {
-  const long long u_first = (w * T / W) / per;
-  return (size_t)(w * maxseg + (u - u_first));
+  while (w_hi + 1 < W && seg_begin(T, W, w_hi + 1) < i1) ++w_hi;
 }
 
 // Per-unit merge by one warp: log-sum-exp over all page and row segments of
 // unit u, then out = (o_rot . H + o_org) / l (or o_rot + o_org . H with
 // AKVQ_OUT_ROTATED).  Partials are read with ld.global.cg (written by other
-// SMs in this or the preceding grid).
+// SMs in this or the preceding grid).  Lane j < #segments fetches segment j's
+// (m, l) so the loads overlap.
 template <int D, int NH>
 __device__ void merge_unit(const DevCache &c, const PagePlan &pp, const RowPlan &rp,
                            const float *pg_part, const float *rw_part, int u, float *out,
                            uint32_t flags, int lane) {
   constexpr int CPL = D / 32;
-  long long pw0, pw1, rw0, rw1;
-  seg_range(pp.T, pp.W, pp.n_pages, u, pw0, pw1);
-  seg_range(rp.T, rp.W, rp.items_per_unit, u, rw0, rw1);
+  int pw0, pw1, rw0, rw1;
+  seg_range((int)pp.T, (int)pp.W, pp.n_pages, u, pw0, pw1);
+  seg_range((int)rp.T, (int)rp.W, rp.items_per_unit, u, rw0, rw1);
+  const int npg = pw1 - pw0 + 1, nrw = rw1 - rw0 + 1, nseg = npg + nrw;
   const bool out_rot = flags & AKVQ_OUT_ROTATED;
+  // record of segment j (page segments first, then row segments)
+  auto seg_rec = [&](int j, int &moff) -> const float * {
+    if (j < npg) {
+      const int w = pw0 + j;
+      const int slot = w * pp.maxseg + (u - seg_begin((int)pp.T, (int)pp.W, w) / pp.n_pages);
+      moff = D;
+      return pg_part + (size_t)slot * NH * Rec<D>::P;
+    }
+    const int w = rw0 + j - npg;
+    const int slot = w * rp.maxseg + (u - seg_begin((int)rp.T, (int)rp.W, w) / rp.items_per_unit);
+    moff = 2 * D;
+    return rw_part + (size_t)slot * NH * Rec<D>::R;
+  };
 #pragma unroll
   for (int h = 0; h < NH; ++h) {
+    // pass 1: running max over segments, lanes fetch 32 segments at a time
     float M = -INFINITY;
-    for (long long w = pw0; w <= pw1; ++w) {
-      const float *r = pg_part + (seg_slot(pp.T, pp.W, pp.n_pages, pp.maxseg, w, u) * NH + h) * Rec<D>::P;
-      M = fmaxf(M, __ldcg(r + D));
-    }
-    for (long long w = rw0; w <= rw1; ++w) {
-      const float *r = rw_part + (seg_slot(rp.T, rp.W, rp.items_per_unit, rp.maxseg, w, u) * NH + h) * Rec<D>::R;
-      M = fmaxf(M, __ldcg(r + 2 * D));
+    for (int b0 = 0; b0 < nseg; b0 += 32) {
+      float ms = -INFINITY;
+      if (b0 + lane < nseg) {
+        int moff;
+        const float *r = seg_rec(b0 + lane, moff);
+        ms = __ldcg(r + (size_t)h * (moff == D ? Rec<D>::P : Rec<D>::R) + moff);
+      }
+      M = fmaxf(M, warp_max(ms));
     }
     float rot[CPL], org[CPL], lsum = 0.f;
 #pragma unroll
     for (int k = 0; k < CPL; ++k) { rot[k] = 0.f; org[k] = 0.f; }
     if (M != -INFINITY) {
-      for (long long w = pw0; w <= pw1; ++w) {
-        const float *r = pg_part + (seg_slot(pp.T, pp.W, pp.n_pages, pp.maxseg, w, u) * NH + h) * Rec<D>::P;
-        const float ms = __ldcg(r + D);
-        if (ms == -INFINITY) continue;
-        const float f = exp2f(ms - M);
-        lsum += f * __ldcg(r + D + 1);
+      for (int b0 = 0; b0 < nseg; b0 += 32) {
+        float f = 0.f, ls = 0.f;
+        const float *rh = nullptr;
+        if (b0 + lane < nseg) {
+          int moff;
+          const float *r = seg_rec(b0 + lane, moff);
+          rh = r + (size_t)h * (moff == D ? Rec<D>::P : Rec<D>::R);
+          const float ms = __ldcg(rh + moff);
+          ls = __ldcg(rh + moff + 1);
+          f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+        }
+        lsum += warp_sum(f * ls);
+        const int nb = min(32, nseg - b0);
+        for (int j = 0; j < nb; ++j) {
+          const float fj = __shfl_sync(0xffffffffu, f, j);
+          const unsigned long long pj =
+              __shfl_sync(0xffffffffu, (unsigned long long)(uintptr_t)rh, j);
+          if (fj == 0.f) continue;
+          const float *r = reinterpret_cast<const float *>((uintptr_t)pj);
+          if (b0 + j < npg) {
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) rot[k] = fmaf(f, __ldcg(r + CPL * lane + k), rot[k]);
-      }
-      for (long long w = rw0; w <= rw1; ++w) {
-        const float *r = rw_part + (seg_slot(rp.T, rp.W, rp.items_per_unit, rp.maxseg, w, u) * NH + h) * Rec<D>::R;
-        const float ms = __ldcg(r + 2 * D);
-        if (ms == -INFINITY) continue;
-        const float f = exp2f(ms - M);
-        lsum += f * __ldcg(r + 2 * D + 1);
+            for (int k = 0; k < CPL; ++k) rot[k] = fmaf(fj, __ldcg(r + CPL * lane + k), rot[k]);
+          } else {
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) {
-          org[k] = fmaf(f, __ldcg(r + CPL * lane + k), org[k]);
-          rot[k] = fmaf(f, __ldcg(r + D + CPL * lane + k), rot[k]);
+            for (int k = 0; k < CPL; ++k) {
+              org[k] = fmaf(fj, __ldcg(r + CPL * lane + k), org[k]);
+              rot[k] = fmaf(fj, __ldcg(r + D + CPL * lane + k), rot[k]);
+            }
+          }
         }
       }
     }

@@ -23,25 +23,31 @@
 namespace akvq {
 
 constexpr int kPgWarps = 4;
-constexpr int kStages = 2;
+constexpr int kStages = 3;
 
-// Per-warp shared-memory block (bytes): stages, q~, limbs, transposed weights, barriers.
+// Per-warp shared-memory block (bytes): kStages half-page stages, q~, limbs,
+// transposed value weights, barriers.  sb = stage bytes (>= either page half).
 template <int D, int G, int NH>
 struct PgSmem {
   static constexpr int NG = D / G;
-  static __host__ __device__ size_t qh_off(size_t pb) { return kStages * pb; }
-  static __host__ __device__ size_t limb_off(size_t pb) { return qh_off(pb) + NH * D * 4; }
-  static __host__ __device__ size_t wt_off(size_t pb) { return limb_off(pb) + NH * 32 * 16; }
-  static __host__ __device__ size_t bar_off(size_t pb) {
-    return (wt_off(pb) + NH * NG * 3 * G + 15) / 16 * 16;
+  static __host__ __device__ size_t qh_off(size_t sb) { return kStages * sb; }
+  static __host__ __device__ size_t limb_off(size_t sb) { return qh_off(sb) + NH * D * 4; }
+  static __host__ __device__ size_t wt_off(size_t sb) { return limb_off(sb) + NH * 32 * 16; }
+  static __host__ __device__ size_t bar_off(size_t sb) {
+    return (wt_off(sb) + NH * NG * 3 * G + 15) / 16 * 16;
   }
-  static __host__ __device__ size_t warp_bytes(size_t pb) {
-    return (bar_off(pb) + kStages * 8 + 127) / 128 * 128;
+  static __host__ __device__ size_t warp_bytes(size_t sb) {
+    return (bar_off(sb) + kStages * 8 + 127) / 128 * 128;
   }
 };
 
+__host__ __device__ inline size_t pg_stage_bytes(size_t page_bytes, size_t pg_vscale) {
+  const size_t a = pg_vscale, b = page_bytes - pg_vscale;
+  return ((a > b ? a : b) + 127) / 128 * 128;
+}
+
 template <int D, int G, int DT, int NH>
-__global__ void __launch_bounds__(kPgWarps * 32, 2)
+__global__ void __launch_bounds__(kPgWarps * 32, 3)
     k_decode_pages(DevCache c, PagePlan pp, RowPlan rp, const uint16_t *__restrict__ q,
                    float *__restrict__ pg_part, const float *__restrict__ rw_part,
                    float *__restrict__ out, uint32_t flags) {
@@ -54,45 +60,52 @@ __global__ void __launch_bounds__(kPgWarps * 32, 2)
   constexpr int GQ = G / 4;         // dp4a token groups of 4 (tokens gi + GQ*i)
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const size_t PB = c.page_bytes;
-  uint8_t *wsm = smem + (size_t)warp * S::warp_bytes(PB);
-  float *qh = reinterpret_cast<float *>(wsm + S::qh_off(PB));
-  uint4 *limbs = reinterpret_cast<uint4 *>(wsm + S::limb_off(PB));
-  uint8_t *wt = wsm + S::wt_off(PB);                    // [NH][NG][3 limbs][G] bytes
-  uint64_t *bar = reinterpret_cast<uint64_t *>(wsm + S::bar_off(PB));
+  const size_t SB = pg_stage_bytes(c.page_bytes, c.pg_vscale);
+  uint8_t *wsm = smem + (size_t)warp * S::warp_bytes(SB);
+  float *qh = reinterpret_cast<float *>(wsm + S::qh_off(SB));
+  uint4 *limbs = reinterpret_cast<uint4 *>(wsm + S::limb_off(SB));
+  uint8_t *wt = wsm + S::wt_off(SB);                    // [NH][NG][3 limbs][G] bytes
+  uint64_t *bar = reinterpret_cast<uint64_t *>(wsm + S::bar_off(SB));
 
   pdl_launch_dependents();                      // let the next layer's kernels queue up
-  const long long gw = (long long)blockIdx.x * kPgWarps + warp;
-  if (gw >= pp.W) return;
-  const long long ib = gw * pp.T / pp.W, ie = (gw + 1) * pp.T / pp.W;
+  const int gw = blockIdx.x * kPgWarps + warp;
+  if (gw >= (int)pp.W) return;
+  const int ib = seg_begin((int)pp.T, (int)pp.W, gw), ie = seg_begin((int)pp.T, (int)pp.W, gw + 1);
   if (ib >= ie) return;
   const int npg = pp.n_pages;
+  const int nsub = 2 * (ie - ib);               // two half-page loads per page
   const float alpha = kLog2e / (float)D;       // (q.H_s) . K^ / d in log2 units
+  const uint32_t kbytes = c.pg_vscale, vbytes = c.page_bytes - c.pg_vscale;
 
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bar[s]);
     mbar_fence_init();
   }
   __syncwarp();
-  auto issue = [&](long long item, int st) {
-    const int u = (int)(item / npg), p = (int)(item % npg);
-    mbar_expect_tx(&bar[st], (uint32_t)PB);
-    bulk_g2s(wsm + (size_t)st * PB, page_ptr(c, u, p), (uint32_t)PB, &bar[st]);
+  // sub-load si: page ib + si/2, K half (even si) or V half (odd si)
+  auto issue = [&](int si, int st) {
+    const int item = ib + (si >> 1);
+    const int u = item / npg, p = item - u * npg;
+    const uint8_t *src = page_ptr(c, u, p) + ((si & 1) ? kbytes : 0u);
+    const uint32_t nb = (si & 1) ? vbytes : kbytes;
+    mbar_expect_tx(&bar[st], nb);
+    bulk_g2s(wsm + (size_t)st * SB, src, nb, &bar[st]);
   };
   if (lane == 0)
-    for (int s = 0; s < kStages && ib + s < ie; ++s) issue(ib + s, s);
+    for (int s = 0; s < kStages && s < nsub; ++s) issue(s, s);
 
   // per-head running state (online softmax, base 2)
   float m_run[NH], l_run[NH], Z[NH][NG], o[NH][16];
+  float lgp[NH][PASSES];                        // page logits between the two halves
   int cur_u = -1;
-  const int u_first = (int)(ib / npg);
+  const int u_first = ib / npg;
 
   const int tq = lane >> 1, half = lane & 1;                // K phase
   const int kw = lane % KPR, tg = lane / KPR;               // V phase
   const int gam = (16 * kw) / G;                            // V channel group of this lane
 
   auto flush = [&](int u) {
-    const size_t slot = (size_t)(gw * pp.maxseg + (u - u_first));
+    const size_t slot = (size_t)gw * pp.maxseg + (u - u_first);
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
       float zg = Z[h][0];
@@ -115,8 +128,8 @@ __global__ void __launch_bounds__(kPgWarps * 32, 2)
       if (lane == 0) { rec[D] = m_run[h]; rec[D + 1] = l_run[h]; }
     }
     // the last page warp of unit u merges it with the row kernel's segments
-    long long w_lo, w_hi;
-    seg_range(pp.T, pp.W, pp.n_pages, u, w_lo, w_hi);
+    int w_lo, w_hi;
+    seg_range((int)pp.T, (int)pp.W, pp.n_pages, u, w_lo, w_hi);
     if (take_ticket(c, u, (int)(w_hi - w_lo + 1), lane)) {
       pdl_wait();                                  // row partials of the preceding grid
       merge_unit<D, NH>(c, pp, rp, pg_part, rw_part, u, out, flags, lane);
@@ -124,228 +137,231 @@ __global__ void __launch_bounds__(kPgWarps * 32, 2)
     }
   };
 
-  for (long long it = ib; it < ie; ++it) {
-    const int st = (int)((it - ib) % kStages);
-    const uint32_t par = (uint32_t)(((it - ib) / kStages) & 1);
-    const int u = (int)(it / npg), pg = (int)(it % npg);
-    if (u != cur_u) {
-      if (cur_u >= 0) flush(cur_u);
-      cur_u = u;
-      // q~ = q . H_s for this unit (unnormalized FWHT in smem, warp-local)
-      for (int i = lane; i < NH * D; i += 32) qh[i] = H16<DT>::to_f(q[(size_t)u * c.g * D + i]);
-      __syncwarp();
-#pragma unroll
-      for (int hs = 1; hs < D; hs <<= 1) {
-        for (int idx = lane; idx < NH * D / 2; idx += 32) {
-          const int h = idx / (D / 2), k = idx % (D / 2);
-          const int i = (k / hs) * 2 * hs + (k % hs);
-          const float a = qh[h * D + i], b = qh[h * D + i + hs];
-          qh[h * D + i] = a + b;
-          qh[h * D + i + hs] = a - b;
-        }
+  int u = u_first, pg = ib - u_first * npg;       // (unit, page) of the current sub-load
+  for (int si = 0; si < nsub; ++si) {
+    const int st = si % kStages;
+    const uint32_t par = (uint32_t)((si / kStages) & 1);
+    const uint8_t *B = wsm + (size_t)st * SB;
+    if ((si & 1) == 0) {
+      if (si > 0 && ++pg == npg) { pg = 0; ++u; }
+      if (u != cur_u) {
+        if (cur_u >= 0) flush(cur_u);
+        cur_u = u;
+        // q~ = q . H_s for this unit (unnormalized FWHT in smem, warp-local)
+        for (int i = lane; i < NH * D; i += 32) qh[i] = H16<DT>::to_f(q[(size_t)u * c.g * D + i]);
         __syncwarp();
+#pragma unroll
+        for (int hs = 1; hs < D; hs <<= 1) {
+          for (int idx = lane; idx < NH * D / 2; idx += 32) {
+            const int h = idx / (D / 2), k = idx % (D / 2);
+            const int i = (k / hs) * 2 * hs + (k % hs);
+            const float a = qh[h * D + i], b = qh[h * D + i + hs];
+            qh[h * D + i] = a + b;
+            qh[h * D + i + hs] = a - b;
+          }
+          __syncwarp();
+        }
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          m_run[h] = -INFINITY; l_run[h] = 0.f;
+#pragma unroll
+          for (int gi = 0; gi < NG; ++gi) Z[h][gi] = 0.f;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) o[h][k] = 0.f;
+        }
       }
+      mbar_wait(&bar[st], par);
+      // ============== K half: logits of the page's G tokens
+      const float *ks = reinterpret_cast<const float *>(B + c.pg_kscale);
+      const int32_t *kz = reinterpret_cast<const int32_t *>(B + c.pg_kzero);
+      const uint8_t *kc = B + c.pg_kcodes;
+      const uint32_t *bmw = c.bitmask + (size_t)u * c.bm_words + (size_t)pg * (G / 32);
+      uint32_t bits[G / 32];
+#pragma unroll
+      for (int w = 0; w < G / 32; ++w) bits[w] = __ldg(bmw + w);
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
-        m_run[h] = -INFINITY; l_run[h] = 0.f;
+        // per-page fixed-point limbs of qs_c = q~_c * s^K_c (22 bits, 3 bytes)
+        float bias, delta;
+        {
+          const int k = lane >> 2, s = lane & 3;
+          int Qv[4] = {0, 0, 0, 0};
+          float qsb[4] = {0.f, 0.f, 0.f, 0.f};
+          float bp = 0.f, am = 0.f;
+          if (k < D / 16) {
 #pragma unroll
-        for (int gi = 0; gi < NG; ++gi) Z[h][gi] = 0.f;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) o[h][k] = 0.f;
-      }
-    }
-    mbar_wait(&bar[st], par);
-    const uint8_t *P = wsm + (size_t)st * PB;
-    const float *ks = reinterpret_cast<const float *>(P + c.pg_kscale);
-    const int32_t *kz = reinterpret_cast<const int32_t *>(P + c.pg_kzero);
-    const uint8_t *kc = P + c.pg_kcodes;
-    const float *vs = reinterpret_cast<const float *>(P + c.pg_vscale);
-    const int32_t *vz = reinterpret_cast<const int32_t *>(P + c.pg_vzero);
-    const uint8_t *vc = P + c.pg_vcodes;
-    const uint32_t *bmw = c.bitmask + (size_t)u * c.bm_words + (size_t)pg * (G / 32);
-    uint32_t bits[G / 32];
-#pragma unroll
-    for (int w = 0; w < G / 32; ++w) bits[w] = __ldg(bmw + w);
-
-#pragma unroll
-    for (int h = 0; h < NH; ++h) {
-      // ---------------- A: per-page fixed-point limbs of qs_c = q~_c * s^K_c
-      float bias, delta;
-      {
-        const int k = lane >> 2, s = lane & 3;
-        int Qv[4] = {0, 0, 0, 0};
-        float qsb[4] = {0.f, 0.f, 0.f, 0.f};
-        float bp = 0.f, am = 0.f;
-        if (k < D / 16) {
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int ch = 16 * k + 4 * b + s;
-            qsb[b] = qh[h * D + ch] * ks[ch];
-            bp = fmaf(qsb[b], (float)kz[ch], bp);
-            am = fmaxf(am, fabsf(qsb[b]));
+            for (int b = 0; b < 4; ++b) {
+              const int ch = 16 * k + 4 * b + s;
+              qsb[b] = qh[h * D + ch] * ks[ch];
+              bp = fmaf(qsb[b], (float)kz[ch], bp);
+              am = fmaxf(am, fabsf(qsb[b]));
+            }
           }
+          bias = warp_sum(bp);
+          const float M = warp_max(am);
+          const float inv = M > 0.f ? 2097151.0f / M : 0.f;       // |Q| <= 2^21 - 1
+          delta = M > 0.f ? M / 2097151.0f : 0.f;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) Qv[b] = __float2int_rn(qsb[b] * inv);
+          const uint32_t lo = prmt(prmt(Qv[0], Qv[1], 0x0040), prmt(Qv[2], Qv[3], 0x0040), 0x5410);
+          const uint32_t mi = prmt(prmt(Qv[0], Qv[1], 0x0051), prmt(Qv[2], Qv[3], 0x0051), 0x5410);
+          const uint32_t hi = prmt(prmt(Qv[0], Qv[1], 0x0062), prmt(Qv[2], Qv[3], 0x0062), 0x5410);
+          limbs[h * 32 + lane] = make_uint4(lo, mi, hi, 0u);
         }
-        bias = warp_sum(bp);
-        const float M = warp_max(am);
-        const float inv = M > 0.f ? 2097151.0f / M : 0.f;       // |Q| <= 2^21 - 1
-        delta = M > 0.f ? M / 2097151.0f : 0.f;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) Qv[b] = __float2int_rn(qsb[b] * inv);
-        const uint32_t lo = prmt(prmt(Qv[0], Qv[1], 0x0040), prmt(Qv[2], Qv[3], 0x0040), 0x5410);
-        const uint32_t mi = prmt(prmt(Qv[0], Qv[1], 0x0051), prmt(Qv[2], Qv[3], 0x0051), 0x5410);
-        const uint32_t hi = prmt(prmt(Qv[0], Qv[1], 0x0062), prmt(Qv[2], Qv[3], 0x0062), 0x5410);
-        limbs[h * 32 + lane] = make_uint4(lo, mi, hi, 0u);
-      }
-      __syncwarp();
-      uint32_t lim[KWL][4][3];
-#pragma unroll
-      for (int w = 0; w < KWL; ++w)
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const uint4 v = limbs[h * 32 + 4 * (half * KWL + w) + s];
-          lim[w][s][0] = v.x; lim[w][s][1] = v.y; lim[w][s][2] = v.z;
-        }
-
-      // ---------------- B: logits of the page's G tokens (2 lanes per token)
-      float lg[PASSES];
-#pragma unroll
-      for (int ps = 0; ps < PASSES; ++ps) {
-        const int t = ps * 16 + tq;
-        uint32_t wd[KWL];
-        if constexpr (KWL == 4) {
-          const uint4 v = *reinterpret_cast<const uint4 *>(kc + (size_t)t * (D / 4) + half * 16);
-          wd[0] = v.x; wd[1] = v.y; wd[2] = v.z; wd[3] = v.w;
-        } else {
-          const uint2 v = *reinterpret_cast<const uint2 *>(kc + (size_t)t * (D / 4) + half * 8);
-          wd[0] = v.x; wd[1] = v.y;
-        }
-        int a0 = 0, a1 = 0, a2 = 0;
+        __syncwarp();
+        uint32_t lim[KWL][4][3];
 #pragma unroll
         for (int w = 0; w < KWL; ++w)
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
-            const uint32_t x = (wd[w] >> (2 * s)) & 0x03030303u;
-            a0 = dp4a_uu(x, lim[w][s][0], a0);
-            a1 = dp4a_uu(x, lim[w][s][1], a1);
-            a2 = dp4a_us(x, lim[w][s][2], a2);
+            const uint4 v = limbs[h * 32 + 4 * (half * KWL + w) + s];
+            lim[w][s][0] = v.x; lim[w][s][1] = v.y; lim[w][s][2] = v.z;
           }
-        int tot = a2 * 65536 + a1 * 256 + a0;
-        tot += __shfl_xor_sync(0xffffffffu, tot, 1);
-        const bool sal = (bits[t >> 5] >> (t & 31)) & 1u;
-        lg[ps] = sal ? -INFINITY : alpha * fmaf((float)tot, delta, -bias);
-      }
-
-      // ---------------- C: online softmax update, fixed-point value weights
-      float mloc = lg[0];
-#pragma unroll
-      for (int ps = 1; ps < PASSES; ++ps) mloc = fmaxf(mloc, lg[ps]);
-#pragma unroll
-      for (int off = 2; off < 32; off <<= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, off));
-      const float m_new = fmaxf(m_run[h], mloc);
-      if (m_new == -INFINITY) continue;                    // nothing unmasked yet (warp-uniform)
-      const float sc = exp2f(m_run[h] - m_new);
-      float pr[PASSES], psum = 0.f;
-#pragma unroll
-      for (int ps = 0; ps < PASSES; ++ps) {
-        pr[ps] = exp2f(lg[ps] - m_new);
-        psum += pr[ps];
-      }
-#pragma unroll
-      for (int off = 2; off < 32; off <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, off);
-      l_run[h] = l_run[h] * sc + psum;
-      m_run[h] = m_new;
-      float dw[NG];
-#pragma unroll
-      for (int gi = 0; gi < NG; ++gi) {
-        float wv[PASSES], wmax = 0.f, zs = 0.f;
 #pragma unroll
         for (int ps = 0; ps < PASSES; ++ps) {
           const int t = ps * 16 + tq;
-          wv[ps] = pr[ps] * vs[t * NG + gi];
-          wmax = fmaxf(wmax, wv[ps]);
-          zs = fmaf(wv[ps], (float)vz[t * NG + gi], zs);
+          uint32_t wd[KWL];
+          if constexpr (KWL == 4) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(kc + (size_t)t * (D / 4) + half * 16);
+            wd[0] = v.x; wd[1] = v.y; wd[2] = v.z; wd[3] = v.w;
+          } else {
+            const uint2 v = *reinterpret_cast<const uint2 *>(kc + (size_t)t * (D / 4) + half * 8);
+            wd[0] = v.x; wd[1] = v.y;
+          }
+          // two independent accumulator sets (even / odd words) to halve the
+          // dp4a dependency chains
+          int a0[2] = {0, 0}, a1[2] = {0, 0}, a2[2] = {0, 0};
+#pragma unroll
+          for (int w = 0; w < KWL; ++w)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              const uint32_t x = (wd[w] >> (2 * s)) & 0x03030303u;
+              a0[w & 1] = dp4a_uu(x, lim[w][s][0], a0[w & 1]);
+              a1[w & 1] = dp4a_uu(x, lim[w][s][1], a1[w & 1]);
+              a2[w & 1] = dp4a_us(x, lim[w][s][2], a2[w & 1]);
+            }
+          int tot = (a2[0] + a2[1]) * 65536 + (a1[0] + a1[1]) * 256 + (a0[0] + a0[1]);
+          tot += __shfl_xor_sync(0xffffffffu, tot, 1);
+          const bool sal = (bits[t >> 5] >> (t & 31)) & 1u;
+          lgp[h][ps] = sal ? -INFINITY : alpha * fmaf((float)tot, delta, -bias);
+        }
+        __syncwarp();
+      }
+    } else {
+      mbar_wait(&bar[st], par);
+      // ============== V half: online softmax update and value accumulation
+      const float *vs = reinterpret_cast<const float *>(B);
+      const int32_t *vz = reinterpret_cast<const int32_t *>(B + (c.pg_vzero - c.pg_vscale));
+      const uint8_t *vc = B + (c.pg_vcodes - c.pg_vscale);
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        float mloc = lgp[h][0];
+#pragma unroll
+        for (int ps = 1; ps < PASSES; ++ps) mloc = fmaxf(mloc, lgp[h][ps]);
+#pragma unroll
+        for (int off = 2; off < 32; off <<= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, off));
+        const float m_new = fmaxf(m_run[h], mloc);
+        if (m_new == -INFINITY) continue;                  // nothing unmasked yet (warp-uniform)
+        const float sc = exp2f(m_run[h] - m_new);
+        float pr[PASSES], psum = 0.f;
+#pragma unroll
+        for (int ps = 0; ps < PASSES; ++ps) {
+          pr[ps] = exp2f(lgp[h][ps] - m_new);
+          psum += pr[ps];
         }
 #pragma unroll
-        for (int off = 2; off < 32; off <<= 1) {
-          wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
-          zs += __shfl_xor_sync(0xffffffffu, zs, off);
-        }
-        Z[h][gi] = Z[h][gi] * sc + zs;
-        // 24-bit fixed point of the page's largest weight (3 uint8 limbs): the
-        // per-token rounding error is shared by all d channels of the token and
-        // adds coherently under the output H, so 16 bits are not enough.
-        const float invw = wmax > 0.f ? 16777215.0f / wmax : 0.f;
-        dw[gi] = wmax / 16777215.0f;
-        if (half == 0) {
-          uint8_t *wl = wt + (h * NG + gi) * 3 * G;
+        for (int off = 2; off < 32; off <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, off);
+        l_run[h] = l_run[h] * sc + psum;
+        m_run[h] = m_new;
+        float dwl = 0.f;
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) {
+          float wv[PASSES], wmax = 0.f, zs = 0.f;
 #pragma unroll
           for (int ps = 0; ps < PASSES; ++ps) {
             const int t = ps * 16 + tq;
-            const uint32_t W = min(__float2uint_rn(wv[ps] * invw), 16777215u);  // w*(2^24-1)/w may round up
-            const int idx = (t % GQ) * 4 + t / GQ;
-            wl[idx] = (uint8_t)W;
-            wl[G + idx] = (uint8_t)(W >> 8);
-            wl[2 * G + idx] = (uint8_t)(W >> 16);
+            wv[ps] = pr[ps] * vs[t * NG + gi];
+            wmax = fmaxf(wmax, wv[ps]);
+            zs = fmaf(wv[ps], (float)vz[t * NG + gi], zs);
+          }
+#pragma unroll
+          for (int off = 2; off < 32; off <<= 1) {
+            wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
+            zs += __shfl_xor_sync(0xffffffffu, zs, off);
+          }
+          Z[h][gi] = Z[h][gi] * sc + zs;
+          // 24-bit fixed point of the page's largest weight (3 uint8 limbs): the
+          // per-token rounding error is shared by all d channels of the token and
+          // adds coherently under the output H, so 16 bits are not enough.
+          const float invw = wmax > 0.f ? 16777215.0f / wmax : 0.f;
+          if (gi == gam) dwl = wmax / 16777215.0f;
+          if (half == 0) {
+            uint8_t *wl = wt + (h * NG + gi) * 3 * G;
+#pragma unroll
+            for (int ps = 0; ps < PASSES; ++ps) {
+              const int t = ps * 16 + tq;
+              const uint32_t W = min(__float2uint_rn(wv[ps] * invw), 16777215u);  // may round up
+              const int idx = (t % GQ) * 4 + t / GQ;
+              wl[idx] = (uint8_t)W;
+              wl[G + idx] = (uint8_t)(W >> 8);
+              wl[2 * G + idx] = (uint8_t)(W >> 16);
+            }
           }
         }
-      }
-      __syncwarp();
-
-      // ---------------- D: o'_c += sum_t W_t code_tc  (dp4a over 4 tokens)
-      int a0[16], a1[16], a2[16];
+        __syncwarp();
+        // o'_c += sum_t W_t code_tc  (dp4a over 4 tokens, codes transposed by PRMT)
+        int a0[16], a1[16], a2[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) { a0[k] = 0; a1[k] = 0; a2[k] = 0; }
-      const uint8_t *wl = wt + (h * NG + gam) * 3 * G;
+        for (int k = 0; k < 16; ++k) { a0[k] = 0; a1[k] = 0; a2[k] = 0; }
+        const uint8_t *wl = wt + (h * NG + gam) * 3 * G;
 #pragma unroll 2
-      for (int gi = tg; gi < GQ; gi += NTG) {
-        const uint32_t w0 = *reinterpret_cast<const uint32_t *>(vc + (size_t)(gi) * (D / 4) + 4 * kw);
-        const uint32_t w1 = *reinterpret_cast<const uint32_t *>(vc + (size_t)(gi + GQ) * (D / 4) + 4 * kw);
-        const uint32_t w2 = *reinterpret_cast<const uint32_t *>(vc + (size_t)(gi + 2 * GQ) * (D / 4) + 4 * kw);
-        const uint32_t w3 = *reinterpret_cast<const uint32_t *>(vc + (size_t)(gi + 3 * GQ) * (D / 4) + 4 * kw);
-        const uint32_t l0 = *reinterpret_cast<const uint32_t *>(wl + 4 * gi);
-        const uint32_t l1 = *reinterpret_cast<const uint32_t *>(wl + G + 4 * gi);
-        const uint32_t l2 = *reinterpret_cast<const uint32_t *>(wl + 2 * G + 4 * gi);
-        const uint32_t ta = prmt(w0, w1, 0x5140), tb = prmt(w0, w1, 0x7362);
-        const uint32_t tc = prmt(w2, w3, 0x5140), td = prmt(w2, w3, 0x7362);
-        const uint32_t Gb[4] = {prmt(ta, tc, 0x5410), prmt(ta, tc, 0x7632), prmt(tb, td, 0x5410),
-                                prmt(tb, td, 0x7632)};
+        for (int gi = tg; gi < GQ; gi += NTG) {
+          const uint32_t w0 = *reinterpret_cast<const uint32_t *>(vc + (size_t)(gi) * (D / 4) + 4 * kw);
+          const uint32_t w1 = *reinterpret_cast<const uint32_t *>(vc + (size_t)(gi + GQ) * (D / 4) + 4 * kw);
+          const uint32_t w2 = *reinterpret_cast<const uint32_t *>(vc + (size_t)(gi + 2 * GQ) * (D / 4) + 4 * kw);
+          const uint32_t w3 = *reinterpret_cast<const uint32_t *>(vc + (size_t)(gi + 3 * GQ) * (D / 4) + 4 * kw);
+          const uint32_t l0 = *reinterpret_cast<const uint32_t *>(wl + 4 * gi);
+          const uint32_t l1 = *reinterpret_cast<const uint32_t *>(wl + G + 4 * gi);
+          const uint32_t l2 = *reinterpret_cast<const uint32_t *>(wl + 2 * G + 4 * gi);
+          const uint32_t ta = prmt(w0, w1, 0x5140), tb = prmt(w0, w1, 0x7362);
+          const uint32_t tc = prmt(w2, w3, 0x5140), td = prmt(w2, w3, 0x7362);
+          const uint32_t Gb[4] = {prmt(ta, tc, 0x5410), prmt(ta, tc, 0x7632), prmt(tb, td, 0x5410),
+                                  prmt(tb, td, 0x7632)};
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb)
+          for (int bb = 0; bb < 4; ++bb)
 #pragma unroll
-          for (int s = 0; s < 4; ++s) {
-            const uint32_t x = Gb[bb] & (0x03030303u << (2 * s));   // code * 4^s per byte
-            a0[bb * 4 + s] = dp4a_uu(x, l0, a0[bb * 4 + s]);
-            a1[bb * 4 + s] = dp4a_uu(x, l1, a1[bb * 4 + s]);
-            a2[bb * 4 + s] = dp4a_uu(x, l2, a2[bb * 4 + s]);
-          }
-      }
-      float dwl = dw[0];
+            for (int s = 0; s < 4; ++s) {
+              const uint32_t x = Gb[bb] & (0x03030303u << (2 * s));   // code * 4^s per byte
+              a0[bb * 4 + s] = dp4a_uu(x, l0, a0[bb * 4 + s]);
+              a1[bb * 4 + s] = dp4a_uu(x, l1, a1[bb * 4 + s]);
+              a2[bb * 4 + s] = dp4a_uu(x, l2, a2[bb * 4 + s]);
+            }
+        }
 #pragma unroll
-      for (int gi = 1; gi < NG; ++gi) if (gi == gam) dwl = dw[gi];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const float sck = dwl * (1.0f / (float)(1 << (2 * (k & 3))));
-        const float val = fmaf((float)a2[k], 65536.f, fmaf((float)a1[k], 256.f, (float)a0[k]));
-        o[h][k] = fmaf(val, sck, o[h][k] * sc);
+        for (int k = 0; k < 16; ++k) {
+          const float sck = dwl * (1.0f / (float)(1 << (2 * (k & 3))));
+          const float val = fmaf((float)a2[k], 65536.f, (float)(a1[k] * 256 + a0[k]));
+          o[h][k] = fmaf(val, sck, o[h][k] * sc);
+        }
       }
     }
     __syncwarp();
-    if (lane == 0 && it + kStages < ie) issue(it + kStages, st);
+    if (lane == 0 && si + kStages < nsub) issue(si + kStages, st);
   }
   if (cur_u >= 0) flush(cur_u);
 }
 
 // Shared memory bytes of one CTA of the page kernel.
 template <int D, int G, int NH>
-static size_t pg_smem(size_t pb) {
-  return (size_t)kPgWarps * PgSmem<D, G, NH>::warp_bytes(pb);
+static size_t pg_smem(size_t sb) {
+  return (size_t)kPgWarps * PgSmem<D, G, NH>::warp_bytes(sb);
 }
 
 template <int D, int G, int DT, int NH>
 static cudaError_t launch_pg(const DevCache &c, const PagePlan &pp, const RowPlan &rp, const void *q,
                              float *pg_part, const float *rw_part, float *out, uint32_t flags,
                              cudaStream_t st) {
-  const size_t smem = pg_smem<D, G, NH>(c.page_bytes);
+  const size_t smem = pg_smem<D, G, NH>(pg_stage_bytes(c.page_bytes, c.pg_vscale));
   auto kern = k_decode_pages<D, G, DT, NH>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg = {};

@@ -63,9 +63,9 @@ __global__ void __launch_bounds__(kRwWarps * 32)
 
   pdl_wait();                     // q / k / v come from the preceding kernels
   pdl_launch_dependents();        // the page kernel may start filling idle SMs
-  const long long gw = (long long)blockIdx.x * kRwWarps + warp;
-  if (gw >= rp.W) return;
-  const long long ib = gw * rp.T / rp.W, ie = (gw + 1) * rp.T / rp.W;
+  const int gw = blockIdx.x * kRwWarps + warp;
+  if (gw >= (int)rp.W) return;
+  const int ib = seg_begin((int)rp.T, (int)rp.W, gw), ie = seg_begin((int)rp.T, (int)rp.W, gw + 1);
   if (ib >= ie) return;
   const int per_u = rp.items_per_unit;
   const bool tsa = c.kind == AKVQ_TSA;
@@ -81,10 +81,10 @@ __global__ void __launch_bounds__(kRwWarps * 32)
 
   // item -> (unit, kind, first row, rows); side items are split by the device count
   struct Item { int u, kind, r0, n; };   // kind 0 ring, 1 side
-  auto decode_item = [&](long long it) {
+  auto decode_item = [&](int it) {
     Item x;
-    x.u = (int)(it / per_u);
-    const int k = (int)(it % per_u);
+    x.u = it / per_u;
+    const int k = it - x.u * per_u;
     if (k < rp.n_ring_chunks) {
       x.kind = 0;
       x.r0 = k * kChunk;
@@ -92,8 +92,8 @@ __global__ void __launch_bounds__(kRwWarps * 32)
     } else {
       const int r = k - rp.n_ring_chunks;
       const int cnt = c.side_cnt[x.u];
-      const int a = (int)((long long)r * cnt / rp.n_side_splits);
-      const int b = (int)((long long)(r + 1) * cnt / rp.n_side_splits);
+      const int a = r * cnt / rp.n_side_splits;
+      const int b = (r + 1) * cnt / rp.n_side_splits;
       x.kind = 1;
       x.r0 = a;
       x.n = b - a;
@@ -123,13 +123,13 @@ __global__ void __launch_bounds__(kRwWarps * 32)
   };
 
   // flattened (item, sub-chunk) stream for the pipeline
-  long long it_cur = ib;
+  int it_cur = ib;
   int sub_cur = 0;
   Item x_cur = decode_item(ib);
-  long long it_nx = ib;           // producer cursor (lane 0 only uses it)
+  int it_nx = ib;           // producer cursor (lane 0 only uses it)
   int sub_nx = 0;
   Item x_nx = x_cur;
-  auto advance = [&](long long &it, int &sub, Item &x) {
+  auto advance = [&](int &it, int &sub, Item &x) {
     ++sub;
     if (sub * kChunk >= x.n) {
       sub = 0;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kRwWarps * 32)
     }
   };
   // skip empty items at the producer start
-  auto skip_empty = [&](long long &it, int &sub, Item &x) {
+  auto skip_empty = [&](int &it, int &sub, Item &x) {
     while (it < ie && x.n <= 0) {
       ++it;
       sub = 0;
@@ -159,13 +159,13 @@ __global__ void __launch_bounds__(kRwWarps * 32)
 
   float m_run[NH], l_run[NH], o_org[NH][16], o_rot[NH][16], Zr[NH][NG];
   int cur_u = -1;
-  const int u_first = (int)(ib / per_u);
+  const int u_first = ib / per_u;
   const int tq = lane >> 1, half = lane & 1;
   const int kw = lane % KPR, tg = lane / KPR;
   const int gam = (16 * kw) / G;
 
   auto flush = [&](int u) {
-    const size_t slot = (size_t)(gw * rp.maxseg + (u - u_first));
+    const size_t slot = (size_t)gw * rp.maxseg + (u - u_first);
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
       float zg = Zr[h][0];
@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(kRwWarps * 32)
     }
     // without quantized pages nothing follows this kernel: merge here
     if (pp.T <= 0) {
-      long long w_lo, w_hi;
-      seg_range(rp.T, rp.W, rp.items_per_unit, u, w_lo, w_hi);
+      int w_lo, w_hi;
+      seg_range((int)rp.T, (int)rp.W, rp.items_per_unit, u, w_lo, w_hi);
       if (take_ticket(c, u, (int)(w_hi - w_lo + 1), lane)) {
         merge_unit<D, NH>(c, pp, rp, pg_part, rw_part, u, out, flags, lane);
         if (lane == 0) c.ticket[u] = 0u;
