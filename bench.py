@@ -222,6 +222,8 @@ def main():
     ap.add_argument("--impl", default="akvq", choices=["akvq", "reference"])
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stream-only", action="store_true",
+                    help="profiling: kernels stream their bytes but skip the math (invalid outputs)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -259,6 +261,8 @@ def main():
         kind = w.kind(layer)
         cfg = ak.make_config(Ul, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4)
         lc = ak.LayerCache(cfg, device=dev)
+        if args.stream_only:
+            lc.handle.options = ak.AKVQ_OPT_STREAM_ONLY
         inp = synth.layer_inputs(w, layer, units=units, device=dev)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

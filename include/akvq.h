@@ -134,6 +134,10 @@ typedef struct {
 /* akvq_cache.options: route 2-bit pages through the generic split-K kernel
  * instead of the persistent dp4a page kernel (test hook for cross-checks). */
 #define AKVQ_OPT_GENERIC_PAGES 1
+/* Profiling hook: the fast decode kernels stream every byte they would read
+ * (same TMA pipeline) but skip all arithmetic; outputs are garbage.  Used
+ * only to measure the memory pipeline's ceiling (bench.py --stream-only). */
+#define AKVQ_OPT_STREAM_ONLY 2
 
 typedef struct {      /* memory_report, host arithmetic           */
   double bytes_fp16, bytes_int4, bytes_int2, bytes_overhead;

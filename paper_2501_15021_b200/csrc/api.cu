@@ -117,6 +117,7 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
       p.rp.items_per_unit = 1;
     }
     p.n_page_splits = p.n_ring_splits = p.n_side_splits = 0;
+    p.pp.stream_only = p.rp.stream_only = (c->options & AKVQ_OPT_STREAM_ONLY) ? 1 : 0;
   }
   p.S = p.n_page_splits + p.n_ring_splits + p.n_side_splits;
   return p;

@@ -6,10 +6,10 @@
 // K codes, V meta, V codes, contiguous in HBM) into shared memory with 1-D TMA
 // bulk copies (cp.async.bulk + mbarrier).  Dequantize-and-dot runs on the
 // integer dp4a path (profiles/r01_microbench_pipes.md):
-//   logits:  q~ prescaled by the page's per-channel K scale, rounded to a 22-bit
-//            fixed-point integer per page (3 int8 limbs), dotted with the codes
-//            as bytes: sum_c Qq_c * code_tc exactly in int32, then
-//            logit = alpha * (delta * sum - sum_c qs_c z_c)        (Eqs. 3-4)
+//   logits:  q~ prescaled by the page's per-channel K scale, rounded to a 16-bit
+//            fixed-point integer per page (2 int8 limbs), dotted with the codes
+//            as bytes: sum_c Qq_c * (code_tc - z_c) exactly in int32, then
+//            logit = alpha * delta * sum                           (Eqs. 3-4)
 //   values:  softmax weights w_t = p_t * s^V_t rounded to 24-bit fixed point of
 //            the page's largest weight (3 uint8 limbs); codes of 4 tokens are
 //            transposed into bytes with PRMT and accumulated with dp4a:
@@ -24,6 +24,7 @@ namespace akvq {
 
 constexpr int kPgWarps = 4;
 constexpr int kStages = 3;
+constexpr int kQMax = 32767;       // K-side fixed point: |Q| <= 2^15 - 1 (2 limbs)
 
 // Per-warp shared-memory block (bytes): kStages half-page stages, q~, limbs,
 // transposed value weights, barriers.  sb = stage bytes (>= either page half).
@@ -82,17 +83,19 @@ __global__ void __launch_bounds__(kPgWarps * 32, 3)
     mbar_fence_init();
   }
   __syncwarp();
-  // sub-load si: page ib + si/2, K half (even si) or V half (odd si)
-  auto issue = [&](int si, int st) {
-    const int item = ib + (si >> 1);
-    const int u = item / npg, p = item - u * npg;
-    const uint8_t *src = page_ptr(c, u, p) + ((si & 1) ? kbytes : 0u);
-    const uint32_t nb = (si & 1) ? vbytes : kbytes;
-    mbar_expect_tx(&bar[st], nb);
-    bulk_g2s(wsm + (size_t)st * SB, src, nb, &bar[st]);
+  // producer cursor (lane 0): sub-load pi is page (pu, pp_) K half (even) or V half (odd)
+  int pi = 0, pu = ib / npg, ppg = ib - (ib / npg) * npg, pst = 0;
+  auto issue_next = [&]() {
+    const uint8_t *src = page_ptr(c, pu, ppg) + ((pi & 1) ? kbytes : 0u);
+    const uint32_t nb = (pi & 1) ? vbytes : kbytes;
+    mbar_expect_tx(&bar[pst], nb);
+    bulk_g2s(wsm + (size_t)pst * SB, src, nb, &bar[pst]);
+    if (pi & 1) { if (++ppg == npg) { ppg = 0; ++pu; } }
+    ++pi;
+    if (++pst == kStages) pst = 0;
   };
   if (lane == 0)
-    for (int s = 0; s < kStages && s < nsub; ++s) issue(s, s);
+    for (int s = 0; s < kStages && s < nsub; ++s) issue_next();
 
   // per-head running state (online softmax, base 2)
   float m_run[NH], l_run[NH], Z[NH][NG], o[NH][16];
@@ -138,29 +141,55 @@ __global__ void __launch_bounds__(kPgWarps * 32, 3)
   };
 
   int u = u_first, pg = ib - u_first * npg;       // (unit, page) of the current sub-load
+  int st = 0;
+  uint32_t par = 0;
   for (int si = 0; si < nsub; ++si) {
-    const int st = si % kStages;
-    const uint32_t par = (uint32_t)((si / kStages) & 1);
     const uint8_t *B = wsm + (size_t)st * SB;
+    if (pp.stream_only) {                          // profiling: pipeline only
+      mbar_wait(&bar[st], par);
+      __syncwarp();
+      if (lane == 0 && pi < nsub) issue_next();
+      if (++st == kStages) { st = 0; par ^= 1u; }
+      continue;
+    }
     if ((si & 1) == 0) {
       if (si > 0 && ++pg == npg) { pg = 0; ++u; }
       if (u != cur_u) {
         if (cur_u >= 0) flush(cur_u);
         cur_u = u;
-        // q~ = q . H_s for this unit (unnormalized FWHT in smem, warp-local)
-        for (int i = lane; i < NH * D; i += 32) qh[i] = H16<DT>::to_f(q[(size_t)u * c.g * D + i]);
-        __syncwarp();
+        // q~ = q . H_s for this unit: lane holds D/32 contiguous channels,
+        // in-register butterflies then shuffle butterflies (unnormalized FWHT)
 #pragma unroll
-        for (int hs = 1; hs < D; hs <<= 1) {
-          for (int idx = lane; idx < NH * D / 2; idx += 32) {
-            const int h = idx / (D / 2), k = idx % (D / 2);
-            const int i = (k / hs) * 2 * hs + (k % hs);
-            const float a = qh[h * D + i], b = qh[h * D + i + hs];
-            qh[h * D + i] = a + b;
-            qh[h * D + i + hs] = a - b;
+        for (int h = 0; h < NH; ++h) {
+          constexpr int CPL = D / 32;
+          float x[CPL];
+          const uint16_t *qs = q + ((size_t)u * c.g + h) * D + CPL * lane;
+          if constexpr (CPL == 4) {
+            const uint2 v = *reinterpret_cast<const uint2 *>(qs);
+            x[0] = H16<DT>::to_f((uint16_t)(v.x & 0xffff)); x[1] = H16<DT>::to_f((uint16_t)(v.x >> 16));
+            x[2] = H16<DT>::to_f((uint16_t)(v.y & 0xffff)); x[3] = H16<DT>::to_f((uint16_t)(v.y >> 16));
+          } else {
+            const uint32_t v = *reinterpret_cast<const uint32_t *>(qs);
+            x[0] = H16<DT>::to_f((uint16_t)(v & 0xffff)); x[1] = H16<DT>::to_f((uint16_t)(v >> 16));
           }
-          __syncwarp();
+#pragma unroll
+          for (int hs = 1; hs < CPL; hs <<= 1)
+#pragma unroll
+            for (int k = 0; k < CPL; ++k)
+              if (!(k & hs)) { const float a = x[k], b = x[k + hs]; x[k] = a + b; x[k + hs] = a - b; }
+#pragma unroll
+          for (int lm = 1; lm < 32; lm <<= 1) {
+            const bool upper = lane & lm;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              const float o2 = __shfl_xor_sync(0xffffffffu, x[k], lm);
+              x[k] = upper ? o2 - x[k] : x[k] + o2;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) qh[h * D + CPL * lane + k] = x[k];
         }
+        __syncwarp();
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
           m_run[h] = -INFINITY; l_run[h] = 0.f;
@@ -187,35 +216,39 @@ __global__ void __launch_bounds__(kPgWarps * 32, 3)
           const int k = lane >> 2, s = lane & 3;
           int Qv[4] = {0, 0, 0, 0};
           float qsb[4] = {0.f, 0.f, 0.f, 0.f};
-          float bp = 0.f, am = 0.f;
+          float am = 0.f;
           if (k < D / 16) {
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
               const int ch = 16 * k + 4 * b + s;
               qsb[b] = qh[h * D + ch] * ks[ch];
-              bp = fmaf(qsb[b], (float)kz[ch], bp);
               am = fmaxf(am, fabsf(qsb[b]));
             }
           }
-          bias = warp_sum(bp);
           const float M = warp_max(am);
-          const float inv = M > 0.f ? 2097151.0f / M : 0.f;       // |Q| <= 2^21 - 1
-          delta = M > 0.f ? M / 2097151.0f : 0.f;
+          const float inv = M > 0.f ? (float)kQMax / M : 0.f;
+          delta = M > 0.f ? M / (float)kQMax : 0.f;
+          long long bq = 0;   // zero-point bias from the same fixed-point q (exact, 64-bit)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) Qv[b] = __float2int_rn(qsb[b] * inv);
+          for (int b = 0; b < 4; ++b) {
+            Qv[b] = __float2int_rn(qsb[b] * inv);
+            if (k < D / 16) bq += (long long)Qv[b] * kz[16 * k + 4 * b + s];
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) bq += __shfl_xor_sync(0xffffffffu, bq, o);
+          bias = delta * (float)bq;
           const uint32_t lo = prmt(prmt(Qv[0], Qv[1], 0x0040), prmt(Qv[2], Qv[3], 0x0040), 0x5410);
-          const uint32_t mi = prmt(prmt(Qv[0], Qv[1], 0x0051), prmt(Qv[2], Qv[3], 0x0051), 0x5410);
-          const uint32_t hi = prmt(prmt(Qv[0], Qv[1], 0x0062), prmt(Qv[2], Qv[3], 0x0062), 0x5410);
-          limbs[h * 32 + lane] = make_uint4(lo, mi, hi, 0u);
+          const uint32_t hi = prmt(prmt(Qv[0], Qv[1], 0x0051), prmt(Qv[2], Qv[3], 0x0051), 0x5410);
+          limbs[h * 32 + lane] = make_uint4(lo, hi, 0u, 0u);
         }
         __syncwarp();
-        uint32_t lim[KWL][4][3];
+        uint32_t lim[KWL][4][2];
 #pragma unroll
         for (int w = 0; w < KWL; ++w)
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
-            const uint4 v = limbs[h * 32 + 4 * (half * KWL + w) + s];
-            lim[w][s][0] = v.x; lim[w][s][1] = v.y; lim[w][s][2] = v.z;
+            const uint2 v = *reinterpret_cast<const uint2 *>(&limbs[h * 32 + 4 * (half * KWL + w) + s]);
+            lim[w][s][0] = v.x; lim[w][s][1] = v.y;
           }
 #pragma unroll
         for (int ps = 0; ps < PASSES; ++ps) {
@@ -230,17 +263,16 @@ __global__ void __launch_bounds__(kPgWarps * 32, 3)
           }
           // two independent accumulator sets (even / odd words) to halve the
           // dp4a dependency chains
-          int a0[2] = {0, 0}, a1[2] = {0, 0}, a2[2] = {0, 0};
+          int a0[2] = {0, 0}, a1[2] = {0, 0};
 #pragma unroll
           for (int w = 0; w < KWL; ++w)
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
               const uint32_t x = (wd[w] >> (2 * s)) & 0x03030303u;
               a0[w & 1] = dp4a_uu(x, lim[w][s][0], a0[w & 1]);
-              a1[w & 1] = dp4a_uu(x, lim[w][s][1], a1[w & 1]);
-              a2[w & 1] = dp4a_us(x, lim[w][s][2], a2[w & 1]);
+              a1[w & 1] = dp4a_us(x, lim[w][s][1], a1[w & 1]);
             }
-          int tot = (a2[0] + a2[1]) * 65536 + (a1[0] + a1[1]) * 256 + (a0[0] + a0[1]);
+          int tot = (a1[0] + a1[1]) * 256 + (a0[0] + a0[1]);
           tot += __shfl_xor_sync(0xffffffffu, tot, 1);
           const bool sal = (bits[t >> 5] >> (t & 31)) & 1u;
           lgp[h][ps] = sal ? -INFINITY : alpha * fmaf((float)tot, delta, -bias);
@@ -346,9 +378,10 @@ __global__ void __launch_bounds__(kPgWarps * 32, 3)
       }
     }
     __syncwarp();
-    if (lane == 0 && si + kStages < nsub) issue(si + kStages, st);
+    if (lane == 0 && pi < nsub) issue_next();        // refills stage st
+    if (++st == kStages) { st = 0; par ^= 1u; }
   }
-  if (cur_u >= 0) flush(cur_u);
+  if (cur_u >= 0 && !pp.stream_only) flush(cur_u);
 }
 
 // Shared memory bytes of one CTA of the page kernel.

@@ -245,6 +245,17 @@ __global__ void __launch_bounds__(kRwWarps * 32)
       }
     }
     mbar_wait(&bar[st], par);
+    if (rp.stream_only) {                             // profiling: pipeline only
+      __syncwarp();
+      if (lane == 0 && n_issued > 0 && it_nx < ie) {
+        issue(x_nx, sub_nx, st);
+        advance(it_nx, sub_nx, x_nx);
+        skip_empty(it_nx, sub_nx, x_nx);
+      }
+      advance(it_cur, sub_cur, x_cur);
+      skip_empty(it_cur, sub_cur, x_cur);
+      continue;
+    }
     const uint8_t *B = wsm + (size_t)st * S::stage;
     const bool rows16 = x.kind == 0 || !tsa;
     // the newest token (Eq. 2): attend to the caller's row -- the stale ring
@@ -389,7 +400,7 @@ __global__ void __launch_bounds__(kRwWarps * 32)
     advance(it_cur, sub_cur, x_cur);
     skip_empty(it_cur, sub_cur, x_cur);
   }
-  if (cur_u >= 0) flush(cur_u);
+  if (cur_u >= 0 && !rp.stream_only) flush(cur_u);
 }
 
 template <int D, int NH>

@@ -23,6 +23,7 @@ struct PagePlan {
   long long W;
   int n_pages;
   int maxseg;
+  int stream_only;      // AKVQ_OPT_STREAM_ONLY (profiling)
 };
 
 // Persistent row-kernel plan: per unit, n_ring_chunks items of 16 ring tokens
@@ -36,6 +37,7 @@ struct RowPlan {
   int n_side_splits;
   int maxseg;
   int L, n_q;
+  int stream_only;      // AKVQ_OPT_STREAM_ONLY (profiling)
 };
 
 // Decode split plan (host-computed, uniform across units).
