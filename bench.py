@@ -224,6 +224,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stream-only", action="store_true",
                     help="profiling: kernels stream their bytes but skip the math (invalid outputs)")
+    ap.add_argument("--skip-rows", action="store_true", help="profiling: no row kernel (invalid)")
+    ap.add_argument("--skip-pages", action="store_true", help="profiling: no page kernel (invalid)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -261,8 +263,9 @@ def main():
         kind = w.kind(layer)
         cfg = ak.make_config(Ul, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4)
         lc = ak.LayerCache(cfg, device=dev)
-        if args.stream_only:
-            lc.handle.options = ak.AKVQ_OPT_STREAM_ONLY
+        lc.handle.options = ((ak.AKVQ_OPT_STREAM_ONLY if args.stream_only else 0) |
+                             (ak.AKVQ_OPT_SKIP_ROWS if args.skip_rows else 0) |
+                             (ak.AKVQ_OPT_SKIP_PAGES if args.skip_pages else 0))
         inp = synth.layer_inputs(w, layer, units=units, device=dev)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -138,6 +138,10 @@ typedef struct {
  * (same TMA pipeline) but skip all arithmetic; outputs are garbage.  Used
  * only to measure the memory pipeline's ceiling (bench.py --stream-only). */
 #define AKVQ_OPT_STREAM_ONLY 2
+/* Profiling hooks: skip the row kernel / the page kernel entirely (outputs are
+ * garbage); used to attribute the decode time (bench.py --skip-rows/pages). */
+#define AKVQ_OPT_SKIP_ROWS 4
+#define AKVQ_OPT_SKIP_PAGES 8
 
 typedef struct {      /* memory_report, host arithmetic           */
   double bytes_fp16, bytes_int4, bytes_int2, bytes_overhead;

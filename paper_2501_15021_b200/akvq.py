@@ -22,6 +22,8 @@ AKVQ_BF16, AKVQ_FP16 = 0, 1
 AKVQ_OUT_ROTATED = 1
 AKVQ_OPT_GENERIC_PAGES = 1
 AKVQ_OPT_STREAM_ONLY = 2
+AKVQ_OPT_SKIP_ROWS = 4
+AKVQ_OPT_SKIP_PAGES = 8
 AKVQ_MAX_PSA_PROMPT = 49152
 
 # every symbol include/akvq.h declares

@@ -139,9 +139,11 @@ akvq_status launch_fast(const akvq_cache *c, const DecodePlan &p, const void *q,
   const size_t g = c->cfg.q_per_kv, dd = c->cfg.head_dim;
   float *pg_part = static_cast<float *>(ws);
   float *rw_part = pg_part + (size_t)p.pp.W * p.pp.maxseg * g * (dd + 4);
-  cudaError_t e = launch_decode_rows(d, c->cfg.dtype16, p.rp, p.pp, q, k, v, types, rw_part,
-                                     pg_part, out, flags, s);
-  if (e == cudaSuccess)
+  cudaError_t e = cudaSuccess;
+  if (!(c->options & AKVQ_OPT_SKIP_ROWS))
+    e = launch_decode_rows(d, c->cfg.dtype16, p.rp, p.pp, q, k, v, types, rw_part, pg_part, out,
+                           flags, s);
+  if (e == cudaSuccess && !(c->options & AKVQ_OPT_SKIP_PAGES))
     e = launch_decode_pages(d, c->cfg.dtype16, p.pp, p.rp, q, pg_part, rw_part, out, flags, s);
   return cuda_status(e);
 }

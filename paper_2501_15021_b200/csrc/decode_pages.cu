@@ -25,6 +25,7 @@ namespace akvq {
 constexpr int kPgWarps = 4;
 constexpr int kStages = 3;
 constexpr int kQMax = 32767;       // K-side fixed point: |Q| <= 2^15 - 1 (2 limbs)
+constexpr int kWMax = 65535;       // V-side fixed point: W <= 2^16 - 1 (2 limbs)
 
 // Per-warp shared-memory block (bytes): kStages half-page stages, q~, limbs,
 // transposed value weights, barriers.  sb = stage bytes (>= either page half).
@@ -35,7 +36,7 @@ struct PgSmem {
   static __host__ __device__ size_t limb_off(size_t sb) { return qh_off(sb) + NH * D * 4; }
   static __host__ __device__ size_t wt_off(size_t sb) { return limb_off(sb) + NH * 32 * 16; }
   static __host__ __device__ size_t bar_off(size_t sb) {
-    return (wt_off(sb) + NH * NG * 3 * G + 15) / 16 * 16;
+    return (wt_off(sb) + NH * NG * 2 * G + 15) / 16 * 16;
   }
   static __host__ __device__ size_t warp_bytes(size_t sb) {
     return (bar_off(sb) + kStages * 8 + 127) / 128 * 128;
@@ -308,44 +309,46 @@ __global__ void __launch_bounds__(kPgWarps * 32, 3)
         float dwl = 0.f;
 #pragma unroll
         for (int gi = 0; gi < NG; ++gi) {
-          float wv[PASSES], wmax = 0.f, zs = 0.f;
+          float wv[PASSES], wmax = 0.f;
 #pragma unroll
           for (int ps = 0; ps < PASSES; ++ps) {
             const int t = ps * 16 + tq;
             wv[ps] = pr[ps] * vs[t * NG + gi];
             wmax = fmaxf(wmax, wv[ps]);
-            zs = fmaf(wv[ps], (float)vz[t * NG + gi], zs);
           }
 #pragma unroll
-          for (int off = 2; off < 32; off <<= 1) {
-            wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
-            zs += __shfl_xor_sync(0xffffffffu, zs, off);
-          }
-          Z[h][gi] = Z[h][gi] * sc + zs;
-          // 24-bit fixed point of the page's largest weight (3 uint8 limbs): the
-          // per-token rounding error is shared by all d channels of the token and
-          // adds coherently under the output H, so 16 bits are not enough.
-          const float invw = wmax > 0.f ? 16777215.0f / wmax : 0.f;
-          if (gi == gam) dwl = wmax / 16777215.0f;
-          if (half == 0) {
-            uint8_t *wl = wt + (h * NG + gi) * 3 * G;
+          for (int off = 2; off < 32; off <<= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
+          // 16-bit fixed point of the page's largest weight (2 uint8 limbs).  The
+          // zero-point term uses the same rounded weights, so the rounding error
+          // multiplies (code - z) -- a dequantized row -- and stays incoherent
+          // across channels (with the exact w it multiplied code >= 0 and piled
+          // up in output channel 0 under H).
+          const float invw = wmax > 0.f ? (float)kWMax / wmax : 0.f;
+          const float dw = wmax / (float)kWMax;
+          if (gi == gam) dwl = dw;
+          long long zq = 0;                          // sum_t W_t z_t, exact
+          uint8_t *wl = wt + (h * NG + gi) * 2 * G;
 #pragma unroll
-            for (int ps = 0; ps < PASSES; ++ps) {
-              const int t = ps * 16 + tq;
-              const uint32_t W = min(__float2uint_rn(wv[ps] * invw), 16777215u);  // may round up
+          for (int ps = 0; ps < PASSES; ++ps) {
+            const int t = ps * 16 + tq;
+            const uint32_t W = min(__float2uint_rn(wv[ps] * invw), (uint32_t)kWMax);  // may round up
+            if (half == 0) {
+              zq += (long long)W * vz[t * NG + gi];
               const int idx = (t % GQ) * 4 + t / GQ;
               wl[idx] = (uint8_t)W;
               wl[G + idx] = (uint8_t)(W >> 8);
-              wl[2 * G + idx] = (uint8_t)(W >> 16);
             }
           }
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) zq += __shfl_xor_sync(0xffffffffu, zq, off);
+          Z[h][gi] = Z[h][gi] * sc + dw * (float)zq;
         }
         __syncwarp();
         // o'_c += sum_t W_t code_tc  (dp4a over 4 tokens, codes transposed by PRMT)
-        int a0[16], a1[16], a2[16];
+        int a0[16], a1[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) { a0[k] = 0; a1[k] = 0; a2[k] = 0; }
-        const uint8_t *wl = wt + (h * NG + gam) * 3 * G;
+        for (int k = 0; k < 16; ++k) { a0[k] = 0; a1[k] = 0; }
+        const uint8_t *wl = wt + (h * NG + gam) * 2 * G;
 #pragma unroll 2
         for (int gi = tg; gi < GQ; gi += NTG) {
           const uint32_t w0 = *reinterpret_cast<const uint32_t *>(vc + (size_t)(gi) * (D / 4) + 4 * kw);
@@ -354,7 +357,6 @@ __global__ void __launch_bounds__(kPgWarps * 32, 3)
           const uint32_t w3 = *reinterpret_cast<const uint32_t *>(vc + (size_t)(gi + 3 * GQ) * (D / 4) + 4 * kw);
           const uint32_t l0 = *reinterpret_cast<const uint32_t *>(wl + 4 * gi);
           const uint32_t l1 = *reinterpret_cast<const uint32_t *>(wl + G + 4 * gi);
-          const uint32_t l2 = *reinterpret_cast<const uint32_t *>(wl + 2 * G + 4 * gi);
           const uint32_t ta = prmt(w0, w1, 0x5140), tb = prmt(w0, w1, 0x7362);
           const uint32_t tc = prmt(w2, w3, 0x5140), td = prmt(w2, w3, 0x7362);
           const uint32_t Gb[4] = {prmt(ta, tc, 0x5410), prmt(ta, tc, 0x7632), prmt(tb, td, 0x5410),
@@ -366,13 +368,12 @@ __global__ void __launch_bounds__(kPgWarps * 32, 3)
               const uint32_t x = Gb[bb] & (0x03030303u << (2 * s));   // code * 4^s per byte
               a0[bb * 4 + s] = dp4a_uu(x, l0, a0[bb * 4 + s]);
               a1[bb * 4 + s] = dp4a_uu(x, l1, a1[bb * 4 + s]);
-              a2[bb * 4 + s] = dp4a_uu(x, l2, a2[bb * 4 + s]);
             }
         }
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const float sck = dwl * (1.0f / (float)(1 << (2 * (k & 3))));
-          const float val = fmaf((float)a2[k], 65536.f, (float)(a1[k] * 256 + a0[k]));
+          const float val = (float)(a1[k] * 256 + a0[k]);          // < 2^31: 32 tokens x 192 x 65535
           o[h][k] = fmaf(val, sck, o[h][k] * sc);
         }
       }
