@@ -129,6 +129,8 @@ typedef struct {
   int32_t n_q;
   int32_t sm_count;    /* filled at init, used to size decode grids           */
   int32_t options;     /* AKVQ_OPT_* bits, 0 by default (set after init)      */
+  int32_t launches;    /* kernels enqueued by the last call on this cache
+                          (host counter, for launch accounting in bench.py)  */
 } akvq_cache;
 
 /* akvq_cache.options: route 2-bit pages through the generic split-K kernel

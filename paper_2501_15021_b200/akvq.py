@@ -59,7 +59,7 @@ class akvq_layout(C.Structure):
 class akvq_cache(C.Structure):
     _fields_ = [("cfg", akvq_config), ("lay", akvq_layout), ("base", C.c_void_p),
                 ("L", C.c_int32), ("n_q", C.c_int32), ("sm_count", C.c_int32),
-                ("options", C.c_int32)]
+                ("options", C.c_int32), ("launches", C.c_int32)]
 
 
 class akvq_mem_report(C.Structure):
@@ -254,6 +254,11 @@ class LayerCache:
             out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
         akvq_decode_step(self.handle, k, v, types, q, out, self.ws, flags, stream)
         return out
+
+    @property
+    def last_launches(self) -> int:
+        """Kernels the library enqueued in the last call on this cache."""
+        return self.handle.launches
 
     def view(self, stream=None):
         U, d = self.cfg.n_units, self.cfg.head_dim

@@ -140,6 +140,10 @@ akvq_status launch_fast(const akvq_cache *c, const DecodePlan &p, const void *q,
   float *pg_part = static_cast<float *>(ws);
   float *rw_part = pg_part + (size_t)p.pp.W * p.pp.maxseg * g * (dd + 4);
   cudaError_t e = cudaSuccess;
+  int n = 0;
+  if (!(c->options & AKVQ_OPT_SKIP_ROWS) && p.rp.T > 0) ++n;
+  if (!(c->options & AKVQ_OPT_SKIP_PAGES) && p.pp.T > 0) ++n;
+  const_cast<akvq_cache *>(c)->launches += n;
   if (!(c->options & AKVQ_OPT_SKIP_ROWS))
     e = launch_decode_rows(d, c->cfg.dtype16, p.rp, p.pp, q, k, v, types, rw_part, pg_part, out,
                            flags, s);
@@ -242,6 +246,7 @@ akvq_status akvq_rotate_quantize(akvq_cache *c, const void *K, const void *V, in
   if (L0 > 0 && (!K || !V)) return AKVQ_EINVAL;
   akvq_status st = akvq_select_salient(c, types, colsum, L0, stream);
   if (st != AKVQ_OK) return st;
+  c->launches = (c->cfg.kind == AKVQ_TSA || c->cfg.top_k > 0) && L0 > 0 ? 1 : 0;
   const akvq_config &f = c->cfg;
   const int n_q = L0 > f.residual ? (L0 - f.residual) / f.group * f.group : 0;   // R9
   const DevCache d = make_dev(c);
@@ -255,14 +260,15 @@ akvq_status akvq_rotate_quantize(akvq_cache *c, const void *K, const void *V, in
   const int nb = n_q / f.group;
   cudaError_t e = launch_quantize_blocks(d, f.dtype16, src, 0, nb, nb - 1, s);
   if (e == cudaSuccess) e = launch_ring_fill(d, K, V, L0, n_q, L0, s);
+  c->launches += (nb > 0) + (L0 > n_q);
   if (e != cudaSuccess) return AKVQ_ECUDA;
   c->L = L0;
   c->n_q = n_q;
   return AKVQ_OK;
 }
 
-akvq_status akvq_append_token(akvq_cache *c, const void *k, const void *v,
-                              const uint8_t *types, akvq_stream_t stream) {
+static akvq_status append_impl(akvq_cache *c, const void *k, const void *v, const uint8_t *types,
+                        akvq_stream_t stream) {
   if (!c || !c->base || !k || !v) return AKVQ_EINVAL;
   const akvq_config &f = c->cfg;
   if (c->L >= f.capacity) return AKVQ_ECAPACITY;
@@ -270,6 +276,7 @@ akvq_status akvq_append_token(akvq_cache *c, const void *k, const void *v,
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = launch_append(d, k, v, types, c->L, s);
   if (e != cudaSuccess) return AKVQ_ECUDA;
+  c->launches += 1;
   c->L += 1;
   if (c->L - f.residual - c->n_q >= f.group) {        // block leaves the window (R9)
     QuantSrc src;
@@ -281,9 +288,16 @@ akvq_status akvq_append_token(akvq_cache *c, const void *k, const void *v,
     const int j = c->n_q / f.group;
     e = launch_quantize_blocks(d, f.dtype16, src, j, 1, j, s);
     if (e != cudaSuccess) return AKVQ_ECUDA;
+    c->launches += 1;
     c->n_q += f.group;
   }
   return AKVQ_OK;
+}
+
+akvq_status akvq_append_token(akvq_cache *c, const void *k, const void *v,
+                              const uint8_t *types, akvq_stream_t stream) {
+  if (c) c->launches = 0;
+  return append_impl(c, k, v, types, stream);
 }
 
 size_t akvq_decode_workspace_bytes(const akvq_cache *c) {
@@ -305,8 +319,8 @@ size_t akvq_decode_workspace_bytes_max(const akvq_cache *c) {
   return b > best ? b : best;
 }
 
-akvq_status akvq_decode_attention(const akvq_cache *c, const void *q, float *out, void *ws,
-                                  size_t ws_bytes, uint32_t flags, akvq_stream_t stream) {
+static akvq_status decode_impl(const akvq_cache *c, const void *q, float *out, void *ws,
+                        size_t ws_bytes, uint32_t flags, akvq_stream_t stream) {
   if (!c || !c->base || !q || !out || !ws) return AKVQ_EINVAL;
   if (c->L == 0) return AKVQ_ESTATE;
   const DecodePlan p = plan_decode(c, c->L, c->n_q);
@@ -314,13 +328,21 @@ akvq_status akvq_decode_attention(const akvq_cache *c, const void *q, float *out
   const DevCache d = make_dev(c);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (p.fast) return launch_fast(c, p, q, nullptr, nullptr, nullptr, out, ws, flags, s);
+  const_cast<akvq_cache *>(c)->launches += 2;         // split + combine
   return cuda_status(launch_decode(d, c->cfg.dtype16, p, q, out, ws, flags, s));
+}
+
+akvq_status akvq_decode_attention(const akvq_cache *c, const void *q, float *out, void *ws,
+                                  size_t ws_bytes, uint32_t flags, akvq_stream_t stream) {
+  if (c) const_cast<akvq_cache *>(c)->launches = 0;
+  return decode_impl(c, q, out, ws, ws_bytes, flags, stream);
 }
 
 akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const uint8_t *types,
                              const void *q, float *out, void *ws, size_t ws_bytes, uint32_t flags,
                              akvq_stream_t stream) {
   if (!c || !c->base || !k || !v || !q || !out || !ws) return AKVQ_EINVAL;
+  c->launches = 0;
   const akvq_config &f = c->cfg;
   if (c->L >= f.capacity) return AKVQ_ECAPACITY;
   const int L1 = c->L + 1;
@@ -328,9 +350,9 @@ akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const 
   const DecodePlan p = plan_decode(c, L1, flush ? c->n_q + f.group : c->n_q);
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
   if (flush || !p.fast || p.rp.T <= 0) {   // flush step (every G tokens) or generic path
-    akvq_status st = akvq_append_token(c, k, v, types, stream);
+    akvq_status st = append_impl(c, k, v, types, stream);
     if (st != AKVQ_OK) return st;
-    return akvq_decode_attention(c, q, out, ws, ws_bytes, flags, stream);
+    return decode_impl(c, q, out, ws, ws_bytes, flags, stream);
   }
   const akvq_status st = launch_fast(c, p, q, k, v, types, out, ws, flags,
                                      reinterpret_cast<cudaStream_t>(stream));

@@ -1,0 +1,21 @@
+#!/bin/bash
+# One gpurun call: GPU parity tests, smoke, bench, ncu launch list + full capture.
+# Usage (on the box): bash tools/gpu_round.sh TAG [what...]   what in {tests,smoke,bench,launches,full}
+TAG=${1:-r01}; shift
+WHAT=${@:-tests smoke bench launches full}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > $OUT/smi.txt 2>&1
+for w in $WHAT; do
+  case $w in
+    tests)  timeout 900 python -m pytest tests -m gpu -x -q > $OUT/tests.log 2>&1; echo "tests rc=$?" ;;
+    smoke)  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" ;;
+    bench)  timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; cat $OUT/bench.json ;;
+    launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+               -k regex:"k_(decode|append|quantize|salient|ring|view|combine)" --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1; echo "launches rc=$?" ;;
+    full)   for k in k_decode_pages k_decode_rows; do
+              timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 200 -c 1 \
+                -o $OUT/full_$k python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$k.log 2>&1; echo "full $k rc=$?"
+            done ;;
+  esac
+done
