@@ -3,6 +3,7 @@
 // Every entry point is asynchronous on the caller's stream, allocates no
 // device memory and never synchronizes.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "akvq.h"
@@ -58,6 +59,17 @@ DevCache make_dev(const akvq_cache *c) {
 
 akvq_status cuda_status(cudaError_t e) { return e == cudaSuccess ? AKVQ_OK : AKVQ_ECUDA; }
 
+// Persistent-grid sizes (CTAs per SM) of the two decode kernels; tuning
+// overrides AKVQ_ROW_CTAS / AKVQ_PG_CTAS are read once (experiments only).
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+int pg_ctas_override() {
+  static const int v = env_int("AKVQ_PG_CTAS", 0);
+  return v;
+}
+
 DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
   const akvq_config &f = c->cfg;
   DecodePlan p;
@@ -80,44 +92,45 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
     p.n_side_splits = bound > 0 ? (bound + 511) / 512 : 0;
     if (p.n_side_splits > 8) p.n_side_splits = 8;
   }
-  // fast path: 16-bit / 4-bit rows through the persistent row kernel (which
-  // also appends the new token), then 2-bit pages through the persistent dp4a
-  // page kernel (programmatic dependent launch); the last warp of each unit
-  // merges its segments and writes the output row.
+  // fast path: ONE persistent launch of k_decode_layer over every tier (pages,
+  // ring, side rows interleaved per unit), the new token appended in-kernel;
+  // the writer of each unit's last segment merges it and writes the output.
   p.fast = 0;
-  memset(&p.pp, 0, sizeof(p.pp));
-  memset(&p.rp, 0, sizeof(p.rp));
-  p.pp.n_pages = p.n_pages > 0 ? p.n_pages : 1;
-  p.rp.items_per_unit = 1;
+  memset(&p.lp, 0, sizeof(p.lp));
+  p.lp.per_u = 1;
   if (!(c->options & AKVQ_OPT_GENERIC_PAGES) &&
-      pages_fast_supported(f.head_dim, f.group, f.q_per_kv)) {
+      layer_supported(f.head_dim, f.group, f.q_per_kv)) {
     p.fast = 1;
-    if (p.n_pages > 0) {
-      p.pp.T = (long long)f.n_units * p.n_pages;
-      const long long wmax = (long long)sms * 3 * pages_warps_per_cta();
-      p.pp.W = p.pp.T < wmax ? p.pp.T : wmax;
-      const long long per = (p.pp.T + p.pp.W - 1) / p.pp.W;
-      p.pp.maxseg = (int)((per + p.n_pages - 1) / p.n_pages + 1);
-    }
-    const int ch = rows_chunk();
-    p.rp.L = L;
-    p.rp.n_q = n_q;
-    p.rp.n_ring_chunks = (L - n_q + ch - 1) / ch;
-    if (f.kind == AKVQ_PSA) p.rp.n_side_splits = (f.top_k > 0 && n_q > 0) ? 1 : 0;
-    else p.rp.n_side_splits = n_q > 0 ? (n_q + 1023) / 1024 : 0;
-    if (p.rp.n_side_splits > 8) p.rp.n_side_splits = 8;
-    p.rp.items_per_unit = p.rp.n_ring_chunks + p.rp.n_side_splits;
-    if (p.rp.items_per_unit > 0) {
-      p.rp.T = (long long)f.n_units * p.rp.items_per_unit;
-      const long long wmax = (long long)sms * 3 * rows_warps_per_cta();
-      p.rp.W = p.rp.T < wmax ? p.rp.T : wmax;
-      const long long per = (p.rp.T + p.rp.W - 1) / p.rp.W;
-      p.rp.maxseg = (int)((per + p.rp.items_per_unit - 1) / p.rp.items_per_unit + 1);
+    LayerPlan &lp = p.lp;
+    const int rows = layer_rows_per_chunk();
+    lp.L = L;
+    lp.n_q = n_q;
+    lp.P = p.n_pages;
+    lp.Rc = (L - n_q + rows - 1) / rows;
+    if (f.kind == AKVQ_PSA) {
+      lp.Sc = (f.top_k > 0 && n_q > 0) ? (f.top_k + rows - 1) / rows : 0;   // <= rows each
     } else {
-      p.rp.items_per_unit = 1;
+      lp.Sc = n_q > 0 ? (n_q + 255) / 256 : 0;                              // text rows <= n_q
+      if (lp.Sc > 8) lp.Sc = 8;
     }
+    if (c->options & AKVQ_OPT_SKIP_ROWS) lp.Rc = lp.Sc = 0;       // profiling hooks
+    if (c->options & AKVQ_OPT_SKIP_PAGES) lp.P = 0;
+    lp.per_u = lp.P + lp.Rc + lp.Sc;
+    lp.nr_q = lp.P > 0 ? (lp.Rc + lp.Sc) / lp.P : 0;
+    lp.nr_r = lp.P > 0 ? (lp.Rc + lp.Sc) % lp.P : 0;
+    if (lp.per_u > 0) {
+      const long long T = (long long)f.n_units * lp.per_u;
+      const int ctas = pg_ctas_override() > 0 ? pg_ctas_override() : layer_ctas_per_sm(f.q_per_kv);
+      const long long wmax = (long long)sms * ctas * layer_warps_per_cta();
+      lp.T = (int)T;
+      lp.W = (int)(T < wmax ? T : wmax);
+      const long long per = (T + lp.W - 1) / lp.W;
+      lp.maxseg = (int)((per + lp.per_u - 1) / lp.per_u + 1);
+    } else {
+      lp.per_u = 1;
+    }
+    lp.stream_only = (c->options & AKVQ_OPT_STREAM_ONLY) ? 1 : 0;
     p.n_page_splits = p.n_ring_splits = p.n_side_splits = 0;
-    p.pp.stream_only = p.rp.stream_only = (c->options & AKVQ_OPT_STREAM_ONLY) ? 1 : 0;
   }
   p.S = p.n_page_splits + p.n_ring_splits + p.n_side_splits;
   return p;
@@ -125,31 +138,18 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
 
 size_t ws_bytes_for(const akvq_cache *c, const DecodePlan &p) {
   const size_t g = c->cfg.q_per_kv, d = c->cfg.head_dim;
-  if (p.fast)
-    return ((size_t)p.pp.W * p.pp.maxseg * g * (d + 4) +
-            (size_t)p.rp.W * p.rp.maxseg * g * (2 * d + 4)) * sizeof(float);
+  if (p.fast) return (size_t)p.lp.W * p.lp.maxseg * g * (2 * d + 4) * sizeof(float);
   return (size_t)c->cfg.n_units * p.S * g * (d + 2) * sizeof(float);
 }
 
-// Fast-path launch: rows kernel (+ append when k != NULL), then page kernel.
+// Fast-path launch: one k_decode_layer (+ append when k != NULL).
 akvq_status launch_fast(const akvq_cache *c, const DecodePlan &p, const void *q, const void *k,
                         const void *v, const uint8_t *types, float *out, void *ws,
                         uint32_t flags, cudaStream_t s) {
   const DevCache d = make_dev(c);
-  const size_t g = c->cfg.q_per_kv, dd = c->cfg.head_dim;
-  float *pg_part = static_cast<float *>(ws);
-  float *rw_part = pg_part + (size_t)p.pp.W * p.pp.maxseg * g * (dd + 4);
-  cudaError_t e = cudaSuccess;
-  int n = 0;
-  if (!(c->options & AKVQ_OPT_SKIP_ROWS) && p.rp.T > 0) ++n;
-  if (!(c->options & AKVQ_OPT_SKIP_PAGES) && p.pp.T > 0) ++n;
-  const_cast<akvq_cache *>(c)->launches += n;
-  if (!(c->options & AKVQ_OPT_SKIP_ROWS))
-    e = launch_decode_rows(d, c->cfg.dtype16, p.rp, p.pp, q, k, v, types, rw_part, pg_part, out,
-                           flags, s);
-  if (e == cudaSuccess && !(c->options & AKVQ_OPT_SKIP_PAGES))
-    e = launch_decode_pages(d, c->cfg.dtype16, p.pp, p.rp, q, pg_part, rw_part, out, flags, s);
-  return cuda_status(e);
+  if (p.lp.T > 0) const_cast<akvq_cache *>(c)->launches += 1;
+  return cuda_status(launch_decode_layer(d, c->cfg.dtype16, p.lp, q, k, v, types,
+                                         static_cast<float *>(ws), out, flags, s));
 }
 
 }  // namespace
@@ -349,7 +349,7 @@ akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const 
   const bool flush = L1 - f.residual - c->n_q >= f.group;
   const DecodePlan p = plan_decode(c, L1, flush ? c->n_q + f.group : c->n_q);
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
-  if (flush || !p.fast || p.rp.T <= 0) {   // flush step (every G tokens) or generic path
+  if (flush || !p.fast || p.lp.T <= 0) {   // flush step (every G tokens) or generic path
     akvq_status st = append_impl(c, k, v, types, stream);
     if (st != AKVQ_OK) return st;
     return decode_impl(c, q, out, ws, ws_bytes, flags, stream);

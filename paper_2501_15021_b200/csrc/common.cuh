@@ -39,6 +39,36 @@ __device__ __forceinline__ uint8_t *side_ptr(const DevCache &c, int u, int e) {
   return c.side + ((size_t)u * c.side_cap + e) * c.side_entry;
 }
 
+// ---- 2-bit code layout inside a page (include/akvq.h) ----
+// Both code regions are arrays of 32-bit words, each a 4 x 4 tile of (token,
+// channel) codes; TQ = G/4 token quads, CQ = d/4 channel quads.
+//  K word ((cq>>2)*TQ + tq)*4 + (cq&3): byte b = channel 4cq+b, bits 2s..2s+1 of
+//    that byte = token 4tq+s.  A mask w & (3<<2s per byte) yields the 4 channels'
+//    codes (x4^s) of ONE token: dp4a against 4 channels of q~ is a partial logit.
+//  V word ((tq>>2)*CQ + cq)*4 + (tq&3): byte b = token 4tq+b (that byte is the
+//    token's S:146 byte for channels 4cq..4cq+3), bits 2s = channel 4cq+s.  A
+//    mask yields 4 tokens' codes (x4^s) of ONE channel: dp4a against 4 tokens'
+//    softmax weights is a partial output.
+// Codes themselves are exactly the paper's (Eqs. 3-6); only their byte order is
+// chosen for the decode kernel.
+__host__ __device__ __forceinline__ int kword_idx(int cq, int tq, int TQ) {
+  return ((cq >> 2) * TQ + tq) * 4 + (cq & 3);
+}
+__host__ __device__ __forceinline__ int vword_idx(int cq, int tq, int CQ) {
+  return ((tq >> 2) * CQ + cq) * 4 + (tq & 3);
+}
+// code of token t (in page), channel ch
+__device__ __forceinline__ uint32_t kcode_at(const uint8_t *kc, int t, int ch, int G) {
+  return (kc[4 * kword_idx(ch >> 2, t >> 2, G >> 2) + (ch & 3)] >> (2 * (t & 3))) & 3u;
+}
+__device__ __forceinline__ uint32_t vcode_at(const uint8_t *vc, int t, int ch, int D) {
+  return (vc[4 * vword_idx(ch >> 2, t >> 2, D >> 2) + (t & 3)] >> (2 * (ch & 3))) & 3u;
+}
+// S:146 byte of token t for channels 4cq..4cq+3 (V region)
+__device__ __forceinline__ uint32_t vbyte_at(const uint8_t *vc, int t, int cq, int D) {
+  return vc[4 * vword_idx(cq, t >> 2, D >> 2) + (t & 3)];
+}
+
 // ---- 16-bit element types --------------------------------------------------
 template <int DT> struct H16;
 template <> struct H16<AKVQ_BF16> {

@@ -39,7 +39,6 @@ __global__ void __launch_bounds__(kThreads) k_decode_split(DevCache c, DecodePla
                                                            float *__restrict__ ws_l,
                                                            float *__restrict__ ws_o) {
   constexpr int CL = D / 32;          // channels per lane in the V phase
-  constexpr int KW = D / 64;          // 32-bit code words per lane in the K phase
   constexpr int NG = D / G;
   extern __shared__ float sm[];
   const int g = c.g;
@@ -131,22 +130,25 @@ __global__ void __launch_bounds__(kThreads) k_decode_split(DevCache c, DecodePla
         if (lane == 0) bias[h] = part;
       }
       __syncwarp();
-      const uint8_t *kc = P + c.pg_kcodes + (size_t)(t0 - pg * G) * (D / 4);
+      const uint8_t *kc = P + c.pg_kcodes;
+      const int tlb = t0 - pg * G;                         // first token in the page
 #pragma unroll
       for (int pass = 0; pass < 4; ++pass) {
         const int ti = pass * 8 + tq;
-        const uint32_t *wp = reinterpret_cast<const uint32_t *>(kc + (size_t)ti * (D / 4)) + cq * KW;
-        uint32_t wd[KW];
+        // the 4-token bytes of this token's channels (K tile layout, common.cuh)
+        uint8_t by[D / 4];
 #pragma unroll
-        for (int w = 0; w < KW; ++w) wd[w] = wp[w];
+        for (int k = 0; k < D / 4; ++k) {
+          const int ch = cq * (D / 4) + k;
+          by[k] = kc[4 * kword_idx(ch >> 2, (tlb + ti) >> 2, G / 4) + (ch & 3)];
+        }
+        const int sh = 2 * ((tlb + ti) & 3);
         for (int h = 0; h < g; ++h) {
           const float *qq = qs + h * D + cq * (D / 4);
           float dot = 0.f;
 #pragma unroll
-          for (int w = 0; w < KW; ++w)
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              dot = fmaf(qq[16 * w + i], (float)((wd[w] >> (2 * i)) & 3u), dot);
+          for (int k = 0; k < D / 4; ++k)
+            dot = fmaf(qq[k], (float)((by[k] >> sh) & 3u), dot);
           dot += __shfl_xor_sync(0xffffffffu, dot, 1);
           dot += __shfl_xor_sync(0xffffffffu, dot, 2);
           if (cq == 0) lg[h * 32 + ti] = dot - bias[h];
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(kThreads) k_decode_split(DevCache c, DecodePla
       const int gi = c0 / G;
       for (int i = 0; i < 32; ++i) {
         const int tl = tl0 + i;
-        const uint32_t byte = vc[(size_t)tl * (D / 4) + c0 / 4];
+        const uint32_t byte = vbyte_at(vc, tl, c0 / 4, D);
         const int sh = 2 * (c0 % 4);
         const float sv = vs[tl * NG + gi];
         const float zv = (float)vz[tl * NG + gi];
@@ -504,11 +506,11 @@ __global__ void k_view(DevCache c, int L, int n_q, float *__restrict__ Ko, float
   const int32_t *kz = reinterpret_cast<const int32_t *>(P + c.pg_kzero);
   const float *vs = reinterpret_cast<const float *>(P + c.pg_vscale);
   const int32_t *vz = reinterpret_cast<const int32_t *>(P + c.pg_vzero);
-  const uint8_t *kc = P + c.pg_kcodes + (size_t)tl * (D / 4);
-  const uint8_t *vc = P + c.pg_vcodes + (size_t)tl * (D / 4);
+  const uint8_t *kc = P + c.pg_kcodes;
+  const uint8_t *vc = P + c.pg_vcodes;
   for (int i = lane; i < D; i += 32) {
-    const int ck = (kc[i / 4] >> (2 * (i % 4))) & 3;
-    const int cv = (vc[i / 4] >> (2 * (i % 4))) & 3;
+    const int ck = (int)kcode_at(kc, tl, i, G);
+    const int cv = (int)vcode_at(vc, tl, i, D);
     ko[i] = ks[i] * (float)(ck - kz[i]);
     vo[i] = vs[tl * NG + i / G] * (float)(cv - vz[tl * NG + i / G]);
   }

@@ -1,7 +1,7 @@
-// decode_common.cuh -- pieces shared by the two persistent decode kernels
-// (k_decode_rows, k_decode_pages): TMA bulk / mbarrier / dp4a wrappers, the
-// partial-record layouts, the (warp, unit) segment mapping and the per-unit
-// merge (log-sum-exp over segments, output Walsh-Hadamard, Fig. 7 / R4).
+// decode_common.cuh -- pieces of the persistent decode kernel (k_decode_layer):
+// TMA bulk / mbarrier / dp4a / PDL wrappers, the partial-record layout, the
+// (warp, unit) segment mapping and the per-unit merge (log-sum-exp over
+// segments, output Walsh-Hadamard, Fig. 7 / R4).
 #pragma once
 #include <math.h>
 
@@ -60,18 +60,17 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Partial records (floats), 16-byte aligned per head:
-//   page segment: [o_rot D][m][l][pad 2]
-//   row segment:  [o_org D][o_rot D][m][l][pad 2]
+// Partial record of one (warp, unit) segment, per head (floats, 16-byte aligned):
+//   [o_org D][o_rot D][m][l][pad 2]
+// o_org: sum p v over 16-bit rows (original basis); o_rot: sum p v^ over 2-bit
+// pages and 4-bit rows (rotated, normalized basis); m, l: base-2 running max
+// and sum of the segment's online softmax.
 template <int D> struct Rec {
-  static constexpr int P = D + 4;
   static constexpr int R = 2 * D + 4;
 };
 
 // Warps of a persistent plan (T work items, W warps, per = items per unit)
 // whose ranges [w*T/W, (w+1)*T/W) intersect unit u's [u*per, (u+1)*per).
-// 32-bit arithmetic: the host guarantees T * W < 2^31 is not needed because
-// products are formed in 64 bits and divided by a 32-bit W (see seg_begin).
 __device__ __forceinline__ int seg_begin(int T, int W, int w) {
   return (int)(((unsigned long long)w * (unsigned)T) / (unsigned)W);   // 64/32 division
 }
@@ -89,45 +88,29 @@ __device__ __forceinline__ void seg_range(int T, int W, int per, int u, int &w_l
   while (w_hi + 1 < W && seg_begin(T, W, w_hi + 1) < i1) ++w_hi;
 }
 
-// Per-unit merge by one warp: log-sum-exp over all page and row segments of
-// unit u, then out = (o_rot . H + o_org) / l (or o_rot + o_org . H with
-// AKVQ_OUT_ROTATED).  Partials are read with ld.global.cg (written by other
-// SMs in this or the preceding grid).  Lane j < #segments fetches segment j's
-// (m, l) so the loads overlap.
+// Per-unit merge by one warp: log-sum-exp over all segments of unit u, then
+// out = (o_rot . H + o_org) / l (or o_rot + o_org . H with AKVQ_OUT_ROTATED),
+// H applied as an unnormalized FWHT times 1/sqrt d (Fig. 7, R4).  Partials are
+// read with ld.global.cg (written by other SMs of this grid).  Lane j < #segs
+// fetches segment j's (m, l) so the loads overlap.
 template <int D, int NH>
-__device__ void merge_unit(const DevCache &c, const PagePlan &pp, const RowPlan &rp,
-                           const float *pg_part, const float *rw_part, int u, float *out,
-                           uint32_t flags, int lane) {
+__device__ __noinline__ void merge_layer_unit(const DevCache &c, const LayerPlan &lp, const float *part, int u,
+                                 float *out, uint32_t flags, int lane) {
   constexpr int CPL = D / 32;
-  int pw0, pw1, rw0, rw1;
-  seg_range((int)pp.T, (int)pp.W, pp.n_pages, u, pw0, pw1);
-  seg_range((int)rp.T, (int)rp.W, rp.items_per_unit, u, rw0, rw1);
-  const int npg = pw1 - pw0 + 1, nrw = rw1 - rw0 + 1, nseg = npg + nrw;
+  int w0, w1;
+  seg_range(lp.T, lp.W, lp.per_u, u, w0, w1);
+  const int nseg = w1 - w0 + 1;
   const bool out_rot = flags & AKVQ_OUT_ROTATED;
-  // record of segment j (page segments first, then row segments)
-  auto seg_rec = [&](int j, int &moff) -> const float * {
-    if (j < npg) {
-      const int w = pw0 + j;
-      const int slot = w * pp.maxseg + (u - seg_begin((int)pp.T, (int)pp.W, w) / pp.n_pages);
-      moff = D;
-      return pg_part + (size_t)slot * NH * Rec<D>::P;
-    }
-    const int w = rw0 + j - npg;
-    const int slot = w * rp.maxseg + (u - seg_begin((int)rp.T, (int)rp.W, w) / rp.items_per_unit);
-    moff = 2 * D;
-    return rw_part + (size_t)slot * NH * Rec<D>::R;
+  auto seg_rec = [&](int j, int h) -> const float * {
+    const int w = w0 + j;
+    const int slot = w * lp.maxseg + (u - seg_begin(lp.T, lp.W, w) / lp.per_u);
+    return part + ((size_t)slot * NH + h) * Rec<D>::R;
   };
 #pragma unroll
   for (int h = 0; h < NH; ++h) {
-    // pass 1: running max over segments, lanes fetch 32 segments at a time
     float M = -INFINITY;
     for (int b0 = 0; b0 < nseg; b0 += 32) {
-      float ms = -INFINITY;
-      if (b0 + lane < nseg) {
-        int moff;
-        const float *r = seg_rec(b0 + lane, moff);
-        ms = __ldcg(r + (size_t)h * (moff == D ? Rec<D>::P : Rec<D>::R) + moff);
-      }
+      const float ms = b0 + lane < nseg ? __ldcg(seg_rec(b0 + lane, h) + 2 * D) : -INFINITY;
       M = fmaxf(M, warp_max(ms));
     }
     float rot[CPL], org[CPL], lsum = 0.f;
@@ -138,11 +121,9 @@ __device__ void merge_unit(const DevCache &c, const PagePlan &pp, const RowPlan 
         float f = 0.f, ls = 0.f;
         const float *rh = nullptr;
         if (b0 + lane < nseg) {
-          int moff;
-          const float *r = seg_rec(b0 + lane, moff);
-          rh = r + (size_t)h * (moff == D ? Rec<D>::P : Rec<D>::R);
-          const float ms = __ldcg(rh + moff);
-          ls = __ldcg(rh + moff + 1);
+          rh = seg_rec(b0 + lane, h);
+          const float ms = __ldcg(rh + 2 * D);
+          ls = __ldcg(rh + 2 * D + 1);
           f = ms == -INFINITY ? 0.f : exp2f(ms - M);
         }
         lsum += warp_sum(f * ls);
@@ -153,15 +134,10 @@ __device__ void merge_unit(const DevCache &c, const PagePlan &pp, const RowPlan 
               __shfl_sync(0xffffffffu, (unsigned long long)(uintptr_t)rh, j);
           if (fj == 0.f) continue;
           const float *r = reinterpret_cast<const float *>((uintptr_t)pj);
-          if (b0 + j < npg) {
 #pragma unroll
-            for (int k = 0; k < CPL; ++k) rot[k] = fmaf(fj, __ldcg(r + CPL * lane + k), rot[k]);
-          } else {
-#pragma unroll
-            for (int k = 0; k < CPL; ++k) {
-              org[k] = fmaf(fj, __ldcg(r + CPL * lane + k), org[k]);
-              rot[k] = fmaf(fj, __ldcg(r + D + CPL * lane + k), rot[k]);
-            }
+          for (int k = 0; k < CPL; ++k) {
+            org[k] = fmaf(fj, __ldcg(r + CPL * lane + k), org[k]);
+            rot[k] = fmaf(fj, __ldcg(r + D + CPL * lane + k), rot[k]);
           }
         }
       }

@@ -1,0 +1,760 @@
+// decode_layer.cu -- AKVQ-VL single-query decode attention over one layer's
+// packed cache on sm_100a, every tier in ONE persistent kernel:
+//   2-bit pages      (K per channel, V per token; rotated basis)
+//   16-bit ring rows (recent window) and PSA pivot rows,
+//                    both in the ORIGINAL basis (R10)
+//   4-bit TSA rows   (text tokens, R11; rotated basis)
+// plus, for akvq_decode_step, the append of the new token (Eq. 2).
+//
+// Work list.  Per unit u the items are its P pages, Rc ring chunks (kRows rows)
+// and Sc side splits, INTERLEAVED (the rows placed before page p are the first
+// floor(p*NR/P) row items, NR = Rc + Sc), so every contiguous range of the
+// flattened (unit-major) list has the same mix of ALU-heavy page work and
+// memory-heavy row work.  Warp w of the persistent grid owns items
+// [w*T/W, (w+1)*T/W) and streams their bytes through its own kStages shared-
+// memory stages with 1-D TMA bulk copies (cp.async.bulk + mbarrier): a page is
+// two sub-loads (K half: K meta + K codes; V half: V meta + V codes), a row
+// item one or more sub-loads of up to one stage.
+//
+// Arithmetic (profiles/r01_microbench_pipes.md):
+//  pages, logits: lane = token quad; q~ * s^K rounded once per page to a 16-bit
+//    fixed point Q_c (two int8 limbs); one LOP3 mask per token of every K tile
+//    word (4 channels x 4 tokens) feeds dp4a against 4 channels' limbs:
+//    sum_c Q_c code_tc exact in int32; logit = delta (sum - sum_c Q_c z_c).
+//  pages, values: lane = channel quad; w_t = p_t s^V_t rounded to a 16-bit fixed
+//    point of the page's largest weight (two uint8 limbs); one mask per channel
+//    of every V tile word (4 tokens x 4 channels) feeds dp4a against 4 tokens'
+//    limbs: o'_c += dw (sum_t W_t code_tc - sum_t W_t z_t).
+//  rows: lane = channel quad (8-byte slices, conflict-free LDS.64); per-row dot
+//    products are reduced across lanes with a reduce-scatter.
+// One online softmax (base 2) per (warp, unit) segment with two accumulators:
+// o_rot (rotated basis: pages, 4-bit rows) and o_org (original basis: 16-bit
+// rows).  Each segment writes one partial; the writer of a unit's last segment
+// (per-unit ticket) merges them: log-sum-exp, out = (o_rot . H + o_org) / l.
+#include <math.h>
+
+#include <type_traits>
+
+#include "decode_common.cuh"
+
+namespace akvq {
+
+constexpr int kLyWarps = 4;        // warps per CTA
+constexpr int kLyStages = 2;       // TMA stages per warp
+constexpr int kRows = 8;           // 16-bit rows per ring chunk / side sub-load
+constexpr int kRows4 = 32;         // 4-bit TSA rows per side sub-load
+constexpr int kQMax = 32767;       // K-side fixed point: |Q| <= 2^15 - 1 (2 limbs)
+constexpr int kWMax = 65535;       // V-side fixed point: W <= 2^16 - 1 (2 limbs)
+__host__ __device__ constexpr int ly_ctas_per_sm(int nh) { return nh >= 4 ? 2 : (nh >= 2 ? 3 : 4); }
+
+// Per-warp shared memory (bytes):
+//   stages [kLyStages][SB] | qh [NH][D] f32 (q~ = q.H_s) | klimb [NH][D/16][8] u32 |
+//   vlimb [NH][NG][G/16][8] u32 | lgs [NH][kRows] f32 | barriers
+template <int D, int G, int NH>
+struct LySmem {
+  static constexpr int NG = D / G;
+  static __host__ __device__ size_t qh_off(size_t sb) { return kLyStages * sb; }
+  static __host__ __device__ size_t kl_off(size_t sb) { return qh_off(sb) + NH * D * 4; }
+  static __host__ __device__ size_t vl_off(size_t sb) { return kl_off(sb) + NH * (D / 16) * 32; }
+  static __host__ __device__ size_t lg_off(size_t sb) { return vl_off(sb) + NH * NG * (G / 16) * 32; }
+  static __host__ __device__ size_t ds_off(size_t sb) { return lg_off(sb) + NH * kRows * 4; }
+  static __host__ __device__ size_t bar_off(size_t sb) { return ds_off(sb) + kLyStages * 32; }
+  static __host__ __device__ size_t warp_bytes(size_t sb) {
+    return (bar_off(sb) + kLyStages * 8 + 127) / 128 * 128;
+  }
+};
+
+// stage bytes: max(page K half, page V half, kRows 16-bit rows, kRows4 side4 rows)
+__host__ __device__ inline size_t ly_stage_bytes(const DevCache &c) {
+  size_t a = c.pg_vscale, b = c.page_bytes - c.pg_vscale;
+  size_t m = a > b ? a : b;
+  const size_t r16 = (size_t)kRows * 4 * c.d;
+  if (r16 > m) m = r16;
+  if (c.kind == AKVQ_TSA) {
+    const size_t r4 = (size_t)kRows4 * c.side_entry;
+    if (r4 > m) m = r4;
+  }
+  return (m + 127) / 128 * 128;
+}
+
+__device__ __forceinline__ uint32_t fmask(uint32_t w, int s) { return w & (0x03030303u << (2 * s)); }
+
+template <int DT>
+__device__ __forceinline__ void cvt2(uint32_t w, float &a, float &b) {
+  if constexpr (DT == AKVQ_BF16) {
+    a = __uint_as_float(w << 16);
+    b = __uint_as_float(w & 0xffff0000u);
+  } else {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w));
+    a = f.x;
+    b = f.y;
+  }
+}
+
+// Sum v[NV] over the CQ lanes of a row group (lane bits below CQ): a reduce-
+// scatter halves the values per step, then a butterfly finishes.  On return
+// `mine` is the slot whose total this lane holds.
+template <int NV, int CQ>
+__device__ __forceinline__ float rs_reduce(float (&v)[NV], int cq, int &mine) {
+  constexpr int L2 = NV == 8 ? 3 : (NV == 4 ? 2 : (NV == 2 ? 1 : 0));
+  static_assert((1 << L2) == NV && (CQ >> L2) >= 1, "reduce shape");
+  mine = 0;
+#pragma unroll
+  for (int step = 0; step < L2; ++step) {
+    const int n = NV >> step, off = CQ >> (step + 1);
+    const bool up = cq & off;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = up ? v[i] : v[i + n / 2];
+      const float keep = up ? v[i + n / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+    if (up) mine += n / 2;
+  }
+  float t = v[0];
+#pragma unroll
+  for (int off = CQ >> (L2 + 1); off >= 1; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+  return t;
+}
+
+// Item decoding: unit-major list, per unit [pages interleaved with row items].
+struct LyItem {
+  int u;      // unit
+  int kind;   // 0 page, 1 ring chunk, 2 side split
+  int idx;    // page index, ring chunk index or side split index
+};
+
+// Cursor over a unit's interleaved items: state (p, r) = pages / row items done;
+// thr = floor(p * NR / P) = row items placed before page p, kept incrementally
+// (thr += NR / P with a Bresenham remainder) so stepping needs no division.
+struct LyCursor {
+  int u, p, r, thr, rem;
+  __device__ __forceinline__ bool next_is_page(const LayerPlan &lp) const {
+    return p < lp.P && r >= thr;
+  }
+  __device__ __forceinline__ LyItem item(const LayerPlan &lp) const {
+    LyItem x;
+    x.u = u;
+    if (next_is_page(lp)) { x.kind = 0; x.idx = p; }
+    else if (r < lp.Rc) { x.kind = 1; x.idx = r; }
+    else { x.kind = 2; x.idx = r - lp.Rc; }
+    return x;
+  }
+  __device__ __forceinline__ void step(const LayerPlan &lp) {
+    if (next_is_page(lp)) {
+      ++p;
+      thr += lp.nr_q;
+      rem += lp.nr_r;
+      if (rem >= lp.P) { rem -= lp.P; ++thr; }
+    } else {
+      ++r;
+    }
+    if (p == lp.P && r == lp.Rc + lp.Sc) { ++u; p = 0; r = 0; thr = 0; rem = 0; }
+  }
+  __device__ __forceinline__ void seek(const LayerPlan &lp, int k) {   // global item k
+    u = k / lp.per_u;
+    p = 0; r = 0; thr = 0; rem = 0;
+    for (int i = k - u * lp.per_u; i > 0; --i) step(lp);
+  }
+};
+
+// One sub-load of the pipeline: an item split into stage-sized pieces.  The
+// producer lane records it in the warp's descriptor ring (one per stage).
+struct LySub {
+  int u, kind;   // kind: 0 page K half, 1 page V half, 2 16-bit rows, 3 4-bit rows, -1 none
+  int a, n;      // page index | first row (ring offset from n_q / side entry) and row count
+  int ring;      // 1 if ring rows
+};
+
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// lane bits that encode slot m of rs_reduce<NV, CQ> (see there)
+template <int NV, int CQ>
+__device__ __forceinline__ constexpr int rs_enc(int m) {
+  constexpr int L2 = NV == 8 ? 3 : (NV == 4 ? 2 : (NV == 2 ? 1 : 0));
+  int e = 0;
+  for (int j = 0; j < L2; ++j)
+    if ((m >> (L2 - 1 - j)) & 1) e |= CQ >> (j + 1);
+  return e;
+}
+
+template <int D, int G, int DT, int NH>
+__global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
+    k_decode_layer(DevCache c, LayerPlan lp, const uint16_t *__restrict__ q,
+                   const uint16_t *__restrict__ app_k, const uint16_t *__restrict__ app_v,
+                   const uint8_t *__restrict__ app_types, float *__restrict__ part,
+                   float *__restrict__ out, uint32_t flags) {
+  using S = LySmem<D, G, NH>;
+  constexpr int NG = D / G;
+  constexpr int CQ = D / 4, TQ = G / 4;     // channel quads, token quads
+  constexpr int CG = D / 16, TG = G / 16;   // 4-quad groups (one LDS.128 of tile words)
+  constexpr int KCS = 32 / TQ;              // page K phase: lanes per token quad
+  constexpr int VTS = 32 / CQ;              // V phase / rows: lanes per channel quad
+  constexpr int NV = kRows / VTS;           // rows per lane per 8-row group
+  constexpr int BFLY = CQ / NV;             // lanes holding the same row total
+  static_assert(TQ <= 32 && CQ <= 32 && CG % KCS == 0 && TG % VTS == 0, "page shape");
+  static_assert(BFLY == 4, "row groups: lane bits >= 2 index the rows");
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t SB = ly_stage_bytes(c);
+  uint8_t *wsm = smem + (size_t)warp * S::warp_bytes(SB);
+  float *qh = reinterpret_cast<float *>(wsm + S::qh_off(SB));
+  uint32_t *klimb = reinterpret_cast<uint32_t *>(wsm + S::kl_off(SB));
+  uint32_t *vlimb = reinterpret_cast<uint32_t *>(wsm + S::vl_off(SB));
+  LySub *desc = reinterpret_cast<LySub *>(wsm + S::ds_off(SB));
+  uint64_t *bar = reinterpret_cast<uint64_t *>(wsm + S::bar_off(SB));
+
+  pdl_wait();                                   // q, k, v and the cache come from preceding work
+  pdl_launch_dependents();                      // the next layer's kernel may queue up
+  const int gw = blockIdx.x * kLyWarps + warp;
+  if (gw >= lp.W) return;
+  const int ib = seg_begin(lp.T, lp.W, gw), ie = seg_begin(lp.T, lp.W, gw + 1);
+  if (ib >= ie) return;
+  const bool tsa = c.kind == AKVQ_TSA;
+  const float alpha_k = kLog2e / (float)D;     // (q.H_s) . K^ / d in log2 units
+  const float alpha_o = kLog2e * c.inv_sqrt_d; // q.k / sqrt d in log2 units
+  const uint32_t kbytes = c.pg_vscale, vbytes = c.page_bytes - c.pg_vscale;
+
+  // ---- producer (lane 0): walks the items, issues TMA sub-loads, records them
+  if (lane == 0) {
+    for (int s = 0; s < kLyStages; ++s) mbar_init(&bar[s]);
+    mbar_fence_init();
+  }
+  LyCursor cur;
+  int left = ie - ib, part_i = 0;
+  if (lane == 0) cur.seek(lp, ib);
+  auto produce = [&](int st) {                  // lane 0 only
+    LySub sb;
+    sb.kind = -1;
+    const int n_ring = lp.L - lp.n_q;
+    while (left > 0) {
+      const LyItem x = cur.item(lp);
+      bool ok = false;
+      sb.u = x.u;
+      sb.ring = 0;
+      if (x.kind == 0) {
+        if (part_i < 2) { sb.kind = part_i; sb.a = x.idx; sb.n = G; ok = true; }
+      } else if (x.kind == 1) {
+        if (part_i < 1) {
+          sb.kind = 2; sb.ring = 1; sb.a = x.idx * kRows; sb.n = min(kRows, n_ring - sb.a);
+          ok = sb.n > 0;
+        }
+      } else {
+        const int cnt = __ldg(c.side_cnt + x.u);
+        const int lo = (int)((long long)x.idx * cnt / lp.Sc);
+        const int hi = (int)((long long)(x.idx + 1) * cnt / lp.Sc);
+        const int per = tsa ? kRows4 : kRows;
+        sb.kind = tsa ? 3 : 2;
+        sb.a = lo + part_i * per;
+        sb.n = min(per, hi - sb.a);
+        ok = sb.n > 0;
+      }
+      if (ok) { ++part_i; break; }
+      cur.step(lp);
+      --left;
+      part_i = 0;
+      sb.kind = -1;
+    }
+    desc[st] = sb;
+    if (sb.kind < 0) return;
+    uint8_t *dst = wsm + (size_t)st * SB;
+    if (sb.kind <= 1) {
+      const uint8_t *src = page_ptr(c, sb.u, sb.a) + (sb.kind ? kbytes : 0u);
+      const uint32_t nb = sb.kind ? vbytes : kbytes;
+      mbar_expect_tx(&bar[st], nb);
+      bulk_g2s(dst, src, nb, &bar[st]);
+    } else if (sb.ring) {
+      const int s0 = (lp.n_q + sb.a) % c.slots;
+      const int n1 = min(sb.n, c.slots - s0);
+      const uint32_t rowb = 4 * D;
+      mbar_expect_tx(&bar[st], (uint32_t)sb.n * rowb);
+      bulk_g2s(dst, ring_row(c, sb.u, s0), (uint32_t)n1 * rowb, &bar[st]);
+      if (n1 < sb.n)
+        bulk_g2s(dst + (size_t)n1 * rowb, ring_row(c, sb.u, 0), (uint32_t)(sb.n - n1) * rowb, &bar[st]);
+    } else {
+      const uint32_t eb = c.side_entry;
+      mbar_expect_tx(&bar[st], (uint32_t)sb.n * eb);
+      bulk_g2s(dst, side_ptr(c, sb.u, sb.a), (uint32_t)sb.n * eb, &bar[st]);
+    }
+  };
+  if (lane == 0)
+    for (int s = 0; s < kLyStages; ++s) produce(s);
+  __syncwarp();
+
+  // lane roles
+  const int ktq = lane % TQ, kcs = lane / TQ;         // page K phase
+  const int vcq = lane % CQ, vts = lane / CQ;         // page V phase and rows
+  const int vgam = (4 * vcq) / G;                     // channel group of the lane's quad
+
+  // per-unit segment state
+  float m_run[NH], l_run[NH], o_rot[NH][4], o_org[NH][4];
+  float qk[NH][4], qt[NH][4], qsum[NH];               // q (orig) * alpha_o; q~ * alpha_k; sum
+  float lg[NH][4];                                    // page logits of the lane's token quad
+  int cur_u = -1;
+  const int u_first = ib / lp.per_u;
+
+  auto flush = [&](int u) {
+    const size_t slot = (size_t)gw * lp.maxseg + (u - u_first);
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+#pragma unroll
+        for (int off = CQ; off < 32; off <<= 1) {
+          o_rot[h][s] += __shfl_xor_sync(0xffffffffu, o_rot[h][s], off);
+          o_org[h][s] += __shfl_xor_sync(0xffffffffu, o_org[h][s], off);
+        }
+      }
+      float *rec = part + (slot * NH + h) * Rec<D>::R;
+      if (vts == 0) {
+        reinterpret_cast<float4 *>(rec)[vcq] = make_float4(o_org[h][0], o_org[h][1], o_org[h][2], o_org[h][3]);
+        reinterpret_cast<float4 *>(rec + D)[vcq] = make_float4(o_rot[h][0], o_rot[h][1], o_rot[h][2], o_rot[h][3]);
+      }
+      if (lane == 0) { rec[2 * D] = m_run[h]; rec[2 * D + 1] = l_run[h]; }
+    }
+    int w_lo, w_hi;
+    seg_range(lp.T, lp.W, lp.per_u, u, w_lo, w_hi);
+    if (take_ticket(c, u, w_hi - w_lo + 1, lane)) {
+      merge_layer_unit<D, NH>(c, lp, part, u, out, flags, lane);
+      if (lane == 0) c.ticket[u] = 0u;
+    }
+  };
+
+  // One group of n <= kRows rows (16-bit original-basis rows, or 4-bit TSA rows)
+  // staged at shared address sb0 with the given pitch.  Lane (vcq, vts) handles
+  // channels 4vcq..4vcq+3 of rows vts + VTS*i.  FULL: n == kRows (no masking).
+  auto rows_group = [&](uint32_t sb0, uint32_t pitch, int n, bool r16, auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      float dot[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const uint32_t ra = sb0 + (uint32_t)(vts + VTS * i) * pitch;
+        if (r16) {
+          const uint2 v = lds64(ra + 8 * vcq);
+          float a0, a1, a2, a3;
+          cvt2<DT>(v.x, a0, a1);
+          cvt2<DT>(v.y, a2, a3);
+          dot[i] = fmaf(qk[h][0], a0, fmaf(qk[h][1], a1, fmaf(qk[h][2], a2, qk[h][3] * a3)));
+        } else {   // s_g (sum q~ code - z_g sum q~) over the lane's 4 channels
+          const float sk = lds_f32(ra + 4 * vgam);
+          const float zk = (float)lds_s32(ra + 4 * NG + 4 * vgam);
+          const uint32_t cw = lds16(ra + 16 * NG + 2 * vcq);
+          float a = qt[h][0] * (float)(cw & 15u);
+          a = fmaf(qt[h][1], (float)((cw >> 4) & 15u), a);
+          a = fmaf(qt[h][2], (float)((cw >> 8) & 15u), a);
+          a = fmaf(qt[h][3], (float)(cw >> 12), a);
+          dot[i] = sk * fmaf(-zk, qsum[h], a);
+        }
+      }
+      int mine;
+      float t = rs_reduce<NV, CQ>(dot, vcq, mine);
+      if (!FULL) t = (vts + VTS * mine) < n ? t : -INFINITY;
+      // softmax over the group: lane bits 2..4 index the rows (bits 0, 1 replicate)
+      float mx = t;
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      const float m_new = fmaxf(m_run[h], mx);
+      const float sc = exp2f(m_run[h] - m_new);
+      const float p = exp2f(t - m_new);
+      float ps = p;
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+      l_run[h] = fmaf(l_run[h], sc, ps);
+      m_run[h] = m_new;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { o_rot[h][k] *= sc; o_org[h][k] *= sc; }
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int row = vts + VTS * i;
+        const float pr = __shfl_sync(0xffffffffu, p, (lane & (BFLY - 1)) | rs_enc<NV, CQ>(i) | (vts * CQ));
+        if (!FULL && row >= n) continue;
+        const uint32_t ra = sb0 + (uint32_t)row * pitch;
+        if (r16) {
+          const uint2 v = lds64(ra + 2 * D + 8 * vcq);
+          float a0, a1, a2, a3;
+          cvt2<DT>(v.x, a0, a1);
+          cvt2<DT>(v.y, a2, a3);
+          o_org[h][0] = fmaf(pr, a0, o_org[h][0]);
+          o_org[h][1] = fmaf(pr, a1, o_org[h][1]);
+          o_org[h][2] = fmaf(pr, a2, o_org[h][2]);
+          o_org[h][3] = fmaf(pr, a3, o_org[h][3]);
+        } else {
+          const float sv = lds_f32(ra + 8 * NG + 4 * vgam);
+          const float zv = (float)lds_s32(ra + 12 * NG + 4 * vgam);
+          const uint32_t cw = lds16(ra + 16 * NG + D / 2 + 2 * vcq);
+          const float wt = pr * sv;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            o_rot[h][k] = fmaf(wt, (float)((cw >> (4 * k)) & 15u) - zv, o_rot[h][k]);
+        }
+      }
+    }
+  };
+
+  int st = 0;
+  uint32_t par = 0;
+  for (;;) {
+    const LySub s = desc[st];
+    if (s.kind < 0) break;
+    uint8_t *B = wsm + (size_t)st * SB;
+    if (lp.stream_only) {                           // profiling: pipeline only
+      mbar_wait(&bar[st], par);
+      __syncwarp();
+      if (lane == 0) produce(st);
+      __syncwarp();
+      if (++st == kLyStages) { st = 0; par ^= 1u; }
+      continue;
+    }
+    if (s.u != cur_u) {
+      if (cur_u >= 0) flush(cur_u);
+      cur_u = s.u;
+      // q~ = q . H_s (unnormalized FWHT: in-register then shuffle butterflies)
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        constexpr int CPL = D / 32;
+        float x[CPL];
+        const uint16_t *qs = q + ((size_t)s.u * c.g + h) * D + CPL * lane;
+        if constexpr (CPL == 4) {
+          const uint2 v = *reinterpret_cast<const uint2 *>(qs);
+          cvt2<DT>(v.x, x[0], x[1]);
+          cvt2<DT>(v.y, x[2], x[3]);
+        } else {
+          cvt2<DT>(*reinterpret_cast<const uint32_t *>(qs), x[0], x[1]);
+        }
+#pragma unroll
+        for (int hs = 1; hs < CPL; hs <<= 1)
+#pragma unroll
+          for (int k = 0; k < CPL; ++k)
+            if (!(k & hs)) { const float a = x[k], b = x[k + hs]; x[k] = a + b; x[k + hs] = a - b; }
+#pragma unroll
+        for (int lm = 1; lm < 32; lm <<= 1) {
+          const bool upper = lane & lm;
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            const float o2 = __shfl_xor_sync(0xffffffffu, x[k], lm);
+            x[k] = upper ? o2 - x[k] : x[k] + o2;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) qh[h * D + CPL * lane + k] = x[k];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        const uint2 v = *reinterpret_cast<const uint2 *>(q + ((size_t)s.u * c.g + h) * D + 4 * vcq);
+        cvt2<DT>(v.x, qk[h][0], qk[h][1]);
+        cvt2<DT>(v.y, qk[h][2], qk[h][3]);
+        const float4 t4 = reinterpret_cast<const float4 *>(qh + h * D)[vcq];
+        qt[h][0] = t4.x * alpha_k; qt[h][1] = t4.y * alpha_k;
+        qt[h][2] = t4.z * alpha_k; qt[h][3] = t4.w * alpha_k;
+        qsum[h] = (qt[h][0] + qt[h][1]) + (qt[h][2] + qt[h][3]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { qk[h][k] *= alpha_o; o_rot[h][k] = 0.f; o_org[h][k] = 0.f; }
+        m_run[h] = -INFINITY;
+        l_run[h] = 0.f;
+      }
+    }
+
+    if (s.kind == 0) {
+      // ================= page K half: logits of the page's G tokens
+      const uint32_t sbits =
+          (__ldg(c.bitmask + (size_t)s.u * c.bm_words + (size_t)s.a * (G / 32) + (ktq >> 3)) >>
+           (4 * (ktq & 7))) & 15u;
+      mbar_wait(&bar[st], par);
+      const float4 *ks4 = reinterpret_cast<const float4 *>(B + c.pg_kscale);
+      const int4 *kz4 = reinterpret_cast<const int4 *>(B + c.pg_kzero);
+      const uint4 *kc4 = reinterpret_cast<const uint4 *>(B + c.pg_kcodes);
+      float dA[NH], bA[NH];
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {      // limbs of Q_c = rn(q~_c s^K_c / delta): lane = channel quad
+        float qsb[4] = {0.f, 0.f, 0.f, 0.f}, am = 0.f;
+        int4 zq = make_int4(0, 0, 0, 0);
+        if (lane < CQ) {
+          const float4 qv = reinterpret_cast<const float4 *>(qh + h * D)[lane];
+          const float4 sv = ks4[lane];
+          zq = kz4[lane];
+          qsb[0] = qv.x * sv.x; qsb[1] = qv.y * sv.y; qsb[2] = qv.z * sv.z; qsb[3] = qv.w * sv.w;
+          am = fmaxf(fmaxf(fabsf(qsb[0]), fabsf(qsb[1])), fmaxf(fabsf(qsb[2]), fabsf(qsb[3])));
+        }
+        const float M = warp_max(am);
+        const float inv = M > 0.f ? (float)kQMax / M : 0.f;
+        const float delta = M > 0.f ? M / (float)kQMax : 0.f;
+        int Qv[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) Qv[b] = __float2int_rn(qsb[b] * inv);
+        // zero-point bias sum_c Q_c z_c (exact in fp32 while |sum| < 2^24)
+        float bq = (float)Qv[0] * (float)zq.x;
+        bq = fmaf((float)Qv[1], (float)zq.y, bq);
+        bq = fmaf((float)Qv[2], (float)zq.z, bq);
+        bq = fmaf((float)Qv[3], (float)zq.w, bq);
+        bq = warp_sum(bq);
+        dA[h] = alpha_k * delta;
+        bA[h] = alpha_k * delta * bq;
+        if (lane < CQ) {
+          const uint32_t lo = prmt(prmt(Qv[0], Qv[1], 0x0040), prmt(Qv[2], Qv[3], 0x0040), 0x5410);
+          const uint32_t hi = prmt(prmt(Qv[0], Qv[1], 0x0051), prmt(Qv[2], Qv[3], 0x0051), 0x5410);
+          uint32_t *kl = klimb + (h * CG + (lane >> 2)) * 8 + (lane & 3);
+          kl[0] = lo;
+          kl[4] = hi;
+        }
+      }
+      __syncwarp();
+      int acc[NH][4][2];
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { acc[h][k][0] = 0; acc[h][k][1] = 0; }
+#pragma unroll 2
+      for (int i = 0; i < CG / KCS; ++i) {
+        const int cg = kcs + KCS * i;
+        const uint4 w4 = kc4[cg * TQ + ktq];
+        const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const uint4 lo4 = reinterpret_cast<const uint4 *>(klimb + (h * CG + cg) * 8)[0];
+          const uint4 hi4 = reinterpret_cast<const uint4 *>(klimb + (h * CG + cg) * 8)[1];
+          const uint32_t lo[4] = {lo4.x, lo4.y, lo4.z, lo4.w};
+          const uint32_t hi[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t x = fmask(wd[j], k);
+              acc[h][k][0] = dp4a_uu(x, lo[j], acc[h][k][0]);
+              acc[h][k][1] = dp4a_us(x, hi[j], acc[h][k][1]);
+            }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          int tot = acc[h][k][1] * 256 + acc[h][k][0];      // sum_c Q_c code_tc * 4^k
+#pragma unroll
+          for (int off = TQ; off < 32; off <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+          const float sc4 = dA[h] * (1.0f / (float)(1 << (2 * k)));
+          lg[h][k] = ((sbits >> k) & 1u) ? -INFINITY : fmaf((float)tot, sc4, -bA[h]);
+        }
+    } else if (s.kind == 1) {
+      // ================= page V half: softmax update, value accumulation
+      mbar_wait(&bar[st], par);
+      const float *vs = reinterpret_cast<const float *>(B);
+      const int32_t *vz = reinterpret_cast<const int32_t *>(B + (c.pg_vzero - c.pg_vscale));
+      const uint4 *vc4 = reinterpret_cast<const uint4 *>(B + (c.pg_vcodes - c.pg_vscale));
+      float dwv[NH][NG], zwv[NH][NG];
+      bool live[NH];
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        const float mloc = warp_max(fmaxf(fmaxf(lg[h][0], lg[h][1]), fmaxf(lg[h][2], lg[h][3])));
+        const float m_new = fmaxf(m_run[h], mloc);
+        live[h] = m_new != -INFINITY;                 // warp-uniform
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) { dwv[h][gi] = 0.f; zwv[h][gi] = 0.f; }
+        if (!live[h]) continue;
+        const float sc = exp2f(m_run[h] - m_new);
+        m_run[h] = m_new;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { o_rot[h][k] *= sc; o_org[h][k] *= sc; }
+        float pr[4], psum = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { pr[k] = exp2f(lg[h][k] - m_new); psum += pr[k]; }
+        psum = warp_sum(kcs == 0 ? psum : 0.f);
+        l_run[h] = l_run[h] * sc + psum;
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) {
+          float wv[4], wmax = 0.f;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            wv[k] = pr[k] * vs[(4 * ktq + k) * NG + gi];
+            wmax = fmaxf(wmax, wv[k]);
+          }
+          wmax = warp_max(wmax);
+          // 16-bit fixed point of the page's largest weight; the zero-point
+          // term uses the same rounded weights (incoherent rounding error)
+          const float invw = wmax > 0.f ? (float)kWMax / wmax : 0.f;
+          uint32_t W[4];
+          float zs = 0.f;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            W[k] = min(__float2uint_rn(wv[k] * invw), (uint32_t)kWMax);
+            zs = fmaf((float)W[k], (float)vz[(4 * ktq + k) * NG + gi], zs);
+          }
+          zwv[h][gi] = warp_sum(kcs == 0 ? zs : 0.f);
+          dwv[h][gi] = wmax / (float)kWMax;
+          if (kcs == 0) {
+            const uint32_t lo = prmt(prmt(W[0], W[1], 0x0040), prmt(W[2], W[3], 0x0040), 0x5410);
+            const uint32_t hi = prmt(prmt(W[0], W[1], 0x0051), prmt(W[2], W[3], 0x0051), 0x5410);
+            uint32_t *vl = vlimb + ((h * NG + gi) * TG + (ktq >> 2)) * 8 + (ktq & 3);
+            vl[0] = lo;
+            vl[4] = hi;
+          }
+        }
+      }
+      __syncwarp();
+      int acc[NH][4][2];
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { acc[h][k][0] = 0; acc[h][k][1] = 0; }
+#pragma unroll 2
+      for (int i = 0; i < TG / VTS; ++i) {
+        const int tg = vts + VTS * i;
+        const uint4 w4 = vc4[tg * CQ + vcq];
+        const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const uint32_t *vl = vlimb + ((h * NG + vgam) * TG + tg) * 8;
+          const uint4 lo4 = reinterpret_cast<const uint4 *>(vl)[0];
+          const uint4 hi4 = reinterpret_cast<const uint4 *>(vl)[1];
+          const uint32_t lo[4] = {lo4.x, lo4.y, lo4.z, lo4.w};
+          const uint32_t hi[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t x = fmask(wd[j], k);
+              acc[h][k][0] = dp4a_uu(x, lo[j], acc[h][k][0]);
+              acc[h][k][1] = dp4a_uu(x, hi[j], acc[h][k][1]);
+            }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        if (!live[h]) continue;
+        float dw = dwv[h][0], zw = zwv[h][0];
+#pragma unroll
+        for (int gi = 1; gi < NG; ++gi) if (gi == vgam) { dw = dwv[h][gi]; zw = zwv[h][gi]; }
+        if (vts != 0) zw = 0.f;                        // the zero term once per channel
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          // < 2^31: 128 tokens x 4 x 192 x 255 per limb
+          const float val = (float)(acc[h][k][1] * 256 + acc[h][k][0]) * (1.0f / (float)(1 << (2 * k)));
+          o_rot[h][k] = fmaf(dw, val - zw, o_rot[h][k]);
+        }
+      }
+    } else {
+      // ================= rows: 16-bit (ring / PSA side, original basis) or
+      //                   4-bit (TSA side, rotated basis), in groups of kRows
+      mbar_wait(&bar[st], par);
+      const bool r16 = s.kind == 2;
+      if (s.ring && app_k != nullptr) {
+        // the newest token (Eq. 2): the stale ring slot was staged -- patch in
+        // the caller's row, append it to the ring and set its TSA text bit
+        const int tl = lp.L - 1 - (lp.n_q + s.a);
+        if (tl >= 0 && tl < s.n) {
+          const uint4 *sk = reinterpret_cast<const uint4 *>(app_k + (size_t)s.u * D);
+          const uint4 *sv = reinterpret_cast<const uint4 *>(app_v + (size_t)s.u * D);
+          uint8_t *Bw = B + (size_t)tl * 4 * D;
+          uint4 *rrow = reinterpret_cast<uint4 *>(ring_row(c, s.u, (lp.L - 1) % c.slots));
+          for (int i = lane; i < D / 8; i += 32) {
+            const uint4 kv = sk[i], vv = sv[i];
+            reinterpret_cast<uint4 *>(Bw)[i] = kv;
+            reinterpret_cast<uint4 *>(Bw + 2 * D)[i] = vv;
+            rrow[i] = kv;
+            rrow[D / 8 + i] = vv;
+          }
+          if (lane == 0 && tsa && app_types != nullptr && app_types[s.u] == 1)
+            atomicOr(&c.bitmask[(size_t)s.u * c.bm_words + (lp.L - 1) / 32], 1u << ((lp.L - 1) % 32));
+          __syncwarp();
+        }
+      }
+      const uint32_t pitch = r16 ? 4u * D : (uint32_t)c.side_entry;
+      const uint32_t sbase = smem_u32(B);
+      for (int g0 = 0; g0 < s.n; g0 += kRows) {
+        const int n = min(kRows, s.n - g0);
+        const uint32_t sb0 = sbase + (uint32_t)g0 * pitch;
+        if (n == kRows) rows_group(sb0, pitch, n, r16, std::integral_constant<bool, true>());
+        else rows_group(sb0, pitch, n, r16, std::integral_constant<bool, false>());
+      }
+    }
+    __syncwarp();
+    if (lane == 0) produce(st);                     // refill stage st, record its descriptor
+    __syncwarp();
+    if (++st == kLyStages) { st = 0; par ^= 1u; }
+  }
+  if (cur_u >= 0 && !lp.stream_only) flush(cur_u);
+}
+
+template <int D, int G, int NH>
+static size_t ly_smem(const DevCache &c) {
+  return (size_t)kLyWarps * LySmem<D, G, NH>::warp_bytes(ly_stage_bytes(c));
+}
+
+template <int D, int G, int DT, int NH>
+static cudaError_t launch_ly(const DevCache &c, const LayerPlan &lp, const void *q, const void *k,
+                             const void *v, const uint8_t *types, float *part, float *out,
+                             uint32_t flags, cudaStream_t st) {
+  const size_t smem = ly_smem<D, G, NH>(c);
+  auto kern = k_decode_layer<D, G, DT, NH>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((lp.W + kLyWarps - 1) / kLyWarps));
+  cfg.blockDim = dim3(kLyWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // overlap the previous tail
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, c, lp, (const uint16_t *)q, (const uint16_t *)k,
+                            (const uint16_t *)v, types, part, out, flags);
+}
+
+int layer_supported(int d, int G, int g) {
+  return (d == 128 || d == 64) && G >= 32 && G <= d && (g == 1 || g == 2 || g == 4);
+}
+int layer_warps_per_cta() { return kLyWarps; }
+int layer_ctas_per_sm(int g) { return ly_ctas_per_sm(g); }
+int layer_rows_per_chunk() { return kRows; }
+int layer_rows4_per_sub() { return kRows4; }
+
+template <int D, int G, int DT>
+static cudaError_t launch_ly_g(const DevCache &c, const LayerPlan &lp, const void *q, const void *k,
+                               const void *v, const uint8_t *types, float *part, float *out,
+                               uint32_t flags, cudaStream_t st) {
+  if (c.g == 1) return launch_ly<D, G, DT, 1>(c, lp, q, k, v, types, part, out, flags, st);
+  if (c.g == 2) return launch_ly<D, G, DT, 2>(c, lp, q, k, v, types, part, out, flags, st);
+  return launch_ly<D, G, DT, 4>(c, lp, q, k, v, types, part, out, flags, st);
+}
+
+cudaError_t launch_decode_layer(const DevCache &c, int dtype16, const LayerPlan &lp, const void *q,
+                                const void *k, const void *v, const uint8_t *types, float *part,
+                                float *out, uint32_t flags, cudaStream_t st) {
+  if (lp.T <= 0) return cudaSuccess;
+#define AKVQ_LCASE(D_, G_)                                                                       \
+  if (c.d == D_ && c.G == G_)                                                                    \
+    return dtype16 == AKVQ_BF16                                                                  \
+               ? launch_ly_g<D_, G_, AKVQ_BF16>(c, lp, q, k, v, types, part, out, flags, st)    \
+               : launch_ly_g<D_, G_, AKVQ_FP16>(c, lp, q, k, v, types, part, out, flags, st);
+  AKVQ_LCASE(64, 32)
+  AKVQ_LCASE(64, 64)
+  AKVQ_LCASE(128, 32)
+  AKVQ_LCASE(128, 64)
+  AKVQ_LCASE(128, 128)
+#undef AKVQ_LCASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace akvq

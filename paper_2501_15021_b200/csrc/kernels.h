@@ -15,26 +15,15 @@ struct QuantSrc {
   int ring_slots;       // 0: linear token index; >0: slot = token % ring_slots
 };
 
-// Persistent page-kernel plan: T = U * n_pages flattened (unit, page) items,
-// W warps each owning items [w*T/W, (w+1)*T/W); a warp writes one partial per
-// unit it touches into slot w*maxseg + (u - first unit of w).
-struct PagePlan {
-  long long T;
-  long long W;
-  int n_pages;
-  int maxseg;
-  int stream_only;      // AKVQ_OPT_STREAM_ONLY (profiling)
-};
-
-// Persistent row-kernel plan: per unit, n_ring_chunks items of 16 ring tokens
-// then n_side_splits items sharing the unit's side entries; same segment /
-// partial-slot scheme as PagePlan (partials hold o_org and o_rot).
-struct RowPlan {
-  long long T;
-  long long W;
-  int items_per_unit;
-  int n_ring_chunks;
-  int n_side_splits;
+// Persistent layer-kernel plan (k_decode_layer): per unit, P pages, Rc ring
+// chunks and Sc side splits, interleaved; T = U * per_u items; W warps, warp w
+// owns items [w*T/W, (w+1)*T/W) and writes one partial per unit it touches
+// into slot w*maxseg + (u - first unit of w).
+struct LayerPlan {
+  int T, W;
+  int per_u;
+  int P, Rc, Sc;
+  int nr_q, nr_r;       // (Rc + Sc) / P and (Rc + Sc) % P (item interleave, P > 0)
   int maxseg;
   int L, n_q;
   int stream_only;      // AKVQ_OPT_STREAM_ONLY (profiling)
@@ -48,9 +37,8 @@ struct DecodePlan {
   int ring_per_split, n_ring_splits;
   int n_side_splits;     // side entries are shared equally among these splits
   int S;                 // total splits of k_decode_split (ring / side / fallback pages)
-  int fast;              // 1: k_decode_rows then k_decode_pages (PDL), merged in-kernel
-  PagePlan pp;
-  RowPlan rp;
+  int fast;              // 1: one k_decode_layer launch (all tiers, merged in-kernel)
+  LayerPlan lp;
 };
 
 cudaError_t launch_salient(const DevCache &c, const uint8_t *types, const float *colsum,
@@ -63,17 +51,14 @@ cudaError_t launch_append(const DevCache &c, const void *k, const void *v,
                           const uint8_t *types, int L, cudaStream_t st);
 cudaError_t launch_decode(const DevCache &c, int dtype16, const DecodePlan &p, const void *q,
                           float *out, void *ws, uint32_t flags, cudaStream_t st);
-cudaError_t launch_decode_rows(const DevCache &c, int dtype16, const RowPlan &rp, const PagePlan &pp,
-                               const void *q, const void *k, const void *v, const uint8_t *types,
-                               float *rw_part, const float *pg_part, float *out, uint32_t flags,
-                               cudaStream_t st);
-cudaError_t launch_decode_pages(const DevCache &c, int dtype16, const PagePlan &pp,
-                                const RowPlan &rp, const void *q, float *pg_part,
-                                const float *rw_part, float *out, uint32_t flags, cudaStream_t st);
-int pages_fast_supported(int d, int G, int g);
-int pages_warps_per_cta();
-int rows_chunk();
-int rows_warps_per_cta();
+cudaError_t launch_decode_layer(const DevCache &c, int dtype16, const LayerPlan &lp, const void *q,
+                                const void *k, const void *v, const uint8_t *types, float *part,
+                                float *out, uint32_t flags, cudaStream_t st);
+int layer_supported(int d, int G, int g);
+int layer_warps_per_cta();
+int layer_ctas_per_sm(int g);
+int layer_rows_per_chunk();
+int layer_rows4_per_sub();
 cudaError_t launch_view(const DevCache &c, int dtype16, int L, int n_q, float *K, float *V,
                         cudaStream_t st);
 

@@ -136,24 +136,38 @@ __global__ void __launch_bounds__(G) k_quantize_blocks(DevCache c, QuantSrc src,
     reinterpret_cast<int32_t *>(pg + c.pg_kzero)[ch] = zero_i32(m.zf);
   }
   __syncthreads();
+  // codes staged as one byte each in smem (xs is dead now), then re-packed into
+  // the page's 4x4-tile K words (common.cuh kword_idx) with coalesced stores
+  uint8_t *cs8 = reinterpret_cast<uint8_t *>(xs);            // [G][D] K codes
+  uint8_t *vb8 = cs8 + G * D;                                 // [G][D/4] V bytes
   {
-    uint32_t wds[D / 16];
 #pragma unroll
-    for (int w = 0; w < D / 16; ++w) {
+    for (int w = 0; w < D / 4; ++w) {
       uint32_t word = 0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int ch = 16 * w + i;
+      for (int i = 0; i < 4; ++i) {
+        const int ch = 4 * w + i;
         QMeta m; m.s = s_s[ch]; m.zf = s_z[ch]; m.mode = s_mode[ch];
         const uint32_t code = sal ? 0u : q_code(x[ch], m, 3.f);
-        word |= code << (2 * i);
+        word |= code << (8 * i);
       }
-      wds[w] = word;
+      reinterpret_cast<uint32_t *>(cs8 + t * D)[w] = word;
     }
-    uint4 *dst = reinterpret_cast<uint4 *>(pg + c.pg_kcodes + (size_t)t * (D / 4));
+  }
+  __syncthreads();
+  {
+    constexpr int TQ = G / 4;
+    uint32_t *dst = reinterpret_cast<uint32_t *>(pg + c.pg_kcodes);
+    for (int wi = t; wi < (D / 4) * TQ; wi += G) {      // word wi -> (cq, tq)
+      const int cq = (wi & 3) + 4 * (wi / (4 * TQ)), tq = (wi / 4) % TQ;
+      uint32_t word = 0;
 #pragma unroll
-    for (int w = 0; w < D / 64; ++w)
-      dst[w] = make_uint4(wds[4 * w], wds[4 * w + 1], wds[4 * w + 2], wds[4 * w + 3]);
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2)
+          word |= (uint32_t)cs8[(4 * tq + s2) * D + 4 * cq + b] << (8 * b + 2 * s2);
+      dst[wi] = word;
+    }
   }
   // side slot of this token (ascending token order within the side table)
   const uint32_t below = (t & 31) ? (s_bits[t >> 5] & ((1u << (t & 31)) - 1u)) : 0u;
@@ -203,10 +217,21 @@ __global__ void __launch_bounds__(G) k_quantize_blocks(DevCache c, QuantSrc src,
         wds[ch / 16] |= (sal ? 0u : q_code(x[ch], m, 3.f)) << (2 * (ch % 16));
       }
     }
-    uint4 *dst = reinterpret_cast<uint4 *>(pg + c.pg_vcodes + (size_t)t * (D / 4));
+    // the token's S:146 bytes -> smem, re-packed below into 4x4-tile V words
 #pragma unroll
-    for (int w = 0; w < D / 64; ++w)
-      dst[w] = make_uint4(wds[4 * w], wds[4 * w + 1], wds[4 * w + 2], wds[4 * w + 3]);
+    for (int w = 0; w < D / 16; ++w) reinterpret_cast<uint32_t *>(vb8 + t * (D / 4))[w] = wds[w];
+  }
+  __syncthreads();
+  {
+    constexpr int CQ = D / 4;
+    uint32_t *dst = reinterpret_cast<uint32_t *>(pg + c.pg_vcodes);
+    for (int wi = t; wi < CQ * (G / 4); wi += G) {      // word wi -> (cq, tq)
+      const int tq = (wi & 3) + 4 * (wi / (4 * CQ)), cq = (wi / 4) % CQ;
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) word |= (uint32_t)vb8[(4 * tq + b) * (D / 4) + cq] << (8 * b);
+      dst[wi] = word;
+    }
   }
   if (sal) {
     c.side_idx[(size_t)u * c.side_cap + pos] = tok;

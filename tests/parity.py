@@ -24,6 +24,27 @@ def unpack4(b: np.ndarray) -> np.ndarray:
     return np.stack([b & 15, b >> 4], axis=-1).reshape(*b.shape[:-1], -1)
 
 
+def k_tiles_to_rows(raw: np.ndarray, U, npg, G, d) -> np.ndarray:
+    """K code region of each page (4x4-tile words, include/akvq.h) -> S:146 row
+    bytes [U, npg*G, d/4].  Word (cq, tq) at ((cq>>2)*TQ + tq)*4 + (cq&3); its
+    byte b = channel 4cq+b, bits 2s = token 4tq+s."""
+    TQ, CG = G // 4, d // 16
+    B = raw.reshape(U, npg, CG, TQ, 4, 4)                       # [.., cg, tq, j, b]
+    codes = (B[..., None] >> (2 * np.arange(4, dtype=np.uint8))) & 3   # [.., cg, tq, j, b, s]
+    codes = codes.transpose(0, 1, 3, 6, 2, 4, 5).reshape(U, npg * G, d)  # token 4tq+s, ch 16cg+4j+b
+    c4 = codes.reshape(U, npg * G, d // 4, 4).astype(np.uint8)
+    return (c4[..., 0] | (c4[..., 1] << 2) | (c4[..., 2] << 4) | (c4[..., 3] << 6)).astype(np.uint8)
+
+
+def v_tiles_to_rows(raw: np.ndarray, U, npg, G, d) -> np.ndarray:
+    """V code region (4x4-tile words) -> S:146 row bytes [U, npg*G, d/4].  Word
+    (cq, tq) at ((tq>>2)*CQ + cq)*4 + (tq&3); its byte b is token 4tq+b's byte
+    for channels 4cq..4cq+3."""
+    TG, CQ = G // 16, d // 4
+    B = raw.reshape(U, npg, TG, CQ, 4, 4)                       # [.., tg, cq, j, b]
+    return np.ascontiguousarray(B.transpose(0, 1, 2, 4, 5, 3)).reshape(U, npg * G, CQ)
+
+
 class GpuState:
     """numpy views of every region of one LayerCache buffer."""
 
@@ -41,10 +62,10 @@ class GpuState:
 
         self.kscale = pg(y.pg_kscale, 4 * d, np.float32).reshape(U, npg, d)
         self.kzero = pg(y.pg_kzero, 4 * d, np.int32).reshape(U, npg, d)
-        self.kcodes = pg(y.pg_kcodes, G * d // 4, np.uint8).reshape(U, npg * G, d // 4)
+        self.kcodes = k_tiles_to_rows(pg(y.pg_kcodes, G * d // 4, np.uint8), U, npg, G, d)
         self.vscale = pg(y.pg_vscale, 4 * G * ng, np.float32).reshape(U, npg * G, ng)
         self.vzero = pg(y.pg_vzero, 4 * G * ng, np.int32).reshape(U, npg * G, ng)
-        self.vcodes = pg(y.pg_vcodes, G * d // 4, np.uint8).reshape(U, npg * G, d // 4)
+        self.vcodes = v_tiles_to_rows(pg(y.pg_vcodes, G * d // 4, np.uint8), U, npg, G, d)
         ring = raw[y.ring_off: y.ring_off + U * y.ring_unit_bytes]
         self.ring = np.ascontiguousarray(ring).view(np.uint16).reshape(U, y.slots, 2, d)
         bm = np.ascontiguousarray(raw[y.bitmask_off: y.bitmask_off + U * y.bitmask_words * 4])

@@ -13,7 +13,7 @@ for w in $WHAT; do
     bench)  timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; cat $OUT/bench.json ;;
     launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
                -k regex:"k_(decode|append|quantize|salient|ring|view|combine)" --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1; echo "launches rc=$?" ;;
-    full)   for k in k_decode_pages k_decode_rows; do
+    full)   for k in ${KERNELS:-k_decode_layer}; do
               timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 200 -c 1 \
                 -o $OUT/full_$k python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$k.log 2>&1; echo "full $k rc=$?"
             done ;;
