@@ -197,7 +197,7 @@ __device__ __forceinline__ constexpr int rs_enc(int m) {
   return e;
 }
 
-template <int D, int G, int DT, int NH>
+template <int D, int G, int DT, int NH, bool TSA>
 __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     k_decode_layer(DevCache c, LayerPlan lp, const uint16_t *__restrict__ q,
                    const uint16_t *__restrict__ app_k, const uint16_t *__restrict__ app_v,
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   if (gw >= lp.W) return;
   const int ib = seg_begin(lp.T, lp.W, gw), ie = seg_begin(lp.T, lp.W, gw + 1);
   if (ib >= ie) return;
-  const bool tsa = c.kind == AKVQ_TSA;
+  constexpr bool tsa = TSA;                     // layer kind (Table I): TSA has 4-bit text rows
   const float alpha_k = kLog2e / (float)D;     // (q.H_s) . K^ / d in log2 units
   const float alpha_o = kLog2e * c.inv_sqrt_d; // q.k / sqrt d in log2 units
   const uint32_t kbytes = c.pg_vscale, vbytes = c.page_bytes - c.pg_vscale;
@@ -341,9 +341,10 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
 
   // One group of n <= kRows rows (16-bit original-basis rows, or 4-bit TSA rows)
   // staged at shared address sb0 with the given pitch.  Lane (vcq, vts) handles
-  // channels 4vcq..4vcq+3 of rows vts + VTS*i.  FULL: n == kRows (no masking).
-  auto rows_group = [&](uint32_t sb0, uint32_t pitch, int n, bool r16, auto full_tag) {
-    constexpr bool FULL = decltype(full_tag)::value;
+  // channels 4vcq..4vcq+3 of rows vts + VTS*i.  Rows n..kRows-1 of a partial
+  // group were zero-filled by the caller (finite), their logits are masked.
+  auto rows_group = [&](uint32_t sb0, uint32_t pitch, int n, auto r16_tag) {
+    constexpr bool r16 = decltype(r16_tag)::value;
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
       float dot[NV];
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       }
       int mine;
       float t = rs_reduce<NV, CQ>(dot, vcq, mine);
-      if (!FULL) t = (vts + VTS * mine) < n ? t : -INFINITY;
+      t = (vts + VTS * mine) < n ? t : -INFINITY;
       // softmax over the group: lane bits 2..4 index the rows (bits 0, 1 replicate)
       float mx = t;
 #pragma unroll
@@ -382,24 +383,31 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       for (int off = 4; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
       l_run[h] = fmaf(l_run[h], sc, ps);
       m_run[h] = m_new;
+      if (r16) {
+        float2 oa = __fmul2_rn(make_float2(o_org[h][0], o_org[h][1]), make_float2(sc, sc));
+        float2 ob = __fmul2_rn(make_float2(o_org[h][2], o_org[h][3]), make_float2(sc, sc));
 #pragma unroll
-      for (int k = 0; k < 4; ++k) { o_rot[h][k] *= sc; o_org[h][k] *= sc; }
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const int row = vts + VTS * i;
-        const float pr = __shfl_sync(0xffffffffu, p, (lane & (BFLY - 1)) | rs_enc<NV, CQ>(i) | (vts * CQ));
-        if (!FULL && row >= n) continue;
-        const uint32_t ra = sb0 + (uint32_t)row * pitch;
-        if (r16) {
-          const uint2 v = lds64(ra + 2 * D + 8 * vcq);
+        for (int i = 0; i < NV; ++i) {
+          const int row = vts + VTS * i;
+          const float pr = __shfl_sync(0xffffffffu, p, (lane & (BFLY - 1)) | rs_enc<NV, CQ>(i) | (vts * CQ));
+          const uint2 v = lds64(sb0 + (uint32_t)row * pitch + 2 * D + 8 * vcq);
           float a0, a1, a2, a3;
           cvt2<DT>(v.x, a0, a1);
           cvt2<DT>(v.y, a2, a3);
-          o_org[h][0] = fmaf(pr, a0, o_org[h][0]);
-          o_org[h][1] = fmaf(pr, a1, o_org[h][1]);
-          o_org[h][2] = fmaf(pr, a2, o_org[h][2]);
-          o_org[h][3] = fmaf(pr, a3, o_org[h][3]);
-        } else {
+          oa = __ffma2_rn(make_float2(pr, pr), make_float2(a0, a1), oa);
+          ob = __ffma2_rn(make_float2(pr, pr), make_float2(a2, a3), ob);
+        }
+        o_org[h][0] = oa.x; o_org[h][1] = oa.y; o_org[h][2] = ob.x; o_org[h][3] = ob.y;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o_rot[h][k] *= sc;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { o_rot[h][k] *= sc; o_org[h][k] *= sc; }
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const int row = vts + VTS * i;
+          const float pr = __shfl_sync(0xffffffffu, p, (lane & (BFLY - 1)) | rs_enc<NV, CQ>(i) | (vts * CQ));
+          const uint32_t ra = sb0 + (uint32_t)row * pitch;
           const float sv = lds_f32(ra + 8 * NG + 4 * vgam);
           const float zv = (float)lds_s32(ra + 12 * NG + 4 * vgam);
           const uint32_t cw = lds16(ra + 16 * NG + D / 2 + 2 * vcq);
@@ -684,8 +692,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       for (int g0 = 0; g0 < s.n; g0 += kRows) {
         const int n = min(kRows, s.n - g0);
         const uint32_t sb0 = sbase + (uint32_t)g0 * pitch;
-        if (n == kRows) rows_group(sb0, pitch, n, r16, std::integral_constant<bool, true>());
-        else rows_group(sb0, pitch, n, r16, std::integral_constant<bool, false>());
+        if (n < kRows) {   // zero-fill the group's missing rows (finite, masked below)
+          uint4 *z = reinterpret_cast<uint4 *>(B + (size_t)(g0 + n) * pitch);
+          for (int i = lane; i < (int)((kRows - n) * pitch / 16); i += 32) z[i] = make_uint4(0, 0, 0, 0);
+          __syncwarp();
+        }
+        if (!tsa || r16) rows_group(sb0, pitch, n, std::integral_constant<bool, true>());
+        else if constexpr (tsa) rows_group(sb0, pitch, n, std::integral_constant<bool, false>());
       }
     }
     __syncwarp();
@@ -706,7 +719,7 @@ static cudaError_t launch_ly(const DevCache &c, const LayerPlan &lp, const void 
                              const void *v, const uint8_t *types, float *part, float *out,
                              uint32_t flags, cudaStream_t st) {
   const size_t smem = ly_smem<D, G, NH>(c);
-  auto kern = k_decode_layer<D, G, DT, NH>;
+  auto kern = c.kind == AKVQ_TSA ? k_decode_layer<D, G, DT, NH, true> : k_decode_layer<D, G, DT, NH, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((lp.W + kLyWarps - 1) / kLyWarps));
