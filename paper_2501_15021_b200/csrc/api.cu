@@ -123,7 +123,9 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
       const int ctas = pg_ctas_override() > 0 ? pg_ctas_override() : layer_ctas_per_sm(f.q_per_kv);
       const long long wmax = (long long)sms * ctas * layer_warps_per_cta();
       lp.T = (int)T;
-      lp.W = (int)(T < wmax ? T : wmax);
+      long long W = T < wmax ? T : wmax;
+      if (T * W >= (1LL << 31)) W = ((1LL << 31) - 1) / T;   // 32-bit segment arithmetic
+      lp.W = (int)(W < 1 ? 1 : W);
       const long long per = (T + lp.W - 1) / lp.W;
       lp.maxseg = (int)((per + lp.per_u - 1) / lp.per_u + 1);
     } else {

@@ -71,8 +71,9 @@ template <int D> struct Rec {
 
 // Warps of a persistent plan (T work items, W warps, per = items per unit)
 // whose ranges [w*T/W, (w+1)*T/W) intersect unit u's [u*per, (u+1)*per).
+// 32-bit arithmetic: the host guarantees T * W < 2^31 (api.cu plan_decode).
 __device__ __forceinline__ int seg_begin(int T, int W, int w) {
-  return (int)(((unsigned long long)w * (unsigned)T) / (unsigned)W);   // 64/32 division
+  return (int)(((unsigned)w * (unsigned)T) / (unsigned)W);
 }
 __device__ __forceinline__ void seg_range(int T, int W, int per, int u, int &w_lo, int &w_hi) {
   w_lo = 0;
@@ -80,7 +81,7 @@ __device__ __forceinline__ void seg_range(int T, int W, int per, int u, int &w_l
   if (T <= 0 || W <= 0) return;
   const int i0 = u * per, i1 = i0 + per;
   // first warp whose range ends after i0: ceil((i0 + 1) * W / T) - 1
-  w_lo = (int)((((unsigned long long)(i0 + 1)) * (unsigned)W + (unsigned)T - 1) / (unsigned)T) - 1;
+  w_lo = (int)(((unsigned)(i0 + 1) * (unsigned)W + (unsigned)T - 1) / (unsigned)T) - 1;
   if (w_lo < 0) w_lo = 0;
   while (w_lo > 0 && seg_begin(T, W, w_lo) > i0) --w_lo;
   while (seg_begin(T, W, w_lo + 1) <= i0) ++w_lo;

@@ -260,8 +260,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         }
       } else {
         const int cnt = __ldg(c.side_cnt + x.u);
-        const int lo = (int)((long long)x.idx * cnt / lp.Sc);
-        const int hi = (int)((long long)(x.idx + 1) * cnt / lp.Sc);
+        const int lo = x.idx * cnt / lp.Sc;          // 32-bit: cnt <= capacity, Sc <= 8
+        const int hi = (x.idx + 1) * cnt / lp.Sc;
         const int per = tsa ? kRows4 : kRows;
         sb.kind = tsa ? 3 : 2;
         sb.a = lo + part_i * per;
