@@ -70,7 +70,8 @@ int pg_ctas_override() {
   return v;
 }
 
-DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
+// build_tab = false: sizes only (workspace queries), the item table is not filled
+DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = true) {
   const akvq_config &f = c->cfg;
   DecodePlan p;
   p.L = L;
@@ -96,7 +97,7 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
   // ring, side rows interleaved per unit), the new token appended in-kernel;
   // the writer of each unit's last segment merges it and writes the output.
   p.fast = 0;
-  memset(&p.lp, 0, sizeof(p.lp));
+  memset(&p.lp, 0, offsetof(LayerPlan, tab));
   p.lp.per_u = 1;
   if (!(c->options & AKVQ_OPT_GENERIC_PAGES) &&
       layer_supported(f.head_dim, f.group, f.q_per_kv)) {
@@ -116,9 +117,28 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
     if (c->options & AKVQ_OPT_SKIP_ROWS) lp.Rc = lp.Sc = 0;       // profiling hooks
     if (c->options & AKVQ_OPT_SKIP_PAGES) lp.P = 0;
     lp.per_u = lp.P + lp.Rc + lp.Sc;
-    lp.nr_q = lp.P > 0 ? (lp.Rc + lp.Sc) / lp.P : 0;
-    lp.nr_r = lp.P > 0 ? (lp.Rc + lp.Sc) % lp.P : 0;
-    if (lp.per_u > 0) {
+    lp.nq_mod = n_q % c->lay.slots;
+    if (lp.per_u > kLyMaxTab) {           // beyond the item table: generic kernels
+      p.fast = 0;
+      lp.per_u = 1;
+    } else if (build_tab) {               // interleave rows between pages (Bresenham)
+      const int NR = lp.Rc + lp.Sc, n_ring = L - n_q;
+      int k = 0, r = 0;
+      auto row_item = [&](int ri) -> uint32_t {
+        if (ri < lp.Rc) {
+          const int a = ri * rows, n = n_ring - a < rows ? n_ring - a : rows;
+          return 2u | ((uint32_t)n << 2) | ((uint32_t)a << 8);
+        }
+        return 3u | ((uint32_t)(ri - lp.Rc) << 8);
+      };
+      for (int pg = 0; pg < lp.P; ++pg) {
+        const int thr = (int)((long long)pg * NR / lp.P);
+        while (r < thr) lp.tab[k++] = row_item(r++);
+        lp.tab[k++] = 0u | ((uint32_t)pg << 8);
+      }
+      while (r < NR) lp.tab[k++] = row_item(r++);
+    }
+    if (p.fast && lp.per_u > 0) {
       const long long T = (long long)f.n_units * lp.per_u;
       const int ctas = pg_ctas_override() > 0 ? pg_ctas_override() : layer_ctas_per_sm(f.q_per_kv);
       const long long wmax = (long long)sms * ctas * layer_warps_per_cta();
@@ -132,7 +152,7 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q) {
       lp.per_u = 1;
     }
     lp.stream_only = (c->options & AKVQ_OPT_STREAM_ONLY) ? 1 : 0;
-    p.n_page_splits = p.n_ring_splits = p.n_side_splits = 0;
+    if (p.fast) p.n_page_splits = p.n_ring_splits = p.n_side_splits = 0;
   }
   p.S = p.n_page_splits + p.n_ring_splits + p.n_side_splits;
   return p;
@@ -304,7 +324,7 @@ akvq_status akvq_append_token(akvq_cache *c, const void *k, const void *v,
 
 size_t akvq_decode_workspace_bytes(const akvq_cache *c) {
   if (!c) return 0;
-  return ws_bytes_for(c, plan_decode(c, c->L, c->n_q));
+  return ws_bytes_for(c, plan_decode(c, c->L, c->n_q, false));
 }
 
 size_t akvq_decode_workspace_bytes_max(const akvq_cache *c) {
@@ -313,11 +333,11 @@ size_t akvq_decode_workspace_bytes_max(const akvq_cache *c) {
   const akvq_config &f = c->cfg;
   for (int L = 1; L <= f.capacity; ++L) {     // plans are cheap; the size is not monotone in L
     const int n_q = L > f.residual ? (L - f.residual) / f.group * f.group : 0;
-    const size_t b = ws_bytes_for(c, plan_decode(c, L, n_q));
+    const size_t b = ws_bytes_for(c, plan_decode(c, L, n_q, false));
     if (b > best) best = b;
   }
   const int n_q = f.capacity > f.residual ? (f.capacity - f.residual) / f.group * f.group : 0;
-  const size_t b = ws_bytes_for(c, plan_decode(c, f.capacity, n_q));
+  const size_t b = ws_bytes_for(c, plan_decode(c, f.capacity, n_q, false));
   return b > best ? b : best;
 }
 

@@ -6,15 +6,16 @@
 //   4-bit TSA rows   (text tokens, R11; rotated basis)
 // plus, for akvq_decode_step, the append of the new token (Eq. 2).
 //
-// Work list.  Per unit u the items are its P pages, Rc ring chunks (kRows rows)
-// and Sc side splits, INTERLEAVED (the rows placed before page p are the first
-// floor(p*NR/P) row items, NR = Rc + Sc), so every contiguous range of the
-// flattened (unit-major) list has the same mix of ALU-heavy page work and
-// memory-heavy row work.  Warp w of the persistent grid owns items
-// [w*T/W, (w+1)*T/W) and streams their bytes through its own kStages shared-
-// memory stages with 1-D TMA bulk copies (cp.async.bulk + mbarrier): a page is
-// two sub-loads (K half: K meta + K codes; V half: V meta + V codes), a row
-// item one or more sub-loads of up to one stage.
+// Work list.  Every unit has the same host-built table of items (kernel
+// parameter LayerPlan::tab): its P pages (two sub-loads each, K half: K meta +
+// K codes; V half: V meta + V codes, never split across warps), Rc ring chunks (kRows rows) and Sc side
+// splits, INTERLEAVED (the rows placed before page p are the first floor(p*NR/P)
+// row items, NR = Rc + Sc), so every contiguous range of the flattened
+// (unit-major) list has the same mix of ALU-heavy page work and memory-heavy
+// row work.  Warp w of the persistent grid owns items [w*T/W, (w+1)*T/W) and
+// streams their bytes through its own shared-memory stages with 1-D TMA bulk
+// copies (cp.async.bulk + mbarrier); a side split (runtime entry count) may
+// take several sub-loads.
 //
 // Arithmetic (profiles/r01_microbench_pipes.md):
 //  pages, logits: lane = token quad; q~ * s^K rounded once per page to a 16-bit
@@ -117,47 +118,6 @@ __device__ __forceinline__ float rs_reduce(float (&v)[NV], int cq, int &mine) {
   return t;
 }
 
-// Item decoding: unit-major list, per unit [pages interleaved with row items].
-struct LyItem {
-  int u;      // unit
-  int kind;   // 0 page, 1 ring chunk, 2 side split
-  int idx;    // page index, ring chunk index or side split index
-};
-
-// Cursor over a unit's interleaved items: state (p, r) = pages / row items done;
-// thr = floor(p * NR / P) = row items placed before page p, kept incrementally
-// (thr += NR / P with a Bresenham remainder) so stepping needs no division.
-struct LyCursor {
-  int u, p, r, thr, rem;
-  __device__ __forceinline__ bool next_is_page(const LayerPlan &lp) const {
-    return p < lp.P && r >= thr;
-  }
-  __device__ __forceinline__ LyItem item(const LayerPlan &lp) const {
-    LyItem x;
-    x.u = u;
-    if (next_is_page(lp)) { x.kind = 0; x.idx = p; }
-    else if (r < lp.Rc) { x.kind = 1; x.idx = r; }
-    else { x.kind = 2; x.idx = r - lp.Rc; }
-    return x;
-  }
-  __device__ __forceinline__ void step(const LayerPlan &lp) {
-    if (next_is_page(lp)) {
-      ++p;
-      thr += lp.nr_q;
-      rem += lp.nr_r;
-      if (rem >= lp.P) { rem -= lp.P; ++thr; }
-    } else {
-      ++r;
-    }
-    if (p == lp.P && r == lp.Rc + lp.Sc) { ++u; p = 0; r = 0; thr = 0; rem = 0; }
-  }
-  __device__ __forceinline__ void seek(const LayerPlan &lp, int k) {   // global item k
-    u = k / lp.per_u;
-    p = 0; r = 0; thr = 0; rem = 0;
-    for (int i = k - u * lp.per_u; i > 0; --i) step(lp);
-  }
-};
-
 // One sub-load of the pipeline: an item split into stage-sized pieces.  The
 // producer lane records it in the warp's descriptor ring (one per stage).
 struct LySub {
@@ -199,7 +159,7 @@ __device__ __forceinline__ constexpr int rs_enc(int m) {
 
 template <int D, int G, int DT, int NH, bool TSA>
 __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
-    k_decode_layer(DevCache c, LayerPlan lp, const uint16_t *__restrict__ q,
+    k_decode_layer(const __grid_constant__ DevCache c, const __grid_constant__ LayerPlan lp, const uint16_t *__restrict__ q,
                    const uint16_t *__restrict__ app_k, const uint16_t *__restrict__ app_v,
                    const uint8_t *__restrict__ app_types, float *__restrict__ part,
                    float *__restrict__ out, uint32_t flags) {
@@ -239,39 +199,40 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     for (int s = 0; s < kLyStages; ++s) mbar_init(&bar[s]);
     mbar_fence_init();
   }
-  LyCursor cur;
-  int left = ie - ib, part_i = 0;
-  if (lane == 0) cur.seek(lp, ib);
+  // producer state: unit, table entry, sub-load within a side split
+  int pu = ib / lp.per_u, pj = ib - (ib / lp.per_u) * lp.per_u, left = ie - ib, part_i = 0;
   auto produce = [&](int st) {                  // lane 0 only
     LySub sb;
     sb.kind = -1;
-    const int n_ring = lp.L - lp.n_q;
     while (left > 0) {
-      const LyItem x = cur.item(lp);
-      bool ok = false;
-      sb.u = x.u;
+      const uint32_t e = lp.tab[pj];
+      const int kind = (int)(e & 3u);
+      const int a = (int)(e >> 8), n = (int)((e >> 2) & 63u);
+      bool ok = true, next = true;
+      sb.u = pu;
       sb.ring = 0;
-      if (x.kind == 0) {
-        if (part_i < 2) { sb.kind = part_i; sb.a = x.idx; sb.n = G; ok = true; }
-      } else if (x.kind == 1) {
-        if (part_i < 1) {
-          sb.kind = 2; sb.ring = 1; sb.a = x.idx * kRows; sb.n = min(kRows, n_ring - sb.a);
-          ok = sb.n > 0;
-        }
-      } else {
-        const int cnt = __ldg(c.side_cnt + x.u);
-        const int lo = x.idx * cnt / lp.Sc;          // 32-bit: cnt <= capacity, Sc <= 8
-        const int hi = (x.idx + 1) * cnt / lp.Sc;
+      if (kind == 0) {                            // page: K half then V half
+        sb.kind = part_i; sb.a = a; sb.n = G;
+        next = part_i == 1;
+        part_i = next ? 0 : 1;
+      } else if (kind == 2) {                     // ring chunk (rows n of it)
+        sb.kind = 2; sb.ring = 1; sb.a = a; sb.n = n;
+      } else {                                    // side split a: entries [lo, hi), runtime count
+        const int cnt = __ldg(c.side_cnt + pu);
+        const int lo = a * cnt / lp.Sc, hi = (a + 1) * cnt / lp.Sc;   // 32-bit: cnt <= capacity
         const int per = tsa ? kRows4 : kRows;
         sb.kind = tsa ? 3 : 2;
         sb.a = lo + part_i * per;
         sb.n = min(per, hi - sb.a);
         ok = sb.n > 0;
+        next = !ok;
+        part_i = ok ? part_i + 1 : 0;
       }
-      if (ok) { ++part_i; break; }
-      cur.step(lp);
-      --left;
-      part_i = 0;
+      if (next) {
+        if (++pj == lp.per_u) { pj = 0; ++pu; }
+        --left;
+      }
+      if (ok) break;
       sb.kind = -1;
     }
     desc[st] = sb;
@@ -283,7 +244,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       mbar_expect_tx(&bar[st], nb);
       bulk_g2s(dst, src, nb, &bar[st]);
     } else if (sb.ring) {
-      const int s0 = (lp.n_q + sb.a) % c.slots;
+      int s0 = lp.nq_mod + sb.a;                  // ring slot of row n_q + a
+      if (s0 >= c.slots) s0 -= c.slots;
       const int n1 = min(sb.n, c.slots - s0);
       const uint32_t rowb = 4 * D;
       mbar_expect_tx(&bar[st], (uint32_t)sb.n * rowb);

@@ -15,18 +15,22 @@ struct QuantSrc {
   int ring_slots;       // 0: linear token index; >0: slot = token % ring_slots
 };
 
-// Persistent layer-kernel plan (k_decode_layer): per unit, P pages, Rc ring
-// chunks and Sc side splits, interleaved; T = U * per_u items; W warps, warp w
-// owns items [w*T/W, (w+1)*T/W) and writes one partial per unit it touches
-// into slot w*maxseg + (u - first unit of w).
+// Persistent layer-kernel plan (k_decode_layer): per unit, the item table tab
+// (P pages as K/V halves, Rc ring chunks and Sc side splits, interleaved);
+// T = U * per_u items; W warps, warp w owns items [w*T/W, (w+1)*T/W) and writes
+// one partial per unit it touches into slot w*maxseg + (u - first unit of w).
+// Item encoding: kind (bits 0-1: 0 page (K and V halves), 2 ring chunk,
+// 3 side split) | rows (bits 2-7, ring chunk) | index (bits 8-31: page, first
+// ring row relative to n_q, or side split).
+constexpr int kLyMaxTab = 2048;
 struct LayerPlan {
   int T, W;
   int per_u;
   int P, Rc, Sc;
-  int nr_q, nr_r;       // (Rc + Sc) / P and (Rc + Sc) % P (item interleave, P > 0)
   int maxseg;
-  int L, n_q;
+  int L, n_q, nq_mod;   // nq_mod = n_q % ring slots
   int stream_only;      // AKVQ_OPT_STREAM_ONLY (profiling)
+  uint32_t tab[kLyMaxTab];
 };
 
 // Decode split plan (host-computed, uniform across units).
