@@ -76,59 +76,185 @@ __global__ void __launch_bounds__(1024) k_salient_psa(DevCache c, const float *_
 }
 
 // ============================================================ K1: quantize
-// One CTA per (block j, unit u); thread t owns token j*G + t of the block.
-//   1. row -> fp32 -> in-register FWHT (x.H_s, R5) -> smem for the K stats
-//   2. thread ch: min/max of channel ch over the block's non-salient tokens,
-//      Eqs. 5-6 -> K meta (per channel, R1)
-//   3. thread t: K codes of its row, packed 4 per byte along channels
-//   4. V row: FWHT, per-token stats over each G-channel group, codes, meta
-//   5. salient tokens -> side table (PSA 16-bit originals; TSA 4-bit rotated)
+// One CTA (8 warps) per (G-token block j, unit u).  Rows are processed by
+// 8-lane groups, CPL = d/8 channels per lane, 4 rows per warp at a time:
+//   1. row -> fp32 -> FWHT x.H_s (R5): log2(CPL) in-lane butterfly stages, then
+//      3 shuffle stages across the 8 lanes (the same addition sequence as a
+//      sequential in-register FWHT, so results are bit-identical to it)
+//   2. K row -> smem (fp32) for the per-channel block stats (R1)
+//   3. V row: per-token stats over each G-channel group (lane reductions),
+//      Eqs. 5-6 -> V meta, codes -> S:146 bytes in smem
+//   4. salient rows -> side table (PSA: original 16-bit rows; TSA: 4-bit per
+//      token over G-channel groups with clip4, R11)
+//   5. thread ch: min/max of K channel ch over the block's non-salient tokens,
+//      Eqs. 5-6 -> K meta; then all threads build the 4x4-tile code words of K
+//      and V (common.cuh kword_idx / vword_idx) with coalesced stores.
 // Source rows come from the prefill inputs or, for a flush, from the ring.
+constexpr int kQThreads = 256;
+
+template <int CPL>
+__device__ __forceinline__ void fwht_lanes8(float (&x)[CPL], int cl) {
+#pragma unroll
+  for (int h = 1; h < CPL; h <<= 1)
+#pragma unroll
+    for (int i = 0; i < CPL; i += 2 * h)
+#pragma unroll
+      for (int j = i; j < i + h; ++j) {
+        const float a = x[j], b = x[j + h];
+        x[j] = __fadd_rn(a, b);
+        x[j + h] = __fsub_rn(a, b);
+      }
+#pragma unroll
+  for (int lm = 1; lm < 8; lm <<= 1) {
+    const float sg = (cl & lm) ? -1.f : 1.f;     // upper: partner - own; lower: own + partner
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) x[k] = __fmaf_rn(sg, x[k], __shfl_xor_sync(0xffffffffu, x[k], lm));
+  }
+}
+
+// min / max over the lanes of a channel group of GL lanes (within the 8-lane row group)
+template <int GL>
+__device__ __forceinline__ void group_minmax(float &mn, float &mx) {
+#pragma unroll
+  for (int o = 1; o < GL; o <<= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+}
+
 template <int D, int G, int DT>
-__global__ void __launch_bounds__(G) k_quantize_blocks(DevCache c, QuantSrc src, int block0,
-                                                       int last_block) {
-  constexpr int P = D + 1;                   // smem pitch (conflict-free columns)
+__global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, QuantSrc src, int block0,
+                                                               int last_block) {
+  constexpr int CPL = D / 8;                 // channels per lane
+  constexpr int GL = G / CPL;                // lanes per V channel group
+  constexpr int P = D + 4;                   // smem pitch (floats), 16-byte rows
   constexpr int NG = D / G;
-  extern __shared__ float xs[];              // [G][D+1]
+  constexpr int NW = kQThreads / 32;
+  extern __shared__ __align__(16) float xs[];     // [G][P] rotated K rows
   __shared__ float s_s[D], s_z[D];
   __shared__ int s_mode[D];
   __shared__ uint32_t s_bits[G / 32];
+  __shared__ __align__(16) uint8_t vb8[G * D / 4];   // V S:146 bytes per token
   __shared__ int s_base;
 
-  const int u = blockIdx.y, j = block0 + blockIdx.x, t = threadIdx.x;
-  const int tok = j * G + t;
+  const int u = blockIdx.y, j = block0 + blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, rg = lane >> 3, cl = lane & 7;
   const uint32_t *bm = c.bitmask + (size_t)u * c.bm_words;
-  if (t < G / 32) s_bits[t] = bm[j * (G / 32) + t];
-  if (t == 0) s_base = 0;
+  if (tid < G / 32) s_bits[tid] = bm[j * (G / 32) + tid];
+  if (tid == 0) s_base = 0;
   __syncthreads();
   {  // salient entries before this block -> first side slot of the block
     int cnt = 0;
-    for (int w = t; w < j * (G / 32); w += G) cnt += __popc(bm[w]);
+    for (int w = tid; w < j * (G / 32); w += kQThreads) cnt += __popc(bm[w]);
     if (cnt) atomicAdd(&s_base, cnt);
   }
-  const bool sal = (s_bits[t >> 5] >> (t & 31)) & 1u;
-  const size_t roff = (size_t)u * src.unit_stride +
-                      (size_t)(src.ring_slots ? tok % src.ring_slots : tok) * src.tok_stride;
-  const uint16_t *krow = src.K + roff;
-  const uint16_t *vrow = src.V + roff;
+  __syncthreads();
   uint8_t *pg = page_ptr(c, u, j);
   const bool tsa = c.kind == AKVQ_TSA;
+  float *vs_g = reinterpret_cast<float *>(pg + c.pg_vscale);
+  int32_t *vz_g = reinterpret_cast<int32_t *>(pg + c.pg_vzero);
 
-  // ---------------- K
-  float x[D];
-  load_row<D, DT>(krow, x);
-  fwht_reg<D>(x);
+  // ---------------- rows: FWHT of K and V, V quantization, side entries
+  for (int r0 = warp * 4; r0 < G; r0 += NW * 4) {
+    const int t = r0 + rg;                   // token within the block
+    const int tok = j * G + t;
+    const bool sal = (s_bits[t >> 5] >> (t & 31)) & 1u;
+    const size_t roff = (size_t)u * src.unit_stride +
+                        (size_t)(src.ring_slots ? tok % src.ring_slots : tok) * src.tok_stride;
+    const uint4 *kr = reinterpret_cast<const uint4 *>(src.K + roff + cl * CPL);
+    const uint4 *vr = reinterpret_cast<const uint4 *>(src.V + roff + cl * CPL);
+    uint4 kraw[CPL / 8], vraw[CPL / 8];
 #pragma unroll
-  for (int i = 0; i < D; ++i) xs[t * P + i] = x[i];
+    for (int i = 0; i < CPL / 8; ++i) { kraw[i] = kr[i]; vraw[i] = vr[i]; }
+    float k[CPL], v[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL / 8; ++i) { cvt8<DT>(kraw[i], k + 8 * i); cvt8<DT>(vraw[i], v + 8 * i); }
+    fwht_lanes8<CPL>(k, cl);
+    fwht_lanes8<CPL>(v, cl);
+    float4 *xk = reinterpret_cast<float4 *>(xs + t * P + cl * CPL);
+#pragma unroll
+    for (int i = 0; i < CPL / 4; ++i) xk[i] = make_float4(k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]);
+
+    // V: per token over the lane's channel group (Eqs. 3-6, clip2), salient -> 0
+    {
+      const int gi = (cl * CPL) / G;
+      float mn = v[0], mx = v[0];
+#pragma unroll
+      for (int i = 1; i < CPL; ++i) { mn = fminf(mn, v[i]); mx = fmaxf(mx, v[i]); }
+      group_minmax<GL>(mn, mx);
+      const QMeta m = q_meta(mn, mx, !sal, c.clip2, 3.f);
+      if ((cl % GL) == 0) {
+        vs_g[t * NG + gi] = sal ? 0.f : __fmul_rn(m.s, c.inv_sqrt_d);
+        vz_g[t * NG + gi] = sal ? 0 : zero_i32(m.zf);
+      }
+      static_assert(CPL == 8 || CPL == 16, "channels per lane");
+      uint32_t w = 0;                         // the lane's CPL/4 S:146 bytes
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) w |= (sal ? 0u : q_code(v[i], m, 3.f)) << (2 * i);
+      if constexpr (CPL == 16) *reinterpret_cast<uint32_t *>(vb8 + t * (D / 4) + cl * 4) = w;
+      else *reinterpret_cast<uint16_t *>(vb8 + t * (D / 4) + cl * 2) = (uint16_t)w;
+    }
+    // TSA 4-bit side stats (group reductions need every lane: computed for all rows)
+    QMeta mk4, mv4;
+    if (tsa) {
+      float mnk = k[0], mxk = k[0], mnv = v[0], mxv = v[0];
+#pragma unroll
+      for (int i = 1; i < CPL; ++i) {
+        mnk = fminf(mnk, k[i]); mxk = fmaxf(mxk, k[i]);
+        mnv = fminf(mnv, v[i]); mxv = fmaxf(mxv, v[i]);
+      }
+      group_minmax<GL>(mnk, mxk);
+      group_minmax<GL>(mnv, mxv);
+      mk4 = q_meta(mnk, mxk, true, c.clip4, 15.f);
+      mv4 = q_meta(mnv, mxv, true, c.clip4, 15.f);
+    }
+    // salient token -> side table (ascending token order); no shuffles below
+    if (sal) {
+      const uint32_t below = (t & 31) ? (s_bits[t >> 5] & ((1u << (t & 31)) - 1u)) : 0u;
+      int pos = s_base + __popc(below);
+      for (int w = 0; w < (t >> 5); ++w) pos += __popc(s_bits[w]);
+      uint8_t *se = side_ptr(c, u, pos);
+      if (cl == 0) c.side_idx[(size_t)u * c.side_cap + pos] = tok;
+      if (tsa) {   // 4-bit per token over G-channel groups, clip4 (R11)
+        const int gi = (cl * CPL) / G;
+        const QMeta mk = mk4, mv = mv4;
+        if ((cl % GL) == 0) {
+          reinterpret_cast<float *>(se)[gi] = __fmul_rn(mk.s, c.inv_sqrt_d);
+          reinterpret_cast<int32_t *>(se + 4 * NG)[gi] = zero_i32(mk.zf);
+          reinterpret_cast<float *>(se + 8 * NG)[gi] = __fmul_rn(mv.s, c.inv_sqrt_d);
+          reinterpret_cast<int32_t *>(se + 12 * NG)[gi] = zero_i32(mv.zf);
+        }
+        uint32_t ck[CPL / 8], cv[CPL / 8];
+#pragma unroll
+        for (int i = 0; i < CPL / 8; ++i) { ck[i] = 0; cv[i] = 0; }
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+          ck[i / 8] |= q_code(k[i], mk, 15.f) << (4 * (i % 8));
+          cv[i / 8] |= q_code(v[i], mv, 15.f) << (4 * (i % 8));
+        }
+        uint32_t *dk = reinterpret_cast<uint32_t *>(se + 16 * NG + cl * (CPL / 2));
+        uint32_t *dv = reinterpret_cast<uint32_t *>(se + 16 * NG + D / 2 + cl * (CPL / 2));
+#pragma unroll
+        for (int i = 0; i < CPL / 8; ++i) { dk[i] = ck[i]; dv[i] = cv[i]; }
+      } else {     // PSA pivot: original 16-bit K and V rows (R10)
+        uint4 *dk = reinterpret_cast<uint4 *>(se) + cl * (CPL / 8);
+        uint4 *dv = reinterpret_cast<uint4 *>(se + 2 * D) + cl * (CPL / 8);
+#pragma unroll
+        for (int i = 0; i < CPL / 8; ++i) { dk[i] = kraw[i]; dv[i] = vraw[i]; }
+      }
+    }
+  }
   __syncthreads();
-  for (int ch = t; ch < D; ch += G) {
+
+  // ---------------- K: per-channel block stats over non-salient tokens (R1)
+  for (int ch = tid; ch < D; ch += kQThreads) {
     float mn = 0.f, mx = 0.f;
     bool any = false;
     for (int i = 0; i < G; ++i) {
       if ((s_bits[i >> 5] >> (i & 31)) & 1u) continue;
-      const float v = xs[i * P + ch];
-      if (!any) { mn = v; mx = v; any = true; }
-      else { mn = fminf(mn, v); mx = fmaxf(mx, v); }
+      const float x = xs[i * P + ch];
+      if (!any) { mn = x; mx = x; any = true; }
+      else { mn = fminf(mn, x); mx = fmaxf(mx, x); }
     }
     const QMeta m = q_meta(mn, mx, any, c.clip2, 3.f);
     s_s[ch] = m.s; s_z[ch] = m.zf; s_mode[ch] = m.mode;
@@ -136,138 +262,39 @@ __global__ void __launch_bounds__(G) k_quantize_blocks(DevCache c, QuantSrc src,
     reinterpret_cast<int32_t *>(pg + c.pg_kzero)[ch] = zero_i32(m.zf);
   }
   __syncthreads();
-  // codes staged as one byte each in smem (xs is dead now), then re-packed into
-  // the page's 4x4-tile K words (common.cuh kword_idx) with coalesced stores
-  uint8_t *cs8 = reinterpret_cast<uint8_t *>(xs);            // [G][D] K codes
-  uint8_t *vb8 = cs8 + G * D;                                 // [G][D/4] V bytes
+  // ---------------- code words in the page's 4x4 tile layout
   {
-#pragma unroll
-    for (int w = 0; w < D / 4; ++w) {
-      uint32_t word = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int ch = 4 * w + i;
-        QMeta m; m.s = s_s[ch]; m.zf = s_z[ch]; m.mode = s_mode[ch];
-        const uint32_t code = sal ? 0u : q_code(x[ch], m, 3.f);
-        word |= code << (8 * i);
-      }
-      reinterpret_cast<uint32_t *>(cs8 + t * D)[w] = word;
-    }
-  }
-  __syncthreads();
-  {
-    constexpr int TQ = G / 4;
-    uint32_t *dst = reinterpret_cast<uint32_t *>(pg + c.pg_kcodes);
-    for (int wi = t; wi < (D / 4) * TQ; wi += G) {      // word wi -> (cq, tq)
+    constexpr int TQ = G / 4, CQ = D / 4;
+    uint32_t *dk = reinterpret_cast<uint32_t *>(pg + c.pg_kcodes);
+    for (int wi = tid; wi < CQ * TQ; wi += kQThreads) {   // K word wi -> (cq, tq)
       const int cq = (wi & 3) + 4 * (wi / (4 * TQ)), tq = (wi / 4) % TQ;
       uint32_t word = 0;
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int b = 0; b < 4; ++b) {
+        const int ch = 4 * cq + b;
+        QMeta m; m.s = s_s[ch]; m.zf = s_z[ch]; m.mode = s_mode[ch];
 #pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2)
-          word |= (uint32_t)cs8[(4 * tq + s2) * D + 4 * cq + b] << (8 * b + 2 * s2);
-      dst[wi] = word;
-    }
-  }
-  // side slot of this token (ascending token order within the side table)
-  const uint32_t below = (t & 31) ? (s_bits[t >> 5] & ((1u << (t & 31)) - 1u)) : 0u;
-  int pos = s_base + __popc(below);
-  for (int w = 0; w < (t >> 5); ++w) pos += __popc(s_bits[w]);
-  uint8_t *se = sal ? side_ptr(c, u, pos) : nullptr;
-  if (sal && tsa) {  // TSA text token: 4-bit per-token K groups, clip4 (R11)
-    float *sk = reinterpret_cast<float *>(se);
-    int32_t *zk = reinterpret_cast<int32_t *>(se + 4 * NG);
-    uint8_t *ck = se + 16 * NG;
-#pragma unroll
-    for (int gi = 0; gi < NG; ++gi) {
-      float mn = x[gi * G], mx = x[gi * G];
-#pragma unroll
-      for (int i = 1; i < G; ++i) { mn = fminf(mn, x[gi * G + i]); mx = fmaxf(mx, x[gi * G + i]); }
-      const QMeta m = q_meta(mn, mx, true, c.clip4, 15.f);
-      sk[gi] = __fmul_rn(m.s, c.inv_sqrt_d);
-      zk[gi] = zero_i32(m.zf);
-#pragma unroll
-      for (int i = 0; i < G; i += 2) {
-        const uint32_t lo = q_code(x[gi * G + i], m, 15.f), hi = q_code(x[gi * G + i + 1], m, 15.f);
-        ck[(gi * G + i) / 2] = (uint8_t)(lo | (hi << 4));
+        for (int s2 = 0; s2 < 4; ++s2) {
+          const int t = 4 * tq + s2;
+          const bool sal = (s_bits[t >> 5] >> (t & 31)) & 1u;
+          word |= (sal ? 0u : q_code(xs[t * P + ch], m, 3.f)) << (8 * b + 2 * s2);
+        }
       }
+      dk[wi] = word;
     }
-  }
-
-  // ---------------- V (per token over G-channel groups)
-  load_row<D, DT>(vrow, x);
-  fwht_reg<D>(x);
-  {
-    float *vs = reinterpret_cast<float *>(pg + c.pg_vscale) + (size_t)t * NG;
-    int32_t *vz = reinterpret_cast<int32_t *>(pg + c.pg_vzero) + (size_t)t * NG;
-    uint32_t wds[D / 16];
-#pragma unroll
-    for (int w = 0; w < D / 16; ++w) wds[w] = 0;
-#pragma unroll
-    for (int gi = 0; gi < NG; ++gi) {
-      float mn = x[gi * G], mx = x[gi * G];
-#pragma unroll
-      for (int i = 1; i < G; ++i) { mn = fminf(mn, x[gi * G + i]); mx = fmaxf(mx, x[gi * G + i]); }
-      QMeta m = q_meta(mn, mx, !sal, c.clip2, 3.f);
-      vs[gi] = sal ? 0.f : __fmul_rn(m.s, c.inv_sqrt_d);
-      vz[gi] = sal ? 0 : zero_i32(m.zf);
-#pragma unroll
-      for (int i = 0; i < G; ++i) {
-        const int ch = gi * G + i;
-        wds[ch / 16] |= (sal ? 0u : q_code(x[ch], m, 3.f)) << (2 * (ch % 16));
-      }
-    }
-    // the token's S:146 bytes -> smem, re-packed below into 4x4-tile V words
-#pragma unroll
-    for (int w = 0; w < D / 16; ++w) reinterpret_cast<uint32_t *>(vb8 + t * (D / 4))[w] = wds[w];
-  }
-  __syncthreads();
-  {
-    constexpr int CQ = D / 4;
-    uint32_t *dst = reinterpret_cast<uint32_t *>(pg + c.pg_vcodes);
-    for (int wi = t; wi < CQ * (G / 4); wi += G) {      // word wi -> (cq, tq)
+    uint32_t *dv = reinterpret_cast<uint32_t *>(pg + c.pg_vcodes);
+    for (int wi = tid; wi < CQ * TQ; wi += kQThreads) {   // V word wi -> (cq, tq)
       const int tq = (wi & 3) + 4 * (wi / (4 * CQ)), cq = (wi / 4) % CQ;
       uint32_t word = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) word |= (uint32_t)vb8[(4 * tq + b) * (D / 4) + cq] << (8 * b);
-      dst[wi] = word;
+      dv[wi] = word;
     }
   }
-  if (sal) {
-    c.side_idx[(size_t)u * c.side_cap + pos] = tok;
-    if (tsa) {
-      float *sv = reinterpret_cast<float *>(se + 8 * NG);
-      int32_t *zv = reinterpret_cast<int32_t *>(se + 12 * NG);
-      uint8_t *cv = se + 16 * NG + D / 2;
-#pragma unroll
-      for (int gi = 0; gi < NG; ++gi) {
-        float mn = x[gi * G], mx = x[gi * G];
-#pragma unroll
-        for (int i = 1; i < G; ++i) { mn = fminf(mn, x[gi * G + i]); mx = fmaxf(mx, x[gi * G + i]); }
-        const QMeta m = q_meta(mn, mx, true, c.clip4, 15.f);
-        sv[gi] = __fmul_rn(m.s, c.inv_sqrt_d);
-        zv[gi] = zero_i32(m.zf);
-#pragma unroll
-        for (int i = 0; i < G; i += 2) {
-          const uint32_t lo = q_code(x[gi * G + i], m, 15.f), hi = q_code(x[gi * G + i + 1], m, 15.f);
-          cv[(gi * G + i) / 2] = (uint8_t)(lo | (hi << 4));
-        }
-      }
-    } else {  // PSA pivot: original 16-bit K and V rows (R10)
-      uint4 *dk = reinterpret_cast<uint4 *>(se);
-      const uint4 *sk = reinterpret_cast<const uint4 *>(krow);
-      const uint4 *sv = reinterpret_cast<const uint4 *>(vrow);
-#pragma unroll
-      for (int i = 0; i < D / 8; ++i) { dk[i] = sk[i]; dk[D / 8 + i] = sv[i]; }
-    }
-  }
-  if (j == last_block) {  // number of side entries after this block
-    __syncthreads();
-    if (t == 0) {
-      int n = s_base;
-      for (int w = 0; w < G / 32; ++w) n += __popc(s_bits[w]);
-      c.side_cnt[u] = n;
-    }
+  if (j == last_block && tid == 0) {  // number of side entries after this block
+    int n = s_base;
+    for (int w = 0; w < G / 32; ++w) n += __popc(s_bits[w]);
+    c.side_cnt[u] = n;
   }
 }
 
@@ -325,11 +352,11 @@ cudaError_t launch_salient(const DevCache &c, const uint8_t *types, const float 
 template <int D, int G, int DT>
 static cudaError_t launch_q(const DevCache &c, const QuantSrc &src, int block0, int nblocks,
                             int last_block, cudaStream_t st) {
-  const size_t smem = (size_t)G * (D + 1) * sizeof(float);
+  const size_t smem = (size_t)G * (D + 4) * sizeof(float);
   auto kern = k_quantize_blocks<D, G, DT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(nblocks, c.U);
-  kern<<<grid, G, smem, st>>>(c, src, block0, last_block);
+  kern<<<grid, kQThreads, smem, st>>>(c, src, block0, last_block);
   return cudaGetLastError();
 }
 

@@ -8,13 +8,13 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > $OUT/smi.txt 2>&1
 for w in $WHAT; do
   case $w in
-    tests)  timeout 900 python -m pytest tests -m gpu -x -q > $OUT/tests.log 2>&1; echo "tests rc=$?" ;;
+    tests)  timeout -k 10 900 python -m pytest tests -m gpu -x -q --timeout 300 -o timeout_method=thread > $OUT/tests.log 2>&1; echo "tests rc=$?" ;;
     smoke)  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" ;;
-    bench)  timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; cat $OUT/bench.json ;;
-    launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+    bench)  timeout -k 10 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; cat $OUT/bench.json ;;
+    launches) timeout -k 10 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
                -k regex:"k_(decode|append|quantize|salient|ring|view|combine)" --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1; echo "launches rc=$?" ;;
     full)   for k in ${KERNELS:-k_decode_layer}; do
-              timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 200 -c 1 \
+              timeout -k 10 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 200 -c 1 \
                 -o $OUT/full_$k python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$k.log 2>&1; echo "full $k rc=$?"
             done ;;
   esac
