@@ -177,9 +177,10 @@ class OracleSample:
         return self.oracle.nthreads()
 
 
-def oracle_baseline(w, seconds=12.0, max_steps=60):
-    """cpu_baseline leg of the GPU run: ~10-30 s of oracle work."""
-    smp = OracleSample(w)
+def oracle_baseline(w, seconds=10.0, max_steps=250):
+    """cpu_baseline leg of the GPU run: ~10-30 s of oracle work (prefill of the
+    sampled units plus up to `seconds` of timed decode steps)."""
+    smp = OracleSample(w, n_units=128)
     vals = []
     while smp.steps < max_steps and smp.t_tot < seconds and smp.oc.L < w.capacity:
         vals.append(smp.step())
@@ -428,7 +429,7 @@ def main():
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic",
+            "dtype": "u8-dp4a+f32", "data": "synthetic",
             "config": {"workload": w.name, "source": "BJ:9 batch sweep at LLaVA-1.5-7B shape",
                        "layers": n_layers, "global_batch": w.batch, "heads": w.hq,
                        "kv_heads": w.hkv, "head_dim": w.d, "prompt_tokens": w.L0,
@@ -440,7 +441,7 @@ def main():
             "attention_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                         "traffic": None, "kernel": "k_decode_fused (append + attention + merge)",
+                         "traffic": None, "kernel": "k_decode_layer (append + all tiers + merge, one launch per layer)",
                          "bytes_per_launch": dec_bytes, "launch_ms": dec_ms,
                          "peak_src": peaks["src"]},
             "prefill": {"ms_all_layers": pre_ms, "quantize_gbs": pre_bytes / (pre_ms * 1e-3) / 1e9,
