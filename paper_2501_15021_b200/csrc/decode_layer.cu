@@ -46,19 +46,20 @@ constexpr int kRows = 8;           // 16-bit rows per ring chunk / side sub-load
 constexpr int kRows4 = 32;         // 4-bit TSA rows per side sub-load
 constexpr int kQMax = 32767;       // K-side fixed point: |Q| <= 2^15 - 1 (2 limbs)
 constexpr int kWMax = 65535;       // V-side fixed point: W <= 2^16 - 1 (2 limbs)
-__host__ __device__ constexpr int ly_ctas_per_sm(int nh) { return nh >= 4 ? 2 : (nh >= 2 ? 3 : 4); }
+__host__ __device__ constexpr int ly_ctas_per_sm(int nh) { return nh >= 4 ? 2 : (nh >= 2 ? 3 : 5); }
 
 // Per-warp shared memory (bytes):
-//   stages [kLyStages][SB] | qh [NH][D] f32 (q~ = q.H_s) | klimb [NH][D/16][8] u32 |
-//   vlimb [NH][NG][G/16][8] u32 | lgs [NH][kRows] f32 | barriers
+//   stages [kLyStages][SB] | qh [NH][D] f32 (q~ = q.H_s) | limbs: K [NH][D/16][8]
+//   u32 during a K half, V [NH][NG][G/16][8] u32 during a V half (same bytes) |
+//   sub-load descriptors | barriers
 template <int D, int G, int NH>
 struct LySmem {
   static constexpr int NG = D / G;
   static __host__ __device__ size_t qh_off(size_t sb) { return kLyStages * sb; }
+  static constexpr size_t KL = (size_t)NH * (D / 16) * 32, VL = (size_t)NH * NG * (G / 16) * 32;
   static __host__ __device__ size_t kl_off(size_t sb) { return qh_off(sb) + NH * D * 4; }
-  static __host__ __device__ size_t vl_off(size_t sb) { return kl_off(sb) + NH * (D / 16) * 32; }
-  static __host__ __device__ size_t lg_off(size_t sb) { return vl_off(sb) + NH * NG * (G / 16) * 32; }
-  static __host__ __device__ size_t ds_off(size_t sb) { return lg_off(sb) + NH * kRows * 4; }
+  static __host__ __device__ size_t vl_off(size_t sb) { return kl_off(sb); }   // shared
+  static __host__ __device__ size_t ds_off(size_t sb) { return kl_off(sb) + (KL > VL ? KL : VL); }
   static __host__ __device__ size_t bar_off(size_t sb) { return ds_off(sb) + kLyStages * 32; }
   static __host__ __device__ size_t warp_bytes(size_t sb) {
     return (bar_off(sb) + kLyStages * 8 + 127) / 128 * 128;
