@@ -382,6 +382,13 @@ def main():
             bytes_layers.append(Ul * decode_bytes_per_unit(w, kind, L, nq, side))
     dec_bytes = sum(bytes_layers) / len(bytes_layers)
     peaks = _peaks()
+    traffic = None          # dram bytes of one launch from a committed ncu --set full capture
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as fh:
+            tj = json.load(fh).get("k_decode_layer", {})
+        if tj.get("workload") == w.name and world == 1:
+            traffic = tj.get("traffic_bytes")
     achieved = dec_bytes / (dec_ms * 1e-3) / 1e9
     tokens_per_s = w.batch / (ms * 1e-3)
 
@@ -482,7 +489,7 @@ def main():
             "attention_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                         "traffic": None, "kernel": "k_decode_layer (append + all tiers + merge, one launch per layer)",
+                         "traffic": traffic, "kernel": "k_decode_layer (append + all tiers + merge, one launch per layer)",
                          "bytes_per_launch": dec_bytes, "launch_ms": dec_ms,
                          "peak_src": peaks["src"]},
             "prefill": {"ms_all_layers": pre_ms, "quantize_gbs": pre_bytes / (pre_ms * 1e-3) / 1e9,

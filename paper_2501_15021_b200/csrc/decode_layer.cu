@@ -79,6 +79,14 @@ __host__ __device__ inline size_t ly_stage_bytes(const DevCache &c) {
   return (m + 127) / 128 * 128;
 }
 
+// 2^x with the SFU's approximate ex2 (rel. error ~2^-22, flushes subnormal
+// results to 0): softmax weights below 2^-126 of the running max are 0 anyway.
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t fmask(uint32_t w, int s) { return w & (0x03030303u << (2 * s)); }
 
 template <int DT>
@@ -339,8 +347,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
       const float m_new = fmaxf(m_run[h], mx);
-      const float sc = exp2f(m_run[h] - m_new);
-      const float p = exp2f(t - m_new);
+      const float sc = ex2(m_run[h] - m_new);
+      const float p = ex2(t - m_new);
       float ps = p;
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
@@ -469,8 +477,10 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           am = fmaxf(fmaxf(fabsf(qsb[0]), fabsf(qsb[1])), fmaxf(fabsf(qsb[2]), fabsf(qsb[3])));
         }
         const float M = warp_max(am);
-        const float inv = M > 0.f ? (float)kQMax / M : 0.f;
-        const float delta = M > 0.f ? M / (float)kQMax : 0.f;
+        // fixed-point scale (any consistent inv / delta pair works: the sum is
+        // exact for the rounded Q; |Q| <= kQMax holds within __fdividef's 2 ulp)
+        const float inv = M > 0.f ? __fdividef((float)kQMax, M) : 0.f;
+        const float delta = M * (1.0f / (float)kQMax);
         int Qv[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) Qv[b] = __float2int_rn(qsb[b] * inv);
@@ -543,13 +553,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
 #pragma unroll
         for (int gi = 0; gi < NG; ++gi) { dwv[h][gi] = 0.f; zwv[h][gi] = 0.f; }
         if (!live[h]) continue;
-        const float sc = exp2f(m_run[h] - m_new);
+        const float sc = ex2(m_run[h] - m_new);
         m_run[h] = m_new;
 #pragma unroll
         for (int k = 0; k < 4; ++k) { o_rot[h][k] *= sc; o_org[h][k] *= sc; }
         float pr[4], psum = 0.f;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { pr[k] = exp2f(lg[h][k] - m_new); psum += pr[k]; }
+        for (int k = 0; k < 4; ++k) { pr[k] = ex2(lg[h][k] - m_new); psum += pr[k]; }
         psum = warp_sum(kcs == 0 ? psum : 0.f);
         l_run[h] = l_run[h] * sc + psum;
 #pragma unroll
@@ -563,7 +573,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           wmax = warp_max(wmax);
           // 16-bit fixed point of the page's largest weight; the zero-point
           // term uses the same rounded weights (incoherent rounding error)
-          const float invw = wmax > 0.f ? (float)kWMax / wmax : 0.f;
+          const float invw = wmax > 0.f ? __fdividef((float)kWMax, wmax) : 0.f;
           uint32_t W[4];
           float zs = 0.f;
 #pragma unroll
@@ -572,7 +582,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
             zs = fmaf((float)W[k], (float)vz[(4 * ktq + k) * NG + gi], zs);
           }
           zwv[h][gi] = warp_sum(kcs == 0 ? zs : 0.f);
-          dwv[h][gi] = wmax / (float)kWMax;
+          dwv[h][gi] = wmax * (1.0f / (float)kWMax);
           if (kcs == 0) {
             const uint32_t lo = prmt(prmt(W[0], W[1], 0x0040), prmt(W[2], W[3], 0x0040), 0x5410);
             const uint32_t hi = prmt(prmt(W[0], W[1], 0x0051), prmt(W[2], W[3], 0x0051), 0x5410);
