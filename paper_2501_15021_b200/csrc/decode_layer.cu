@@ -134,6 +134,21 @@ struct LySub {
   int a, n;      // page index | first row (ring offset from n_q / side entry) and row count
   int ring;      // 1 if ring rows
 };
+// descriptor as it travels from the producer lane to the warp: two words
+//   x = u, y = (kind + 1) | ring << 3 | n << 4 (n < 64) | a << 10
+__device__ __forceinline__ uint2 pack_sub(const LySub &s) {
+  return make_uint2((uint32_t)s.u, (uint32_t)(s.kind + 1) | ((uint32_t)s.ring << 3) |
+                                       ((uint32_t)s.n << 4) | ((uint32_t)s.a << 10));
+}
+__device__ __forceinline__ LySub unpack_sub(uint2 w) {
+  LySub s;
+  s.u = (int)w.x;
+  s.kind = (int)(w.y & 7u) - 1;
+  s.ring = (int)((w.y >> 3) & 1u);
+  s.n = (int)((w.y >> 4) & 63u);
+  s.a = (int)(w.y >> 10);
+  return s;
+}
 
 __device__ __forceinline__ uint2 lds64(uint32_t a) {
   uint2 v;
@@ -189,7 +204,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   float *qh = reinterpret_cast<float *>(wsm + S::qh_off(SB));
   uint32_t *klimb = reinterpret_cast<uint32_t *>(wsm + S::kl_off(SB));
   uint32_t *vlimb = reinterpret_cast<uint32_t *>(wsm + S::vl_off(SB));
-  LySub *desc = reinterpret_cast<LySub *>(wsm + S::ds_off(SB));
+  uint2 *desc = reinterpret_cast<uint2 *>(wsm + S::ds_off(SB));
   uint64_t *bar = reinterpret_cast<uint64_t *>(wsm + S::bar_off(SB));
 
   pdl_wait();                                   // q, k, v and the cache come from preceding work
@@ -221,7 +236,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       sb.u = pu;
       sb.ring = 0;
       if (kind == 0) {                            // page: K half then V half
-        sb.kind = part_i; sb.a = a; sb.n = G;
+        sb.kind = part_i; sb.a = a; sb.n = 0;      // (n unused for pages; 6-bit field)
         next = part_i == 1;
         part_i = next ? 0 : 1;
       } else if (kind == 2) {                     // ring chunk (rows n of it)
@@ -244,7 +259,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       if (ok) break;
       sb.kind = -1;
     }
-    desc[st] = sb;
+    desc[st] = pack_sub(sb);
     if (sb.kind < 0) return;
     uint8_t *dst = wsm + (size_t)st * SB;
     if (sb.kind <= 1) {
@@ -327,7 +342,9 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           float a0, a1, a2, a3;
           cvt2<DT>(v.x, a0, a1);
           cvt2<DT>(v.y, a2, a3);
-          dot[i] = fmaf(qk[h][0], a0, fmaf(qk[h][1], a1, fmaf(qk[h][2], a2, qk[h][3] * a3)));
+          float2 t2 = __fmul2_rn(make_float2(qk[h][0], qk[h][1]), make_float2(a0, a1));
+          t2 = __ffma2_rn(make_float2(qk[h][2], qk[h][3]), make_float2(a2, a3), t2);
+          dot[i] = t2.x + t2.y;
         } else {   // s_g (sum q~ code - z_g sum q~) over the lane's 4 channels
           const float sk = lds_f32(ra + 4 * vgam);
           const float zk = (float)lds_s32(ra + 4 * NG + 4 * vgam);
@@ -394,7 +411,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   int st = 0;
   uint32_t par = 0;
   for (;;) {
-    const LySub s = desc[st];
+    const LySub s = unpack_sub(desc[st]);
     if (s.kind < 0) break;
     uint8_t *B = wsm + (size_t)st * SB;
     if (lp.stream_only) {                           // profiling: pipeline only
