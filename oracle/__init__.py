@@ -46,7 +46,7 @@ class _Cfg(C.Structure):
     _fields_ = [("U", C.c_int), ("g", C.c_int), ("d", C.c_int), ("G", C.c_int),
                 ("R", C.c_int), ("capacity", C.c_int), ("top_k", C.c_int),
                 ("kind", C.c_int), ("dtype16", C.c_int), ("clip2", C.c_float),
-                ("clip4", C.c_float)]
+                ("clip4", C.c_float), ("k_axis", C.c_int)]
 
 
 class _Export(C.Structure):
@@ -177,6 +177,7 @@ class OracleConfig:
     dtype16: int = BF16
     clip2: float = 0.8
     clip4: float = 1.0
+    k_axis: int = 0          # 0 per channel (R1), 1 per token (NEXT-1)
 
 
 class OracleCache:
@@ -185,7 +186,7 @@ class OracleCache:
     def __init__(self, cfg: OracleConfig):
         self.cfg = cfg
         c = _Cfg(cfg.U, cfg.g, cfg.d, cfg.G, cfg.R, cfg.capacity, cfg.top_k, cfg.kind,
-                 cfg.dtype16, cfg.clip2, cfg.clip4)
+                 cfg.dtype16, cfg.clip2, cfg.clip4, cfg.k_axis)
         st = C.c_int(0)
         self._h = lib().orc_new(C.byref(c), C.byref(st))
         if not self._h:
@@ -270,4 +271,7 @@ class OracleCache:
         lib().orc_export(self._h, C.byref(ex))
         for k in ("side_index", "side16", "side4", "side4_scale", "side4_zero"):
             a[k] = a[k][:, :sc]
+        if cfg.k_axis == 1:      # per-token K meta: [U][cap][d/G] (same element count)
+            for k in ("kscale", "kzero", "kscale32"):
+                a[k] = a[k].reshape(U, cap, ng)
         return a

@@ -244,7 +244,8 @@ orc_cache *orc_new(const orc_config *cfg, int *status) {
       cfg->R < 0 || cfg->capacity < 1 || cfg->top_k < 0 ||
       !(cfg->clip2 > 0.0f && cfg->clip2 <= 1.0f) ||
       !(cfg->clip4 > 0.0f && cfg->clip4 <= 1.0f) ||
-      (cfg->kind != ORC_TSA && cfg->kind != ORC_PSA)) {
+      (cfg->kind != ORC_TSA && cfg->kind != ORC_PSA) ||
+      (cfg->k_axis != 0 && cfg->k_axis != 1)) {
     if (status) *status = ORC_EINVAL;
     return NULL;
   }
@@ -312,7 +313,9 @@ static void rotate_row_fp32(const orc_cache *c, const uint16_t *row, float *out)
 }
 
 /* Quantize block j = tokens [jG, (j+1)G) of unit u (R1):     */
-/*  K: per channel c over the block's non-salient tokens (2-bit, clip2). */
+/*  K: per channel c over the block's non-salient tokens (2-bit, clip2), */
+/*     or (k_axis 1, P:246 literally) per token over G-channel groups    */
+/*     exactly like V, meta at [token][group] in the same arrays.        */
 /*  V: per token over G-channel groups (2-bit, clip2); salient tokens    */
 /*     get codes 0 and meta (0, 0).                                      */
 /*  Salient tokens enter the side table in ascending token order:        */
@@ -326,11 +329,27 @@ static void quantize_block(orc_cache *c, int u, int j) {
   }
   const uint8_t *skip = c->sal + (long)u * c->cap + t0;
   const long mb = ((long)u * (c->cap / G) + j) * d;
-  for (int ch = 0; ch < d; ++ch)           /* K per channel over G tokens */
-    orc_quantize_group(c->xk + ROW(c, u, t0) + ch, skip, G, d, 2, c->cfg.clip2,
-                       &c->ks32[mb + ch], &c->kz[mb + ch],
-                       c->kc + ROW(c, u, t0) + ch, d);
   const int ng = d / G;
+  if (c->cfg.k_axis == 0) {
+    for (int ch = 0; ch < d; ++ch)         /* K per channel over G tokens */
+      orc_quantize_group(c->xk + ROW(c, u, t0) + ch, skip, G, d, 2, c->cfg.clip2,
+                         &c->ks32[mb + ch], &c->kz[mb + ch],
+                         c->kc + ROW(c, u, t0) + ch, d);
+  } else {
+    for (int t = t0; t < t0 + G; ++t) {    /* K per token over G channels */
+      const long km = ((long)u * c->cap + t) * ng;
+      for (int gi = 0; gi < ng; ++gi) {
+        if (c->sal[(long)u * c->cap + t]) {
+          c->ks32[km + gi] = 0.0f; c->kz[km + gi] = 0;
+          memset(c->kc + ROW(c, u, t) + gi * G, 0, (size_t)G);
+        } else {
+          orc_quantize_group(c->xk + ROW(c, u, t) + gi * G, NULL, G, 1, 2,
+                             c->cfg.clip2, &c->ks32[km + gi], &c->kz[km + gi],
+                             c->kc + ROW(c, u, t) + gi * G, 1);
+        }
+      }
+    }
+  }
   for (int t = t0; t < t0 + G; ++t) {      /* V per token over G channels */
     const long vm = ((long)u * c->cap + t) * ng;
     for (int gi = 0; gi < ng; ++gi) {
@@ -452,8 +471,9 @@ static void view_row(const orc_cache *c, int u, int t, double *Kh, double *Vh) {
   const long mb = ((long)u * (c->cap / G) + j) * d;
   const long vm = ((long)u * c->cap + t) * ng;
   for (int i = 0; i < d; ++i) {
-    Kh[i] = (double)c->ks32[mb + i] * rs *
-            ((double)c->kc[ROW(c, u, t) + i] - (double)c->kz[mb + i]);
+    const long ki = c->cfg.k_axis == 0 ? mb + i : vm + i / G;   /* per channel | per token */
+    Kh[i] = (double)c->ks32[ki] * rs *
+            ((double)c->kc[ROW(c, u, t) + i] - (double)c->kz[ki]);
     Vh[i] = (double)c->vs32[vm + i / G] * rs *
             ((double)c->vc[ROW(c, u, t) + i] - (double)c->vz[vm + i / G]);
   }

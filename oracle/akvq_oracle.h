@@ -43,6 +43,9 @@ typedef struct {
   int dtype16;    /* ORC_BF16 / ORC_FP16                                    */
   float clip2;    /* clip ratio for 2-bit (0.8)                      */
   float clip4;    /* clip ratio for 4-bit (1.0)                      */
+  int k_axis;     /* 0: K per channel over G-token blocks (R1, graded);
+                     1: K per token over G-channel groups, the paper-literal
+                     "per-token dynamic" rule of P:246       */
 } orc_config;
 
 typedef struct orc_cache orc_cache;

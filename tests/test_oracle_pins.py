@@ -241,6 +241,73 @@ def test_per_channel_block_hand_worked(orc):
         assert np.allclose(e["kscale"][0, 0], np.array([1, -1, 0, 0]) / 2)
 
 
+def test_per_token_k_hand_worked(orc):
+    """k_axis = 1 ("per-token"): K quantized per token over
+    G-channel groups.  d = G = 4, 2-bit, clip 0.8, rotated targets chosen by hand.
+      token 0: [0, 1, 2, 4] -> cmx 3.2, cmn 0, scale 3.2/3, zero 0,
+               x/scale = [0, .9375, 1.875, 3.75] -> codes [0, 1, 2, 3]
+      token 1: [-4, -2, 0, 2] -> cmx 1.6, cmn -3.2, scale 1.6, zero 2,
+               x/scale = [-2.5?] avoided: [-4,-2,0,2]/1.6 = [-2.5, ...] is a tie,
+               so token 1 = [-4, -1, 0, 3]: cmx 2.4, cmn -3.2, scale 5.6/3,
+               cmn/scale = -12/7 -> zero 2, x/scale = [-15/7, -15/28, 0, 45/28]
+               -> rne [-2, -1, 0, 2] + 2 -> codes [0, 1, 2, 3] (clamped 4 -> 3)
+      tokens 2, 3: constant rows (degenerate: scale = the constant, zero 0, codes 1)
+    The same rows with k_axis = 0 give per-channel meta instead (shape check)."""
+    X = np.array([[0, 1, 2, 4], [-4, -1, 0, 3], [2, 2, 2, 2], [0, 0, 0, 0]], float)
+    K = _rows_with_rotation(X)[None]
+    c = orc.OracleCache(_cfg(orc, kind=orc.PSA, top_k=0, k_axis=1))
+    assert c.prefill(K, K, colsum=np.zeros((1, 1, 4), np.float32)) == 0 and c.nq == 4
+    e = c.export()
+    assert e["kscale32"].shape == (1, c.cap, 1)
+    s0, s1 = np.float32(np.float32(3.2) / np.float32(3.0)), np.float32(5.6) / np.float32(3.0)
+    assert np.isclose(e["kscale32"][0, 0, 0], 3.2 / 3, rtol=1e-6)
+    assert np.isclose(e["kscale32"][0, 1, 0], 5.6 / 3, rtol=1e-6)
+    assert e["kscale32"][0, 2, 0] == 2.0 and e["kscale32"][0, 3, 0] == 0.0
+    assert e["kzero"][0, :4, 0].tolist() == [0, 2, 0, 0]
+    codes = orc.unpack(e["kcodes"][0, :4].reshape(-1), 16, 2).reshape(4, 4)
+    assert codes.tolist() == [[0, 1, 2, 3], [0, 1, 2, 3], [1, 1, 1, 1], [1, 1, 1, 1]]
+    # dequantized K (normalized basis) = scale/sqrt(d) * (code - zero)
+    Kh, _ = c.view()
+    assert np.allclose(Kh[0, 0], (3.2 / 3) / 2 * np.array([0, 1, 2, 3]), atol=1e-6)
+    assert np.allclose(Kh[0, 1], (5.6 / 3) / 2 * (np.array([0, 1, 2, 3]) - 2), atol=1e-6)
+    assert np.allclose(Kh[0, 2], 2.0 / 2 * 1) and np.allclose(Kh[0, 3], 0.0)
+    del s0, s1
+
+
+def test_per_token_k_bounds_and_library_sdpa(orc):
+    """k_axis = 1 on random outlier data: every in-clip K element within scale/2
+    of its dequantized value, and decode = library SDPA (torch,
+    fp64) over the oracle's own dequantized view, un-rotated by scipy's H."""
+    rng = np.random.default_rng(7)
+    d, G, L0 = 64, 32, 80
+    K = rng.standard_normal((2, L0, d)) * 2.0
+    K[:, :, 5] *= 20.0
+    V = rng.standard_normal((2, L0, d))
+    cfg = _cfg(orc, U=2, d=d, G=G, R=8, capacity=96, top_k=3, k_axis=1)
+    c = orc.OracleCache(cfg)
+    cs = rng.random((2, 1, L0)).astype(np.float32)
+    assert c.prefill(_f16_bits(K), _f16_bits(V), colsum=cs) == 0
+    e = c.export()
+    Kh, Vh = c.view()
+    nq = c.nq
+    xs = e["xs_k"][:, :nq].astype(np.float64) / np.sqrt(d)      # rotated, normalized
+    sal = e["salient"][:, :nq].astype(bool)
+    sc = np.repeat(e["kscale"][:, :nq], G, axis=-1)             # per token, per channel
+    zf = np.repeat(e["kzero"][:, :nq], G, axis=-1).astype(np.float64)
+    lo, hi = sc * (0 - zf), sc * (3 - zf)
+    inclip = (xs >= np.minimum(lo, hi) - 1e-9) & (xs <= np.maximum(lo, hi) + 1e-9)
+    err = np.abs(xs - Kh[:, :nq])
+    ok = (err <= sc / 2 + 1e-9) | ~inclip
+    assert ok[~sal].all()
+    q = _f16_bits(rng.standard_normal((2, 1, d)))
+    out = c.decode(q)
+    H = scipy.linalg.hadamard(d) / np.sqrt(d)
+    for u in range(2):
+        qh = q[u].view(np.float16).astype(np.float64) @ H
+        ref = _sdpa64(qh, Kh[u], Vh[u]) @ H
+        assert np.abs(out[u] - ref).max() < 1e-9
+
+
 def test_tier_rule_examples(orc):
     """S:332-333 tier examples, with G chosen so the block boundary equals L - R."""
     L, R, d, G = 300, 128, 4, 4
