@@ -56,6 +56,9 @@ typedef enum {
 
 typedef enum { AKVQ_TSA = 0, AKVQ_PSA = 1 } akvq_kind;        /* Table I */
 typedef enum { AKVQ_BF16 = 0, AKVQ_FP16 = 1 } akvq_dtype16;   /* R13 */
+/* K quantization axis: per channel over G-token blocks (R1, BJ:5, graded) or
+ * per token over G-channel groups (P:246 literally). */
+typedef enum { AKVQ_K_PER_CHANNEL = 0, AKVQ_K_PER_TOKEN = 1 } akvq_k_axis;
 
 /* decode flags */
 #define AKVQ_OUT_ROTATED 1u     /* return o' = sum p V^ in the rotated basis
@@ -78,6 +81,7 @@ typedef struct {
   int32_t dtype16;    /* akvq_dtype16 of K/V/q inputs and 16-bit tiers        */
   float clip2;        /* 2-bit clip ratio, (0,1], paper 0.8           */
   float clip4;        /* 4-bit clip ratio, (0,1], paper 1.0           */
+  int32_t k_axis;     /* akvq_k_axis (0 = per channel, the graded default)    */
 } akvq_config;
 
 /* Byte layout of the caller's cache buffer (all offsets from its base;
@@ -85,8 +89,9 @@ typedef struct {
  * n_pages = cap / G; ng = d / G; slots = R + G.
  *
  *  pages   [U][n_pages][page_bytes]        one page = one G-token block:
- *            +pg_kscale  f32 [d]     K scale per channel (normalized basis)
- *            +pg_kzero   i32 [d]     K zero point per channel
+ *            +pg_kscale  f32 [d]     K scale per channel (normalized basis);
+ *                                    per token: f32 [G][ng] (same bytes)
+ *            +pg_kzero   i32 [d]     K zero point per channel; per token [G][ng]
  *            +pg_kcodes  u8  [G][d/4] K codes, 4 per byte along channels
  *            +pg_vscale  f32 [G][ng] V scale per token and channel group
  *            +pg_vzero   i32 [G][ng]

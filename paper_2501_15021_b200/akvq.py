@@ -45,7 +45,7 @@ class akvq_config(C.Structure):
     _fields_ = [("n_units", C.c_int32), ("q_per_kv", C.c_int32), ("head_dim", C.c_int32),
                 ("group", C.c_int32), ("residual", C.c_int32), ("capacity", C.c_int32),
                 ("top_k", C.c_int32), ("kind", C.c_int32), ("dtype16", C.c_int32),
-                ("clip2", C.c_float), ("clip4", C.c_float)]
+                ("clip2", C.c_float), ("clip4", C.c_float), ("k_axis", C.c_int32)]
 
 
 class akvq_layout(C.Structure):
@@ -147,8 +147,8 @@ def _stream(stream: Optional[torch.cuda.Stream]):
 
 
 def make_config(U, g, d, G, R, capacity, top_k, kind, dtype16=AKVQ_BF16, clip2=0.8,
-                clip4=1.0) -> akvq_config:
-    return akvq_config(U, g, d, G, R, capacity, top_k, kind, dtype16, clip2, clip4)
+                clip4=1.0, k_axis=0) -> akvq_config:
+    return akvq_config(U, g, d, G, R, capacity, top_k, kind, dtype16, clip2, clip4, k_axis)
 
 
 # ----------------------------------------------------------------- C-ABI calls

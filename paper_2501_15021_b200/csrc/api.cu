@@ -23,7 +23,8 @@ akvq_status check_config(const akvq_config *f) {
       f->top_k < 0 || !is_pow2(f->head_dim) || !is_pow2(f->group) ||
       !(f->clip2 > 0.f && f->clip2 <= 1.f) || !(f->clip4 > 0.f && f->clip4 <= 1.f) ||
       (f->kind != AKVQ_TSA && f->kind != AKVQ_PSA) ||
-      (f->dtype16 != AKVQ_BF16 && f->dtype16 != AKVQ_FP16))
+      (f->dtype16 != AKVQ_BF16 && f->dtype16 != AKVQ_FP16) ||
+      (f->k_axis != AKVQ_K_PER_CHANNEL && f->k_axis != AKVQ_K_PER_TOKEN))
     return AKVQ_EINVAL;
   if ((f->head_dim != 64 && f->head_dim != 128) || f->group < 32 || f->group > 128 ||
       f->group > f->head_dim || f->q_per_kv > 16 || f->top_k > 32)
@@ -51,7 +52,7 @@ DevCache make_dev(const akvq_cache *c) {
   d.n_pages = y.n_pages; d.slots = y.slots; d.bm_words = y.bitmask_words;
   d.side_cap = y.side_cap;
   d.U = f.n_units; d.g = f.q_per_kv; d.d = f.head_dim; d.G = f.group; d.R = f.residual;
-  d.ng = y.ng; d.kind = f.kind;
+  d.ng = y.ng; d.kind = f.kind; d.k_axis = f.k_axis;
   d.clip2 = f.clip2; d.clip4 = f.clip4;
   d.inv_sqrt_d = (float)(1.0 / sqrt((double)f.head_dim));
   return d;

@@ -25,7 +25,7 @@ struct DevCache {
   uint32_t page_bytes, pg_kscale, pg_kzero, pg_kcodes, pg_vscale, pg_vzero, pg_vcodes;
   uint32_t side_entry;
   int32_t n_pages, slots, bm_words, side_cap;
-  int32_t U, g, d, G, R, ng, kind;
+  int32_t U, g, d, G, R, ng, kind, k_axis;
   float clip2, clip4, inv_sqrt_d;
 };
 

@@ -118,13 +118,15 @@ __global__ void __launch_bounds__(kThreads) k_decode_split(DevCache c, DecodePla
       const uint8_t *P = page_ptr(c, u, pg);
       const float *ks = reinterpret_cast<const float *>(P + c.pg_kscale);
       const int32_t *kz = reinterpret_cast<const int32_t *>(P + c.pg_kzero);
-      // prescale q~ by the page's per-channel K scale; bias = sum qs * zero
+      // per channel: prescale q~ by the page's K scale, bias = sum qs * zero;
+      // per token (NEXT-1): q~ only, scale / zero applied per token below
+      const bool kt = c.k_axis == AKVQ_K_PER_TOKEN;
       for (int h = 0; h < g; ++h) {
         float part = 0.f;
         for (int ch = lane; ch < D; ch += 32) {
-          const float v = qh[h * D + ch] * ks[ch] * alpha_q;
+          const float v = qh[h * D + ch] * (kt ? 1.f : ks[ch]) * alpha_q;
           qs[h * D + ch] = v;
-          part += v * (float)kz[ch];
+          part += kt ? 0.f : v * (float)kz[ch];
         }
         part = warp_sum(part);
         if (lane == 0) bias[h] = part;
@@ -145,10 +147,16 @@ __global__ void __launch_bounds__(kThreads) k_decode_split(DevCache c, DecodePla
         const int sh = 2 * ((tlb + ti) & 3);
         for (int h = 0; h < g; ++h) {
           const float *qq = qs + h * D + cq * (D / 4);
-          float dot = 0.f;
+          float dot = 0.f, qsum = 0.f;
 #pragma unroll
-          for (int k = 0; k < D / 4; ++k)
+          for (int k = 0; k < D / 4; ++k) {
             dot = fmaf(qq[k], (float)((by[k] >> sh) & 3u), dot);
+            qsum += qq[k];
+          }
+          if (kt) {   // this lane's D/4 channels lie in one G-channel group
+            const int mi = (tlb + ti) * NG + (cq * (D / 4)) / G;
+            dot = ks[mi] * (dot - (float)kz[mi] * qsum);
+          }
           dot += __shfl_xor_sync(0xffffffffu, dot, 1);
           dot += __shfl_xor_sync(0xffffffffu, dot, 2);
           if (cq == 0) lg[h * 32 + ti] = dot - bias[h];
@@ -508,10 +516,12 @@ __global__ void k_view(DevCache c, int L, int n_q, float *__restrict__ Ko, float
   const int32_t *vz = reinterpret_cast<const int32_t *>(P + c.pg_vzero);
   const uint8_t *kc = P + c.pg_kcodes;
   const uint8_t *vc = P + c.pg_vcodes;
+  const bool kt = c.k_axis == AKVQ_K_PER_TOKEN;
   for (int i = lane; i < D; i += 32) {
     const int ck = (int)kcode_at(kc, tl, i, G);
     const int cv = (int)vcode_at(vc, tl, i, D);
-    ko[i] = ks[i] * (float)(ck - kz[i]);
+    const int ki = kt ? tl * NG + i / G : i;         // per token [G][NG] | per channel [D]
+    ko[i] = ks[ki] * (float)(ck - kz[ki]);
     vo[i] = vs[tl * NG + i / G] * (float)(cv - vz[tl * NG + i / G]);
   }
 }

@@ -481,6 +481,98 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       const float4 *ks4 = reinterpret_cast<const float4 *>(B + c.pg_kscale);
       const int4 *kz4 = reinterpret_cast<const int4 *>(B + c.pg_kzero);
       const uint4 *kc4 = reinterpret_cast<const uint4 *>(B + c.pg_kcodes);
+      if (c.k_axis == AKVQ_K_PER_TOKEN) {
+        // ---- per-token K (NEXT-1): Q_c = rn(q~_c / delta) once per page,
+        // logit_t = alpha delta sum_g s_tg (sum_{c in g} Q_c code_tc - z_tg SQ_g)
+        const float *ksT = reinterpret_cast<const float *>(B + c.pg_kscale);    // [G][NG]
+        const int32_t *kzT = reinterpret_cast<const int32_t *>(B + c.pg_kzero);
+        constexpr int IPG = (G / 16) / KCS > 0 ? (G / 16) / KCS : 1;   // K iterations per group
+        float dT[NH];
+        int sq16[NH];                                // lanes 4cg..4cg+3: sum of Q over cg's 16 channels
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          float qv4[4] = {0.f, 0.f, 0.f, 0.f}, am = 0.f;
+          if (lane < CQ) {
+            const float4 qv = reinterpret_cast<const float4 *>(qh + h * D)[lane];
+            qv4[0] = qv.x; qv4[1] = qv.y; qv4[2] = qv.z; qv4[3] = qv.w;
+            am = fmaxf(fmaxf(fabsf(qv.x), fabsf(qv.y)), fmaxf(fabsf(qv.z), fabsf(qv.w)));
+          }
+          const float M = warp_max(am);
+          const float inv = M > 0.f ? __fdividef((float)kQMax, M) : 0.f;
+          dT[h] = alpha_k * M * (1.0f / (float)kQMax);
+          int Qv[4];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) Qv[b] = __float2int_rn(qv4[b] * inv);
+          int sq = (Qv[0] + Qv[1]) + (Qv[2] + Qv[3]);
+          sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+          sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+          sq16[h] = sq;
+          if (lane < CQ) {
+            const uint32_t lo = prmt(prmt(Qv[0], Qv[1], 0x0040), prmt(Qv[2], Qv[3], 0x0040), 0x5410);
+            const uint32_t hi = prmt(prmt(Qv[0], Qv[1], 0x0051), prmt(Qv[2], Qv[3], 0x0051), 0x5410);
+            uint32_t *kl = klimb + (h * CG + (lane >> 2)) * 8 + (lane & 3);
+            kl[0] = lo;
+            kl[4] = hi;
+          }
+        }
+        __syncwarp();
+        int acc[NH][4][2], zacc[NH];                // zacc: sum of Q over the folded cgs
+        float part[NH][4];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          zacc[h] = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) { acc[h][k][0] = 0; acc[h][k][1] = 0; part[h][k] = 0.f; }
+        }
+#pragma unroll
+        for (int i = 0; i < CG / KCS; ++i) {
+          const int cg = kcs + KCS * i;
+          const uint4 w4 = kc4[cg * TQ + ktq];
+          const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            const uint4 lo4 = reinterpret_cast<const uint4 *>(klimb + (h * CG + cg) * 8)[0];
+            const uint4 hi4 = reinterpret_cast<const uint4 *>(klimb + (h * CG + cg) * 8)[1];
+            const uint32_t lo[4] = {lo4.x, lo4.y, lo4.z, lo4.w};
+            const uint32_t hi[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t x = fmask(wd[j], k);
+                acc[h][k][0] = dp4a_uu(x, lo[j], acc[h][k][0]);
+                acc[h][k][1] = dp4a_us(x, hi[j], acc[h][k][1]);
+              }
+          }
+#pragma unroll
+          for (int h = 0; h < NH; ++h) zacc[h] += __shfl_sync(0xffffffffu, sq16[h], 4 * cg);
+          if ((i + 1) % IPG == 0) {                  // group of cg ends: fold with s_tg, z_tg
+            const int gi = (cg * 16) / G;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+              const float sqg = (float)zacc[h];
+              zacc[h] = 0;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int mi = (4 * ktq + k) * NG + gi;
+                const float tot = (float)(acc[h][k][1] * 256 + acc[h][k][0]) * (1.0f / (float)(1 << (2 * k)));
+                part[h][k] = fmaf(ksT[mi], tot - (float)kzT[mi] * sqg, part[h][k]);
+                acc[h][k][0] = 0;
+                acc[h][k][1] = 0;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            float tot = part[h][k];
+#pragma unroll
+            for (int off = TQ; off < 32; off <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+            lg[h][k] = ((sbits >> k) & 1u) ? -INFINITY : tot * dT[h];
+          }
+      } else {
       float dA[NH], bA[NH];
 #pragma unroll
       for (int h = 0; h < NH; ++h) {      // limbs of Q_c = rn(q~_c s^K_c / delta): lane = channel quad
@@ -554,6 +646,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           const float sc4 = dA[h] * (1.0f / (float)(1 << (2 * k)));
           lg[h][k] = ((sbits >> k) & 1u) ? -INFINITY : fmaf((float)tot, sc4, -bA[h]);
         }
+      }   // per-channel K
     } else if (s.kind == 1) {
       // ================= page V half: softmax update, value accumulation
       mbar_wait(&bar[st], par);

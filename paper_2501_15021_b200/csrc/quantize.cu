@@ -174,6 +174,20 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
     float4 *xk = reinterpret_cast<float4 *>(xs + t * P + cl * CPL);
 #pragma unroll
     for (int i = 0; i < CPL / 4; ++i) xk[i] = make_float4(k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]);
+    if (c.k_axis == AKVQ_K_PER_TOKEN) {   // K per token over G-channel groups (NEXT-1)
+      const int gi = (cl * CPL) / G;
+      float mn = k[0], mx = k[0];
+#pragma unroll
+      for (int i = 1; i < CPL; ++i) { mn = fminf(mn, k[i]); mx = fmaxf(mx, k[i]); }
+      group_minmax<GL>(mn, mx);
+      const QMeta m = q_meta(mn, mx, !sal, c.clip2, 3.f);
+      if ((cl % GL) == 0) {
+        const int mi = t * NG + gi;                  // meta [G][NG], same bytes as [D]
+        s_s[mi] = m.s; s_z[mi] = m.zf; s_mode[mi] = m.mode;
+        reinterpret_cast<float *>(pg + c.pg_kscale)[mi] = sal ? 0.f : __fmul_rn(m.s, c.inv_sqrt_d);
+        reinterpret_cast<int32_t *>(pg + c.pg_kzero)[mi] = sal ? 0 : zero_i32(m.zf);
+      }
+    }
 
     // V: per token over the lane's channel group (Eqs. 3-6, clip2), salient -> 0
     {
@@ -247,7 +261,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
   __syncthreads();
 
   // ---------------- K: per-channel block stats over non-salient tokens (R1)
-  for (int ch = tid; ch < D; ch += kQThreads) {
+  for (int ch = tid; ch < D && c.k_axis == AKVQ_K_PER_CHANNEL; ch += kQThreads) {
     float mn = 0.f, mx = 0.f;
     bool any = false;
     for (int i = 0; i < G; ++i) {
@@ -272,10 +286,11 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int ch = 4 * cq + b;
-        QMeta m; m.s = s_s[ch]; m.zf = s_z[ch]; m.mode = s_mode[ch];
 #pragma unroll
         for (int s2 = 0; s2 < 4; ++s2) {
           const int t = 4 * tq + s2;
+          const int mi = c.k_axis == AKVQ_K_PER_TOKEN ? t * NG + ch / G : ch;
+          QMeta m; m.s = s_s[mi]; m.zf = s_z[mi]; m.mode = s_mode[mi];
           const bool sal = (s_bits[t >> 5] >> (t & 31)) & 1u;
           word |= (sal ? 0u : q_code(xs[t * P + ch], m, 3.f)) << (8 * b + 2 * s2);
         }

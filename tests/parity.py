@@ -60,8 +60,12 @@ class GpuState:
         def pg(off, nbytes, dt):
             return np.ascontiguousarray(pages[:, :, off: off + nbytes]).view(dt)
 
-        self.kscale = pg(y.pg_kscale, 4 * d, np.float32).reshape(U, npg, d)
-        self.kzero = pg(y.pg_kzero, 4 * d, np.int32).reshape(U, npg, d)
+        if getattr(cfg, "k_axis", 0) == 1:    # per-token K meta [G][ng] per page
+            self.kscale = pg(y.pg_kscale, 4 * d, np.float32).reshape(U, npg * G, ng)
+            self.kzero = pg(y.pg_kzero, 4 * d, np.int32).reshape(U, npg * G, ng)
+        else:
+            self.kscale = pg(y.pg_kscale, 4 * d, np.float32).reshape(U, npg, d)
+            self.kzero = pg(y.pg_kzero, 4 * d, np.int32).reshape(U, npg, d)
         self.kcodes = k_tiles_to_rows(pg(y.pg_kcodes, G * d // 4, np.uint8), U, npg, G, d)
         self.vscale = pg(y.pg_vscale, 4 * G * ng, np.float32).reshape(U, npg * G, ng)
         self.vzero = pg(y.pg_vzero, 4 * G * ng, np.int32).reshape(U, npg * G, ng)
@@ -115,15 +119,18 @@ def compare_state(gs: GpuState, ex: dict, cfg, report: dict | None = None, units
         assert np.array_equal(gs.side_idx[u, :cnt], ex["side_index"][ui, :cnt]), f"side idx u{u}"
         if nb == 0:
             continue
-        # K meta per channel per block
-        ks_g, ks_o = gs.kscale[u, :nb], ex["kscale"][ui, :nb]
+        # K meta: per channel per block [nb, d], or per token per group [n_q, ng]
+        kt = getattr(cfg, "k_axis", 0) == 1
+        nm = n_q if kt else nb
+        ks_g, ks_o = gs.kscale[u, :nm], ex["kscale"][ui, :nm]
         assert np.all(np.abs(ks_g - ks_o) <= 1e-6 * np.abs(ks_o) + 1e-30), f"kscale u{u}"
-        kz_g, kz_o = gs.kzero[u, :nb], ex["kzero"][ui, :nb]
+        kz_g, kz_o = gs.kzero[u, :nm], ex["kzero"][ui, :nm]
         kc_g = unpack2(gs.kcodes[u, :n_q]).astype(np.int32)
         kc_o = unpack2(ex["kcodes"][ui, :n_q]).astype(np.int32)
         x = ex["xs_k"][ui, :n_q].astype(np.float64)
-        s32 = np.repeat(ex["kscale32"][ui, :nb].astype(np.float64), G, axis=0)
-        zt = np.repeat(kz_g != kz_o, G, axis=0)
+        ax = 1 if kt else 0          # expand meta to [n_q, d]
+        s32 = np.repeat(ex["kscale32"][ui, :nm].astype(np.float64), G, axis=ax)
+        zt = np.repeat(kz_g != kz_o, G, axis=ax)
         if np.any(kz_g != kz_o):
             # zero-point tie: cmn/scale within TIE_EPS of a half-integer
             rep["zero_ties"] += int((kz_g != kz_o).sum())

@@ -31,25 +31,27 @@ def sy():
     return synth
 
 
-def _configs(ak, orc, w, layer, units_n, kind=None, cap=None):
+def _configs(ak, orc, w, layer, units_n, kind=None, cap=None, k_axis=0):
     kind = w.kind(layer) if kind is None else kind
     dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
     cap = w.capacity if cap is None else cap
-    gcfg = ak.make_config(units_n, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4)
+    gcfg = ak.make_config(units_n, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4,
+                          k_axis)
     ocfg = orc.OracleConfig(units_n, w.g, w.d, w.G, w.R, cap, w.top_k, kind,
-                            orc.BF16 if dt == ak.AKVQ_BF16 else orc.FP16, w.clip2, w.clip4)
+                            orc.BF16 if dt == ak.AKVQ_BF16 else orc.FP16, w.clip2, w.clip4,
+                            k_axis)
     return gcfg, ocfg
 
 
 def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every=1,
-              flags=0, report=None, options=0, fused_step=None):
+              flags=0, report=None, options=0, fused_step=None, k_axis=0):
     """Prefill + `steps` decode steps on the GPU for all units; the oracle runs the
     sampled `units` (default all).  Compares state after prefill and after every
     flush, outputs every `check_every` steps."""
     U = w.U
     us = list(range(U)) if units is None else list(units)
-    gcfg, _ = _configs(ak, orc, w, layer, U, kind)
-    _, ocfg = _configs(ak, orc, w, layer, len(us), kind)
+    gcfg, _ = _configs(ak, orc, w, layer, U, kind, k_axis=k_axis)
+    _, ocfg = _configs(ak, orc, w, layer, len(us), kind, k_axis=k_axis)
     dev = "cuda"
     inp = sy.layer_inputs(w, layer, device=dev)
     lc = ak.LayerCache(gcfg, options=options)
@@ -222,3 +224,30 @@ def test_determinism_and_errors(ak, orc, sy):
     with pytest.raises(ak.AkvqError) as e:
         lc.append(di["k"], di["v"], di["types"])
     assert e.value.status == ak.AKVQ_ECAPACITY
+
+
+# ----------------------------------------------------------------- per-token K (NEXT-1)
+@pytest.mark.parametrize("options", [0, 1], ids=["dp4a-pages", "generic-pages"])
+@pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
+def test_tiny_per_token_k(ak, orc, sy, kind, options):
+    """k_axis = 1: codes, per-token K meta, view and decode vs the oracle,
+    across a flush (tiny: L crosses 104 within 12 steps)."""
+    lc, oc, _ = _run_case(ak, orc, sy, sy.TINY, 0, kind=kind, steps=12, options=options,
+                          k_axis=1)
+    K, V = lc.view()
+    Ko, Vo = oc.view()
+    for a, b in ((K, Ko), (V, Vo)):
+        a = a.double().cpu().numpy()
+        assert np.all(np.abs(a - b) <= 1e-6 * np.maximum(np.abs(b), np.abs(b).max(-1, keepdims=True)) + 1e-7)
+
+
+@pytest.mark.parametrize("layer", [0, 2], ids=["TSA-L0", "PSA-L2"])
+def test_llava7b_per_token_k(ak, orc, sy, layer):
+    _run_case(ak, orc, sy, sy.LLAVA7B, layer, steps=3, units=[0, 13, 31], k_axis=1)
+
+
+@pytest.mark.parametrize("name,layer", [("sweep@b16", 2), ("video13b", 3)])
+def test_full_size_per_token_k_sampled(ak, orc, sy, name, layer):
+    w = sy.get(name)
+    _run_case(ak, orc, sy, w, layer, steps=2, units=[0, w.U // 2, w.U - 1], k_axis=1)
+
