@@ -222,6 +222,8 @@ def main():
     ap.add_argument("--workload", default="sweep@b64")
     ap.add_argument("--impl", default="akvq", choices=["akvq", "reference"])
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
+    ap.add_argument("--k-axis", default="channel", choices=["channel", "token"],
+                    help="K quantization axis: per channel (R1, graded) or per token (P:246)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stream-only", action="store_true",
                     help="profiling: kernels stream their bytes but skip the math (invalid outputs)")
@@ -261,7 +263,8 @@ def main():
     caches, pre_ms, pre_bytes = [], 0.0, 0.0
     for layer in range(n_layers):
         kind = w.kind(layer)
-        cfg = ak.make_config(Ul, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4)
+        cfg = ak.make_config(Ul, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4,
+                             1 if args.k_axis == "token" else 0)
         lc = ak.LayerCache(cfg, device=dev)
         lc.handle.options = ((ak.AKVQ_OPT_STREAM_ONLY if args.stream_only else 0) |
                              (ak.AKVQ_OPT_SKIP_ROWS if args.skip_rows else 0) |
@@ -387,7 +390,7 @@ def main():
     if os.path.exists(tf):
         with open(tf) as fh:
             tj = json.load(fh).get("k_decode_layer", {})
-        if tj.get("workload") == w.name and world == 1:
+        if tj.get("workload") == w.name and world == 1 and args.k_axis == "channel":
             traffic = tj.get("traffic_bytes")
     achieved = dec_bytes / (dec_ms * 1e-3) / 1e9
     tokens_per_s = w.batch / (ms * 1e-3)
@@ -483,6 +486,7 @@ def main():
                        "kv_heads": w.hkv, "head_dim": w.d, "prompt_tokens": w.L0,
                        "group": w.G, "residual": w.R, "top_k": w.top_k,
                        "tsa_layers": list(w.tsa_layers), "kv_bits": 2,
+                       "k_axis": "per-" + args.k_axis,
                        "parallelism": f"units (batch x kv-head) sharded over {world} GPU(s)",
                        "l2": "no flush: per-step working set "
                              f"{sum(bytes_layers[:n_layers]) / 1e9:.2f} GB/rank >> 126 MB L2"},
