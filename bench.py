@@ -302,7 +302,7 @@ def main():
     n_step = [0]
     launches = [0]
 
-    def one_step(q, k, v, types, ev=None):
+    def one_step(q, k, v, types):
         b = n_step[0] % len(gathers)
         if pending[b] is not None:
             pending[b].wait()                     # buffer b's previous gather is done
@@ -310,13 +310,9 @@ def main():
         outs = gathers[b].local_view()
         for layer, lc in enumerate(caches):
             nq = lc.n_q
-            if ev is not None:
-                ev[layer][0].record()
             # append + decode attention through the C ABI (one fused launch when
             # no block flush is due; append + quantize + decode when it is)
             lc.step(k[layer], v[layer], q[layer], types, out=outs[layer])
-            if ev is not None:
-                ev[layer][1].record()
             launches[0] += lc.last_launches
         if world > 1:
             pending[b] = gathers[b].gather(async_op=True)
@@ -337,8 +333,8 @@ def main():
         dist.barrier()
 
     # ---------------- timed region (device)
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(n_layers)]
-           for _ in range(args.steps)]
+    # one event per step boundary (none between the PDL-chained layer launches)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     L_at = [caches[2 % n_layers].L]
     nq_at = [caches[2 % n_layers].n_q]
     sampler = ClockSampler(local)
@@ -349,8 +345,13 @@ def main():
         dist.barrier()
     with sampler:
         t0.record()
+        evs[0].record()
+        step_launches = []
         for s in range(args.steps):
-            one_step(*inputs[args.warmup + s], ev=evs[s])
+            l0 = launches[0]
+            one_step(*inputs[args.warmup + s])
+            evs[s + 1].record()
+            step_launches.append(launches[0] - l0)
             L_at.append(caches[2 % n_layers].L)
             nq_at.append(caches[2 % n_layers].n_q)
         drain()
@@ -360,8 +361,14 @@ def main():
         dist.barrier()
     n_launch = launches[0]
     ms = t0.elapsed_time(t1) / args.steps
-    dec_ms = sum(evs[s][l][0].elapsed_time(evs[s][l][1]) for s in range(args.steps)
-                 for l in range(n_layers)) / (args.steps * n_layers)
+    # mean k_decode_layer launch duration: steps whose launches are exactly the
+    # n_layers decode launches (no block flush) -> step time / n_layers (includes
+    # the inter-launch gaps, so it is a conservative per-launch time)
+    plain = [s for s in range(args.steps) if step_launches[s] == n_layers]
+    if world == 1 and plain:
+        dec_ms = sum(evs[s].elapsed_time(evs[s + 1]) for s in plain) / (len(plain) * n_layers)
+    else:
+        dec_ms = ms / n_layers
     if dist:
         t = torch.tensor([ms, dec_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -406,48 +413,48 @@ def main():
     dv = torch.empty_like(inputs[0][2]); dty = torch.empty_like(inputs[0][3])
     h2d = sum(t.numel() * t.element_size() for t in host_in[0])
     d2h = host_out.numel() * host_out.element_size()
-    # Per-layer pipelining (world == 1): inputs of layer l are copied host->device
-    # on an H2D stream (double-buffered across steps), layer l's step waits only
-    # for its own inputs, and its outputs go device->host on a D2H stream right
-    # after it, so the copies overlap the attention of the other layers.
+    # Step-level pipelining (world == 1): step s+1's inputs are copied host->device
+    # on an H2D stream while step s computes (double-buffered), and step s's
+    # outputs go device->host on a D2H stream while step s+1 computes.  Events
+    # only at step boundaries, so the layer launches stay PDL-chained.
     h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     main_s = torch.cuda.current_stream()
     dbufs = [tuple(torch.empty_like(t) for t in inputs[0]) for _ in range(2)]
     obufs = [torch.empty((n_layers, Ul, w.g, w.d), dtype=torch.float32, device=dev) for _ in range(2)]
-    ev_in = [[torch.cuda.Event() for _ in range(n_layers)] for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_used = [torch.cuda.Event() for _ in range(2)]
-    ev_out = [[torch.cuda.Event() for _ in range(n_layers)] for _ in range(2)]
     ev_read = [torch.cuda.Event() for _ in range(2)]
+
+    def prefetch_inputs(s):
+        b = s % 2
+        h2d_s.wait_event(ev_used[b])                   # buffer b no longer read by step s-2
+        with torch.cuda.stream(h2d_s):
+            for dst, src in zip(dbufs[b], host_in[s]):
+                dst.copy_(src, non_blocking=True)
+            ev_in[b].record(h2d_s)
 
     def e2e_step_pipelined(s):
         b = s % 2
         dq, dk, dv, dty = dbufs[b]
-        hq, hk, hv, hty = host_in[s]
-        h2d_s.wait_event(ev_used[b])                   # buffer b no longer read by step s-2
-        with torch.cuda.stream(h2d_s):
-            dty.copy_(hty, non_blocking=True)
-            for l in range(n_layers):
-                dq[l].copy_(hq[l], non_blocking=True)
-                dk[l].copy_(hk[l], non_blocking=True)
-                dv[l].copy_(hv[l], non_blocking=True)
-                ev_in[b][l].record(h2d_s)
+        if s + 1 < e2e_steps:
+            prefetch_inputs(s + 1)                     # the next step's inputs
+        main_s.wait_event(ev_in[b])
         main_s.wait_event(ev_read[b])                  # obufs[b] copied out (step s-2)
         for l, lc in enumerate(caches):
-            main_s.wait_event(ev_in[b][l])
             lc.step(dk[l], dv[l], dq[l], dty, out=obufs[b][l])
-            launches[0] += lc.last_launches
-            ev_out[b][l].record(main_s)
-            d2h_s.wait_event(ev_out[b][l])
-            with torch.cuda.stream(d2h_s):
-                host_out[l].copy_(obufs[b][l], non_blocking=True)
         ev_used[b].record(main_s)
-        ev_read[b].record(d2h_s)
+        d2h_s.wait_event(ev_used[b])
+        with torch.cuda.stream(d2h_s):
+            host_out.copy_(obufs[b], non_blocking=True)
+            ev_read[b].record(d2h_s)
 
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    if world == 1:
+        prefetch_inputs(0)
     for s in range(e2e_steps):
         if world == 1:
             e2e_step_pipelined(s)
