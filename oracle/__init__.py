@@ -102,6 +102,17 @@ def nthreads() -> int:
 
 
 # ---------------------------------------------------------------- primitives
+def detect_pivots(residual, dtype16: int, tau: float = 50.0, n_max: int = 15) -> np.ndarray:
+    """Massive-activation pivots of one residual stream [L0, hidden] (uint16 bits)."""
+    r = np.ascontiguousarray(residual, np.uint16)
+    out = np.zeros(max(n_max, 1), np.int32)
+    L = lib()
+    L.orc_detect_pivots.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_float, C.c_int,
+                                    C.c_void_p]
+    n = L.orc_detect_pivots(r.shape[0], r.shape[1], _p(r), dtype16, float(tau), n_max, _p(out))
+    return out[:n]
+
+
 def hadamard(d: int, normalized: bool = True) -> np.ndarray:
     H = np.zeros((d, d), np.float64)
     if lib().orc_hadamard(d, int(normalized), _p(H)) != 0:
@@ -220,6 +231,15 @@ class OracleCache:
         ty = None if types is None else np.ascontiguousarray(types, np.uint8)
         cs = None if colsum is None else np.ascontiguousarray(colsum, np.float32)
         return lib().orc_prefill(self._h, _p(K16), _p(V16), K16.shape[1], _p(ty), _p(cs))
+
+    def prefill_pivots(self, K16, V16, pivot_mask) -> int:
+        """PSA prefill with an explicit pivot mask [U, L0] (NEXT-2)."""
+        K16 = np.ascontiguousarray(K16, np.uint16)
+        V16 = np.ascontiguousarray(V16, np.uint16)
+        m = np.ascontiguousarray(pivot_mask, np.uint8)
+        lib().orc_prefill_pivots.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                             C.c_void_p]
+        return lib().orc_prefill_pivots(self._h, _p(K16), _p(V16), K16.shape[1], _p(m))
 
     def append(self, k16, v16, types=None) -> int:
         k16 = np.ascontiguousarray(k16, np.uint16)

@@ -234,6 +234,54 @@ void orc_select_salient(int kind, int g, int L0, int top_k,
 }
 
 /* ------------------------------------------------------------------ */
+/* Massive-activation pivot detection (SPEC S:317-321,        */
+/* SURVEY NEXT-2) for one residual stream [L0][hidden] (16-bit):         */
+/*   score(t) = max_c |residual[t][c]|            (exact, stored fp32)   */
+/*   m = median over tokens of score: the middle value for odd L0, the   */
+/*       fp32 mean (a + b) * 0.5 of the two middle values for even L0    */
+/*       (R22)                                                 */
+/*   pivots = tokens with score > tau * m (fp32 product, R6), ordered by */
+/*       (score desc, index asc), truncated to n_max; none -> [0].       */
+static int cmp_float_asc(const void *a, const void *b) {
+  const float x = *(const float *)a, y = *(const float *)b;
+  return (x > y) - (x < y);
+}
+int orc_detect_pivots(int L0, int hidden, const uint16_t *residual, int dtype16, float tau,
+                      int n_max, int32_t *out) {
+  if (L0 <= 0 || hidden <= 0 || n_max <= 0) return 0;
+  float *score = (float *)malloc(sizeof(float) * L0);
+  float *sorted = (float *)malloc(sizeof(float) * L0);
+  int *order = (int *)malloc(sizeof(int) * L0);
+  for (int t = 0; t < L0; ++t) {
+    double mx = 0.0;
+    for (int c = 0; c < hidden; ++c) {
+      const double a = fabs(orc_half_to_double(residual[(long)t * hidden + c], dtype16));
+      if (a > mx) mx = a;
+    }
+    score[t] = (float)mx;                 /* exact: |16-bit| fits fp32 */
+    sorted[t] = score[t];
+  }
+  qsort(sorted, (size_t)L0, sizeof(float), cmp_float_asc);
+  const float m = (L0 & 1) ? sorted[L0 / 2] : (sorted[L0 / 2 - 1] + sorted[L0 / 2]) * 0.5f;
+  const float thr = tau * m;
+  int n = 0;
+  for (int t = 0; t < L0; ++t)
+    if (score[t] > thr) order[n++] = t;
+#ifdef _OPENMP
+#pragma omp critical(orc_sort)
+#endif
+  {
+    g_sort_scores = score;
+    qsort(order, (size_t)n, sizeof(int), cmp_desc_score_asc_idx);
+  }
+  if (n > n_max) n = n_max;
+  for (int i = 0; i < n; ++i) out[i] = order[i];
+  if (n == 0) { out[0] = 0; n = 1; }      /* attention-sink fallback */
+  free(score); free(sorted); free(order);
+  return n;
+}
+
+/* ------------------------------------------------------------------ */
 static long ROW(const orc_cache *c, int u, int t) {
   return ((long)u * c->cap + t) * c->cfg.d;
 }
@@ -383,14 +431,23 @@ static void quantize_block(orc_cache *c, int u, int j) {
 
 /* Prefill: store rows, select salient tokens,     */
 /* quantize blocks [0, n_q) with n_q = G floor(max(0, L0 - R)/G) (R9).    */
-int orc_prefill(orc_cache *c, const uint16_t *K, const uint16_t *V, int L0,
-                const uint8_t *types, const float *colsum) {
+/* mask != NULL (PSA with explicit pivots, NEXT-2): salient = mask[u][t]. */
+static int prefill_impl(orc_cache *c, const uint16_t *K, const uint16_t *V, int L0,
+                        const uint8_t *types, const float *colsum, const uint8_t *mask) {
   const orc_config *f = &c->cfg;
   if (c->L != 0) return ORC_ESTATE;
   if (L0 < 0) return ORC_EINVAL;
   if (L0 > f->capacity) return ORC_ECAPACITY;
-  if (f->kind == ORC_PSA && L0 > 0 && !colsum) return ORC_EINVAL;
+  if (f->kind == ORC_PSA && L0 > 0 && !colsum && !mask) return ORC_EINVAL;
   if (f->kind == ORC_TSA && L0 > 0 && !types) return ORC_EINVAL;
+  if (mask) {                                /* at most top_k pivots per unit */
+    if (f->kind != ORC_PSA) return ORC_EINVAL;
+    for (int u = 0; u < f->U; ++u) {
+      int n = 0;
+      for (int t = 0; t < L0; ++t) n += mask[(long)u * L0 + t] != 0;
+      if (n > f->top_k) return ORC_EINVAL;
+    }
+  }
   const int d = f->d;
   const int nq = L0 > f->R ? (L0 - f->R) / f->G * f->G : 0;
 #ifdef _OPENMP
@@ -401,15 +458,28 @@ int orc_prefill(orc_cache *c, const uint16_t *K, const uint16_t *V, int L0,
       memcpy(c->K + ROW(c, u, t), K + ((long)u * L0 + t) * d, (size_t)d * 2);
       memcpy(c->V + ROW(c, u, t), V + ((long)u * L0 + t) * d, (size_t)d * 2);
     }
-    orc_select_salient(f->kind, f->g, L0, f->top_k,
-                       types ? types + (long)u * L0 : NULL,
-                       colsum ? colsum + (long)u * f->g * L0 : NULL,
-                       c->sal + (long)u * c->cap);
+    if (mask) {
+      for (int t = 0; t < L0; ++t) c->sal[(long)u * c->cap + t] = mask[(long)u * L0 + t] != 0;
+    } else {
+      orc_select_salient(f->kind, f->g, L0, f->top_k,
+                         types ? types + (long)u * L0 : NULL,
+                         colsum ? colsum + (long)u * f->g * L0 : NULL,
+                         c->sal + (long)u * c->cap);
+    }
     for (int j = 0; j < nq / f->G; ++j) quantize_block(c, u, j);
   }
   c->L = L0;
   c->nq = nq;
   return ORC_OK;
+}
+
+int orc_prefill(orc_cache *c, const uint16_t *K, const uint16_t *V, int L0,
+                const uint8_t *types, const float *colsum) {
+  return prefill_impl(c, K, V, L0, types, colsum, NULL);
+}
+int orc_prefill_pivots(orc_cache *c, const uint16_t *K, const uint16_t *V, int L0,
+                       const uint8_t *pivot_mask) {
+  return prefill_impl(c, K, V, L0, NULL, NULL, pivot_mask);
 }
 
 /* Append one decode token per unit (Eq. 2).        */

@@ -81,6 +81,14 @@ int  orc_nthreads(void);
 /* K, V [U][L0][d] 16-bit bit patterns; types [U][L0]; colsum [U][g][L0]. */
 int  orc_prefill(orc_cache *c, const uint16_t *K, const uint16_t *V, int L0,
                  const uint8_t *types, const float *colsum);
+/* Massive-activation pivots of one residual stream [L0][hidden] 16-bit
+ * (NEXT-2); writes <= n_max token indices (>= 1), returns
+ * the count. */
+int  orc_detect_pivots(int L0, int hidden, const uint16_t *residual, int dtype16, float tau,
+                       int n_max, int32_t *out);
+/* PSA prefill with an explicit pivot mask [U][L0] (<= top_k per unit). */
+int  orc_prefill_pivots(orc_cache *c, const uint16_t *K, const uint16_t *V, int L0,
+                        const uint8_t *pivot_mask);
 /* k, v [U][d]; types [U] */
 int  orc_append(orc_cache *c, const uint16_t *k, const uint16_t *v,
                 const uint8_t *types);

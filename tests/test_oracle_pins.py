@@ -516,3 +516,86 @@ def test_codes_are_scale_invariant(orc):
         if fr.min() > 1e-4 and frz > 1e-4:
             assert z1 == z2 and np.array_equal(c1, c2)
             assert s2 == pytest.approx(s1 / math.sqrt(128), rel=1e-6)
+
+
+# ----------------------------------------------------------------- NEXT-2 pivots
+def _residual(rng, L0, hidden, inject=()):
+    """|N(0,1)| background with injected massive activations."""
+    x = np.abs(rng.standard_normal((L0, hidden)))
+    for t, mag in inject:
+        x[t, rng.integers(hidden)] = mag
+    return _bf16_bits(x)
+
+
+def test_detect_pivots_spec_examples(orc):
+    """S:321-323: token 7 at 1000x over a unit-Gaussian background (tau 50) -> [7];
+    all tokens identical -> fallback [0]; tokens 3 and 11 at 2000 and 1000 ->
+    [3, 11] in descending-score order."""
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((32, 64))
+    x[7] *= 1000.0
+    assert orc.detect_pivots(_bf16_bits(x), orc.BF16, 50.0, 15).tolist() == [7]
+    same = np.tile(rng.standard_normal((1, 64)), (20, 1))
+    assert orc.detect_pivots(_bf16_bits(same), orc.BF16, 50.0, 15).tolist() == [0]
+    r = _residual(rng, 40, 64, inject=[(11, 1000.0), (3, 2000.0)])
+    assert orc.detect_pivots(r, orc.BF16, 50.0, 15).tolist() == [3, 11]
+    # truncation to n_max keeps the largest
+    assert orc.detect_pivots(r, orc.BF16, 50.0, 1).tolist() == [3]
+
+
+def test_detect_pivots_median_and_invariants(orc):
+    """The threshold is tau x median (numpy's median: the library routine, mean of
+    the two middle values for even L0): a token just above / below it flips;
+    scale invariance (power-of-two scale, exact in bf16); injection
+    recovery for random background."""
+    rng = np.random.default_rng(12)
+    for L0 in (31, 32):                          # odd and even token counts
+        base = np.full((L0, 8), 1.0)
+        base[:, 0] = np.arange(1, L0 + 1, dtype=float)      # score(t) = t + 1
+        med = float(np.median(np.arange(1, L0 + 1, dtype=float)))
+        tau = 2.0
+        # token 25 (above the median, so moving it up keeps the median): exactly
+        # tau * median is not selected (strict >), one above is
+        for val, want in ((tau * med, False), (tau * med + 1.0, True)):
+            x = base.copy()
+            x[25, 3] = val
+            got = orc.detect_pivots(_bf16_bits(x), orc.BF16, tau, 15).tolist()
+            assert got == ([25] if want else [0]), (L0, val, got)
+    for _ in range(20):
+        r = np.abs(rng.standard_normal((50, 32)))
+        t = int(rng.integers(50))
+        r[t, int(rng.integers(32))] = 50.0 * 10 * np.max(r)      # >= tau x 10 (S:347)
+        bits = _bf16_bits(r)
+        got = orc.detect_pivots(bits, orc.BF16, 50.0, 15).tolist()
+        assert t in got
+        r2 = bits.view(np.int16).astype(np.int32)
+        scaled = torch.tensor(r, dtype=torch.float32).to(torch.bfloat16).float().numpy() * 4.0
+        assert orc.detect_pivots(_bf16_bits(scaled), orc.BF16, 50.0, 15).tolist() == got
+        del r2
+
+
+def test_prefill_with_pivot_mask(orc):
+    """A PSA prefill with an explicit pivot mask equals the colsum top-k prefill
+    that selects the same tokens; more pivots than top_k is rejected."""
+    rng = np.random.default_rng(13)
+    U, d, G, L0 = 2, 64, 32, 72
+    K = _bf16_bits(rng.standard_normal((U, L0, d))); V = _bf16_bits(rng.standard_normal((U, L0, d)))
+    piv = [[0, 17, 40], [5, 33]]
+    mask = np.zeros((U, L0), np.uint8)
+    cs = np.zeros((U, 1, L0), np.float32)
+    for u, ps in enumerate(piv):
+        for i, t in enumerate(ps):
+            mask[u, t] = 1
+            cs[u, 0, t] = 10.0 - i
+    cfg = _cfg(orc, U=U, d=d, G=G, R=8, capacity=80, top_k=3, dtype16=orc.BF16)
+    a = orc.OracleCache(cfg); b = orc.OracleCache(cfg)
+    assert a.prefill_pivots(K, V, mask) == 0
+    cs[1, 0, 60] = 0.5                      # unit 1: top-3 = {5, 33, 60}; mask has 2 pivots
+    assert b.prefill(K, V, colsum=cs) == 0
+    ea, eb = a.export(), b.export()
+    assert np.array_equal(ea["salient"][0], eb["salient"][0])
+    assert np.array_equal(ea["kcodes"][0], eb["kcodes"][0])
+    assert ea["salient"][1, :L0].nonzero()[0].tolist() == [5, 33]
+    over = mask.copy(); over[0, 50] = 1; over[0, 51] = 1
+    assert orc.OracleCache(cfg).prefill_pivots(K, V, over) == 1      # EINVAL
+
