@@ -231,6 +231,33 @@ akvq_status akvq_select_salient(akvq_cache *c, const uint8_t *types,
                                 const float *colsum, int32_t L0,
                                 akvq_stream_t stream);
 
+/* ------------------------------------------------------------- NEXT-2 */
+/* Massive-activation pivot detection (SPEC detect_pivot_tokens,
+ * S:317-321; R22) for n_rows residual streams:
+ *   score(t) = max_c |residual[r][t][c]|, m = median over t of score,
+ *   pivots[r] = tokens with score > tau * m, ordered (score desc, index asc),
+ *   at most n_max (1..32); none -> [0] (attention-sink fallback).
+ *   residual  device [n_rows][L0][hidden] 16-bit (dtype16)
+ *   score_ws  device f32 scratch of n_rows * L0 floats
+ *   pivots    device i32 [n_rows][n_max] (entries >= counts[r] untouched)
+ *   counts    device i32 [n_rows] (1..n_max)
+ * Errors: EINVAL (NULL, sizes < 1, tau <= 0, n_max outside 1..32),
+ *         EUNSUPPORTED (L0 > AKVQ_MAX_PSA_PROMPT). */
+akvq_status akvq_detect_pivots(const void *residual, int32_t n_rows, int32_t L0, int32_t hidden,
+                               int32_t dtype16, float tau, int32_t n_max, float *score_ws,
+                               int32_t *pivots, int32_t *counts, akvq_stream_t stream);
+
+/* PSA prefill with explicit pivots (NEXT-2): like akvq_rotate_quantize, but
+ * the salient set of unit u is pivots[u / units_per_row][0 .. counts[...]) (the
+ * pivot set of its batch row, R22) instead of the column-sum top-k.
+ *   pivots, counts  device, as written by akvq_detect_pivots (stride n_max)
+ * Errors: as akvq_rotate_quantize; EINVAL for a TSA cache, NULL pivot
+ * arrays, units_per_row < 1 or n_max > top_k (side capacity). */
+akvq_status akvq_rotate_quantize_pivots(akvq_cache *c, const void *K, const void *V, int32_t L0,
+                                        const int32_t *pivots, const int32_t *counts,
+                                        int32_t n_max, int32_t units_per_row,
+                                        akvq_stream_t stream);
+
 /* dequantized_view: K^, V^ device f32 [U][L][d] in the rotated
  * normalized basis (R5).  Test hook.  Errors: ESTATE (L == 0). */
 akvq_status akvq_dequantize_view(const akvq_cache *c, float *K, float *V,

@@ -32,6 +32,7 @@ EXPORTS = (
     "akvq_append_token", "akvq_decode_workspace_bytes", "akvq_decode_workspace_bytes_max",
     "akvq_decode_attention", "akvq_select_salient", "akvq_dequantize_view",
     "akvq_memory_report", "akvq_status_str", "akvq_version", "akvq_decode_step",
+    "akvq_detect_pivots", "akvq_rotate_quantize_pivots",
 )
 
 
@@ -110,6 +111,12 @@ def lib() -> C.CDLL:
         L.akvq_memory_report.argtypes = [C.POINTER(akvq_cache), C.c_int32,
                                          C.POINTER(akvq_mem_report)]
         L.akvq_memory_report.restype = S
+        L.akvq_detect_pivots.argtypes = [P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                         C.c_float, C.c_int32, P, P, P, P]
+        L.akvq_detect_pivots.restype = S
+        L.akvq_rotate_quantize_pivots.argtypes = [C.POINTER(akvq_cache), P, P, C.c_int32, P, P,
+                                                  C.c_int32, C.c_int32, P]
+        L.akvq_rotate_quantize_pivots.restype = S
         L.akvq_status_str.argtypes = [S]
         L.akvq_status_str.restype = C.c_char_p
         L.akvq_version.argtypes = []
@@ -202,6 +209,27 @@ def akvq_select_salient(cache, types, colsum, L0, stream=None):
                                      _stream(stream)), "akvq_select_salient")
 
 
+def akvq_detect_pivots(residual, dtype16, tau=50.0, n_max=15, stream=None):
+    """residual [rows, L0, hidden] 16-bit CUDA tensor -> (pivots [rows, n_max] i32,
+    counts [rows] i32) device tensors (NEXT-2)."""
+    rows, L0, hidden = residual.shape
+    dev = residual.device
+    ws = torch.empty(rows * L0, dtype=torch.float32, device=dev)
+    piv = torch.full((rows, n_max), -1, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(rows, dtype=torch.int32, device=dev)
+    _check(lib().akvq_detect_pivots(_ptr(residual), rows, L0, hidden, int(dtype16), float(tau),
+                                    int(n_max), _ptr(ws), _ptr(piv), _ptr(cnt), _stream(stream)),
+           "akvq_detect_pivots")
+    return piv, cnt
+
+
+def akvq_rotate_quantize_pivots(cache, K, V, L0, pivots, counts, units_per_row, stream=None):
+    _check(lib().akvq_rotate_quantize_pivots(C.byref(cache), _ptr(K), _ptr(V), int(L0),
+                                             _ptr(pivots), _ptr(counts), int(pivots.shape[1]),
+                                             int(units_per_row), _stream(stream)),
+           "akvq_rotate_quantize_pivots")
+
+
 def akvq_dequantize_view(cache, K, V, stream=None):
     _check(lib().akvq_dequantize_view(C.byref(cache), _ptr(K), _ptr(V), _stream(stream)),
            "akvq_dequantize_view")
@@ -238,6 +266,10 @@ class LayerCache:
 
     def prefill(self, K, V, types=None, colsum=None, stream=None):
         akvq_rotate_quantize(self.handle, K, V, K.shape[1], types, colsum, stream)
+
+    def prefill_pivots(self, K, V, pivots, counts, units_per_row, stream=None):
+        akvq_rotate_quantize_pivots(self.handle, K, V, K.shape[1], pivots, counts,
+                                    units_per_row, stream)
 
     def append(self, k, v, types=None, stream=None):
         akvq_append_token(self.handle, k, v, types, stream)

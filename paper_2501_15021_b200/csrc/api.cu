@@ -260,6 +260,9 @@ akvq_status akvq_select_salient(akvq_cache *c, const uint8_t *types, const float
                                     reinterpret_cast<cudaStream_t>(stream)));
 }
 
+static akvq_status quantize_prompt(akvq_cache *c, const void *K, const void *V, int32_t L0,
+                                   akvq_stream_t stream);
+
 akvq_status akvq_rotate_quantize(akvq_cache *c, const void *K, const void *V, int32_t L0,
                                  const uint8_t *types, const float *colsum,
                                  akvq_stream_t stream) {
@@ -270,6 +273,45 @@ akvq_status akvq_rotate_quantize(akvq_cache *c, const void *K, const void *V, in
   akvq_status st = akvq_select_salient(c, types, colsum, L0, stream);
   if (st != AKVQ_OK) return st;
   c->launches = (c->cfg.kind == AKVQ_TSA || c->cfg.top_k > 0) && L0 > 0 ? 1 : 0;
+  return quantize_prompt(c, K, V, L0, stream);
+}
+
+akvq_status akvq_rotate_quantize_pivots(akvq_cache *c, const void *K, const void *V, int32_t L0,
+                                        const int32_t *pivots, const int32_t *counts,
+                                        int32_t n_max, int32_t units_per_row,
+                                        akvq_stream_t stream) {
+  if (!c || !c->base || L0 < 0 || !pivots || !counts || units_per_row < 1 || n_max < 1)
+    return AKVQ_EINVAL;
+  if (c->cfg.kind != AKVQ_PSA || n_max > c->cfg.top_k) return AKVQ_EINVAL;
+  if (c->L != 0) return AKVQ_ESTATE;
+  if (L0 > c->cfg.capacity) return AKVQ_ECAPACITY;
+  if (L0 > 0 && (!K || !V)) return AKVQ_EINVAL;
+  c->launches = 0;
+  if (L0 > 0) {
+    const DevCache d = make_dev(c);
+    if (launch_salient_from_pivots(d, pivots, counts, n_max, units_per_row, L0,
+                                   reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
+      return AKVQ_ECUDA;
+    c->launches = 1;
+  }
+  return quantize_prompt(c, K, V, L0, stream);
+}
+
+akvq_status akvq_detect_pivots(const void *residual, int32_t n_rows, int32_t L0, int32_t hidden,
+                               int32_t dtype16, float tau, int32_t n_max, float *score_ws,
+                               int32_t *pivots, int32_t *counts, akvq_stream_t stream) {
+  if (!residual || !score_ws || !pivots || !counts || n_rows < 1 || L0 < 1 || hidden < 1 ||
+      !(tau > 0.f) || n_max < 1 || n_max > 32 ||
+      (dtype16 != AKVQ_BF16 && dtype16 != AKVQ_FP16))
+    return AKVQ_EINVAL;
+  if (L0 > AKVQ_MAX_PSA_PROMPT) return AKVQ_EUNSUPPORTED;
+  return cuda_status(launch_pivot_detect(residual, n_rows, L0, hidden, dtype16, tau, n_max,
+                                         score_ws, pivots, counts,
+                                         reinterpret_cast<cudaStream_t>(stream)));
+}
+
+static akvq_status quantize_prompt(akvq_cache *c, const void *K, const void *V, int32_t L0,
+                                   akvq_stream_t stream) {
   const akvq_config &f = c->cfg;
   const int n_q = L0 > f.residual ? (L0 - f.residual) / f.group * f.group : 0;   // R9
   const DevCache d = make_dev(c);

@@ -63,6 +63,12 @@ int layer_warps_per_cta();
 int layer_ctas_per_sm(int g);
 int layer_rows_per_chunk();
 int layer_rows4_per_sub();
+cudaError_t launch_pivot_detect(const void *res, int n_rows, int L0, int hidden, int dtype16,
+                                float tau, int n_max, float *score_ws, int32_t *pivots,
+                                int32_t *counts, cudaStream_t st);
+cudaError_t launch_salient_from_pivots(const DevCache &c, const int32_t *pivots,
+                                       const int32_t *counts, int n_max, int units_per_row,
+                                       int L0, cudaStream_t st);
 cudaError_t launch_view(const DevCache &c, int dtype16, int L, int n_q, float *K, float *V,
                         cudaStream_t st);
 

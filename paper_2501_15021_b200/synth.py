@@ -51,6 +51,7 @@ class Workload:
     seed: int = 0
     clip2: float = 0.8
     clip4: float = 1.0
+    hidden: int = 4096                      # residual-stream width (NEXT-2 inputs)
 
     @property
     def g(self) -> int:
@@ -86,7 +87,7 @@ def _run(*parts):
 # BJ:7 tiny: [16 T][64 V][16 T], fp16, 4 MHA heads, d 64, G 32, top-4, R 8.
 TINY = Workload("tiny", 1, 1, 4, 4, 64, 32, 8, 4, "fp16",
                 _run((TEXT, 16), (VISION, 64), (TEXT, 16)), (), 2, 20.0,
-                fixed_outlier_ch=(3, 17), pivots_fixed=(0, 40), decode_steps=16)
+                fixed_outlier_ch=(3, 17), pivots_fixed=(0, 40), decode_steps=16, hidden=256)
 # BJ:8 LLaVA-1.5-7B: 32 L, 32 MHA heads, d 128, [35 T][576 V][60 T] = 671.
 LLAVA7B = Workload("llava7b", 32, 1, 32, 32, 128, 128, 32, 15, "bf16",
                    _run((TEXT, 35), (VISION, 576), (TEXT, 60)), (0, 1), 4, 15.0,
@@ -98,11 +99,11 @@ SWEEP = Workload("sweep", 32, 64, 32, 32, 128, 128, 32, 15, "bf16",
 # BJ:10 LLaVA-13B video: 40 L, 40 heads, batch 8, [35 T]([576 V][5 T])x8[125 T].
 VIDEO13B = Workload("video13b", 40, 8, 40, 40, 128, 128, 64, 15, "bf16",
                     _run((TEXT, 35), *((VISION, 576), (TEXT, 5)) * 8, (TEXT, 125)),
-                    (0, 1), 4, 15.0, pivots_per_frame=True, decode_steps=128)
+                    (0, 1), 4, 15.0, pivots_per_frame=True, decode_steps=128, hidden=5120)
 # BJ:11 Qwen2-VL-like GQA: 28 L, 28/4 heads, batch 16, [68 T]([600 V][54 T])x50.
 QWEN = Workload("qwen_gqa", 28, 16, 28, 4, 128, 128, 128, 8, "bf16",
                 _run((TEXT, 68), *((VISION, 600), (TEXT, 54)) * 50), (0, 1), 4, 20.0,
-                pivots_random_vision=7, decode_steps=64)
+                pivots_random_vision=7, decode_steps=64, hidden=3584)
 
 WORKLOADS = {w.name: w for w in (TINY, LLAVA7B, SWEEP, VIDEO13B, QWEN)}
 
@@ -131,7 +132,7 @@ def _key(*parts: int) -> int:
     return k
 
 
-_KIND = {"K": 1, "V": 2, "q": 3, "k": 4, "v": 5, "attn": 6, "ch": 7, "piv": 8}
+_KIND = {"K": 1, "V": 2, "q": 3, "k": 4, "v": 5, "attn": 6, "ch": 7, "piv": 8, "res": 9}
 
 
 def _uniform_bits(keys: torch.Tensor, n: int, device) -> torch.Tensor:
@@ -253,3 +254,28 @@ def decode_inputs(w: Workload, layer: int, step: int,
 def to_u16(t: torch.Tensor):
     """16-bit torch tensor -> numpy uint16 bit patterns (for the oracle)."""
     return t.detach().cpu().contiguous().view(torch.int16).numpy().view("uint16")
+
+
+def residual_inputs(w: Workload, rows: Optional[Sequence[int]] = None, device="cpu",
+                    magnitude: float = 1000.0) -> torch.Tensor:
+    """Residual stream [n_rows, L0, hidden] (16-bit) of the batch rows (NEXT-2).
+
+    Background N(0,1); at each planted pivot of the row (pivot_positions) two
+    fixed channels carry a massive activation (Sun et al., cited at P:209) of
+    +-magnitude * (1 - 0.05 i) for the i-th pivot, so the expected pivot order
+    is the planted order.  The same pivots drive colsum in layer_inputs.
+    """
+    rows = list(range(w.batch)) if rows is None else list(rows)
+    n, L0, hd = len(rows), w.L0, w.hidden
+    keys = _unit_keys(w, 0, rows, "res", 0, device)
+    x = normal(keys, L0 * hd, device).view(n, L0, hd)
+    ck = torch.tensor([_key(w.seed, _KIND["res"], 1)], dtype=torch.int64)
+    h = _uniform_bits(ck, 2, "cpu")[0].tolist()
+    chans = [int(h[0]) % hd, (int(h[0]) % hd + 1 + int(h[1]) % (hd - 1)) % hd]
+    for i, b in enumerate(rows):
+        for j, p in enumerate(pivot_positions(w, b)):
+            m = magnitude * (1.0 - 0.05 * j)
+            x[i, p, chans[0]] = m
+            x[i, p, chans[1]] = -m
+    return _round16(x, w)
+

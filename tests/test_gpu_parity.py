@@ -251,3 +251,74 @@ def test_full_size_per_token_k_sampled(ak, orc, sy, name, layer):
     w = sy.get(name)
     _run_case(ak, orc, sy, w, layer, steps=2, units=[0, w.U // 2, w.U - 1], k_axis=1)
 
+
+
+# ----------------------------------------------------------------- NEXT-2 pivots
+@pytest.mark.parametrize("name", ["tiny", "llava7b", "sweep@b16", "video13b"])
+def test_detect_pivots_parity(ak, orc, sy, name):
+    """Massive-activation pivots (R22): GPU lists == oracle lists per
+    batch row, bit for bit, and the planted pivots are recovered in order."""
+    w = sy.get(name)
+    dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
+    res = sy.residual_inputs(w, device="cuda")
+    n_max = w.top_k
+    piv, cnt = ak.akvq_detect_pivots(res, dt, 50.0, n_max)
+    piv, cnt = piv.cpu().numpy(), cnt.cpu().numpy()
+    od = orc.BF16 if dt == ak.AKVQ_BF16 else orc.FP16
+    rows = sorted({0, w.batch // 2, w.batch - 1})
+    for b in rows:
+        ref = orc.detect_pivots(f16_bits(res[b]), od, 50.0, n_max)
+        assert piv[b, :cnt[b]].tolist() == ref.tolist(), f"row {b}"
+        assert ref.tolist()[: len(sy.pivot_positions(w, b))] == sy.pivot_positions(w, b)[:n_max]
+
+
+def test_detect_pivots_fallback_and_errors(ak, orc):
+    """No token above tau x median -> [0]; even and odd token counts; errors."""
+    g = torch.Generator().manual_seed(5)
+    for L0 in (33, 64):
+        row = torch.randn(1, 1, 128, generator=g).to(torch.bfloat16)
+        res = row.expand(2, L0, 128).contiguous().cuda()
+        piv, cnt = ak.akvq_detect_pivots(res, ak.AKVQ_BF16, 50.0, 4)
+        assert cnt.tolist() == [1, 1] and piv[:, 0].tolist() == [0, 0]
+        noisy = torch.randn(2, L0, 128, generator=g).to(torch.bfloat16)
+        noisy[1, L0 - 1, 7] = 900.0
+        p2, c2 = ak.akvq_detect_pivots(noisy.cuda(), ak.AKVQ_BF16, 2.0, 8)
+        for b in range(2):
+            ref = orc.detect_pivots(f16_bits(noisy[b]), orc.BF16, 2.0, 8)
+            assert p2[b, :int(c2[b])].tolist() == ref.tolist()
+    with pytest.raises(ak.AkvqError):
+        ak.akvq_detect_pivots(torch.zeros(1, 4, 8, dtype=torch.bfloat16, device="cuda"),
+                              ak.AKVQ_BF16, 50.0, 33)
+
+
+@pytest.mark.parametrize("name,layer", [("tiny", 0), ("llava7b", 2), ("sweep@b16", 2)])
+def test_prefill_with_detected_pivots(ak, orc, sy, name, layer):
+    """PSA prefill from the detected pivots (NEXT-2): cache state and decode
+    outputs vs the oracle prefilled with the same pivot mask."""
+    w = sy.get(name)
+    dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
+    us = sorted({0, w.U // 2, w.U - 1})
+    gcfg, _ = _configs(ak, orc, w, layer, w.U, kind=1)
+    _, ocfg = _configs(ak, orc, w, layer, len(us), kind=1)
+    res = sy.residual_inputs(w, device="cuda")
+    piv, cnt = ak.akvq_detect_pivots(res, dt, 50.0, w.top_k)
+    inp = sy.layer_inputs(w, layer, device="cuda")
+    lc = ak.LayerCache(gcfg)
+    lc.prefill_pivots(inp["K"], inp["V"], piv, cnt, w.hkv)
+    mask = np.zeros((len(us), w.L0), np.uint8)
+    pc, cc = piv.cpu().numpy(), cnt.cpu().numpy()
+    for i, u in enumerate(us):
+        b = u // w.hkv
+        mask[i, pc[b, :cc[b]]] = 1
+    oc = orc.OracleCache(ocfg)
+    inp_o = sy.layer_inputs(w, layer, units=us, device="cpu")
+    assert oc.prefill_pivots(f16_bits(inp_o["K"]), f16_bits(inp_o["V"]), mask) == 0
+    compare_state(GpuState(lc), oc.export(), gcfg, None, units=us)
+    for step in range(3):
+        di = sy.decode_inputs(w, layer, step, device="cuda")
+        out = lc.step(di["k"], di["v"], di["q"], di["types"])
+        do = sy.decode_inputs(w, layer, step, units=us, device="cpu")
+        oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
+        ref = oc.decode(f16_bits(do["q"]))
+        err = np.abs(out[us].double().cpu().numpy() - ref).max()
+        assert err <= OUT_TOL, f"step {step}: {err}"
