@@ -222,6 +222,9 @@ def main():
     ap.add_argument("--workload", default="sweep@b64")
     ap.add_argument("--impl", default="akvq", choices=["akvq", "reference"])
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
+    ap.add_argument("--pivots", default="colsum", choices=["colsum", "massive"],
+                    help="PSA saliency: column-sum top-k (BJ:5, graded) or massive-activation "
+                         "pivots from a synthetic residual stream (P:209-213, NEXT-2)")
     ap.add_argument("--k-axis", default="channel", choices=["channel", "token"],
                     help="K quantization axis: per channel (R1, graded) or per token (P:246)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -261,6 +264,22 @@ def main():
 
     # ---------------- prefill every layer (timed separately)
     caches, pre_ms, pre_bytes = [], 0.0, 0.0
+    piv = None
+    if args.pivots == "massive":      # one pivot set per batch row, for every PSA layer (R22)
+        rows = sorted({u // w.hkv for u in units})
+        res = synth.residual_inputs(w, rows=rows, device=dev)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        piv, cnt = ak.akvq_detect_pivots(res, dt, 50.0, w.top_k)
+        e1.record()
+        torch.cuda.synchronize()
+        pre_ms += e0.elapsed_time(e1)
+        pre_bytes += res.numel() * res.element_size()
+        del res
+        # per local unit (its batch row's list), so any unit slicing works
+        sel = torch.tensor([u // w.hkv - rows[0] for u in units], device=dev)
+        piv, cnt = piv.index_select(0, sel).contiguous(), cnt.index_select(0, sel).contiguous()
     for layer in range(n_layers):
         kind = w.kind(layer)
         cfg = ak.make_config(Ul, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4,
@@ -273,7 +292,10 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
+        if piv is not None and kind == 1:
+            lc.prefill_pivots(inp["K"], inp["V"], piv, cnt, 1)
+        else:
+            lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
         e1.record()
         torch.cuda.synchronize()
         pre_ms += e0.elapsed_time(e1)
@@ -493,7 +515,7 @@ def main():
                        "kv_heads": w.hkv, "head_dim": w.d, "prompt_tokens": w.L0,
                        "group": w.G, "residual": w.R, "top_k": w.top_k,
                        "tsa_layers": list(w.tsa_layers), "kv_bits": 2,
-                       "k_axis": "per-" + args.k_axis,
+                       "k_axis": "per-" + args.k_axis, "pivots": args.pivots,
                        "parallelism": f"units (batch x kv-head) sharded over {world} GPU(s)",
                        "l2": "no flush: per-step working set "
                              f"{sum(bytes_layers[:n_layers]) / 1e9:.2f} GB/rank >> 126 MB L2"},
