@@ -122,7 +122,7 @@ __device__ __forceinline__ void group_minmax(float &mn, float &mx) {
   }
 }
 
-template <int D, int G, int DT>
+template <int D, int G, int DT, bool KT>
 __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, QuantSrc src, int block0,
                                                                int last_block) {
   constexpr int CPL = D / 8;                 // channels per lane
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
   constexpr int NG = D / G;
   constexpr int NW = kQThreads / 32;
   extern __shared__ __align__(16) float xs[];     // [G][P] rotated K rows
-  __shared__ float s_s[D], s_z[D];
+  __shared__ float s_s[D], s_z[D], s_rs[D];
   __shared__ int s_mode[D];
   __shared__ uint32_t s_bits[G / 32];
   __shared__ __align__(16) uint8_t vb8[G * D / 4];   // V S:146 bytes per token
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
     float4 *xk = reinterpret_cast<float4 *>(xs + t * P + cl * CPL);
 #pragma unroll
     for (int i = 0; i < CPL / 4; ++i) xk[i] = make_float4(k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]);
-    if (c.k_axis == AKVQ_K_PER_TOKEN) {   // K per token over G-channel groups (NEXT-1)
+    if constexpr (KT) {                   // K per token over G-channel groups (NEXT-1)
       const int gi = (cl * CPL) / G;
       float mn = k[0], mx = k[0];
 #pragma unroll
@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
       if ((cl % GL) == 0) {
         const int mi = t * NG + gi;                  // meta [G][NG], same bytes as [D]
         s_s[mi] = m.s; s_z[mi] = m.zf; s_mode[mi] = m.mode;
+        s_rs[mi] = m.mode == 0 ? __frcp_rn(m.s) : 0.f;
         reinterpret_cast<float *>(pg + c.pg_kscale)[mi] = sal ? 0.f : __fmul_rn(m.s, c.inv_sqrt_d);
         reinterpret_cast<int32_t *>(pg + c.pg_kzero)[mi] = sal ? 0 : zero_i32(m.zf);
       }
@@ -203,8 +204,9 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
       }
       static_assert(CPL == 8 || CPL == 16, "channels per lane");
       uint32_t w = 0;                         // the lane's CPL/4 S:146 bytes
+      const float rs = m.mode == 0 ? __frcp_rn(m.s) : 0.f;
 #pragma unroll
-      for (int i = 0; i < CPL; ++i) w |= (sal ? 0u : q_code(v[i], m, 3.f)) << (2 * i);
+      for (int i = 0; i < CPL; ++i) w |= (sal ? 0u : q_code_fast(v[i], m, rs, 3.f)) << (2 * i);
       if constexpr (CPL == 16) *reinterpret_cast<uint32_t *>(vb8 + t * (D / 4) + cl * 4) = w;
       else *reinterpret_cast<uint16_t *>(vb8 + t * (D / 4) + cl * 2) = (uint16_t)w;
     }
@@ -260,20 +262,36 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
   }
   __syncthreads();
 
-  // ---------------- K: per-channel block stats over non-salient tokens (R1)
-  for (int ch = tid; ch < D && c.k_axis == AKVQ_K_PER_CHANNEL; ch += kQThreads) {
-    float mn = 0.f, mx = 0.f;
-    bool any = false;
-    for (int i = 0; i < G; ++i) {
+  // ---------------- K: per-channel block stats over non-salient tokens (R1);
+  // NS threads per channel each scan G/NS rows, then one combines (min / max
+  // are order-independent, so the result is exact)
+  if constexpr (!KT) {
+    constexpr int NS = kQThreads / D;
+    float *red_mn = xs + G * P;                      // [NS][D] after the K rows
+    float *red_mx = red_mn + NS * D;
+    const int ch = tid % D, part = tid / D;
+    float mn = INFINITY, mx = -INFINITY;
+    for (int i = part * (G / NS); i < (part + 1) * (G / NS); ++i) {
       if ((s_bits[i >> 5] >> (i & 31)) & 1u) continue;
       const float x = xs[i * P + ch];
-      if (!any) { mn = x; mx = x; any = true; }
-      else { mn = fminf(mn, x); mx = fmaxf(mx, x); }
+      mn = fminf(mn, x);
+      mx = fmaxf(mx, x);
     }
-    const QMeta m = q_meta(mn, mx, any, c.clip2, 3.f);
-    s_s[ch] = m.s; s_z[ch] = m.zf; s_mode[ch] = m.mode;
-    reinterpret_cast<float *>(pg + c.pg_kscale)[ch] = __fmul_rn(m.s, c.inv_sqrt_d);
-    reinterpret_cast<int32_t *>(pg + c.pg_kzero)[ch] = zero_i32(m.zf);
+    red_mn[part * D + ch] = mn;
+    red_mx[part * D + ch] = mx;
+    __syncthreads();
+    if (tid < D) {
+      for (int p2 = 1; p2 < NS; ++p2) {
+        mn = fminf(mn, red_mn[p2 * D + ch]);
+        mx = fmaxf(mx, red_mx[p2 * D + ch]);
+      }
+      const bool any = mn <= mx;                     // some non-salient token seen
+      const QMeta m = q_meta(any ? mn : 0.f, any ? mx : 0.f, any, c.clip2, 3.f);
+      s_s[ch] = m.s; s_z[ch] = m.zf; s_mode[ch] = m.mode;
+      s_rs[ch] = m.mode == 0 ? __frcp_rn(m.s) : 0.f;
+      reinterpret_cast<float *>(pg + c.pg_kscale)[ch] = __fmul_rn(m.s, c.inv_sqrt_d);
+      reinterpret_cast<int32_t *>(pg + c.pg_kzero)[ch] = zero_i32(m.zf);
+    }
   }
   __syncthreads();
   // ---------------- code words in the page's 4x4 tile layout
@@ -286,13 +304,20 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int ch = 4 * cq + b;
+        QMeta mc;                                    // per-channel meta, hoisted
+        float rc = 0.f;
+        if constexpr (!KT) { mc.s = s_s[ch]; mc.zf = s_z[ch]; mc.mode = s_mode[ch]; rc = s_rs[ch]; }
 #pragma unroll
         for (int s2 = 0; s2 < 4; ++s2) {
           const int t = 4 * tq + s2;
-          const int mi = c.k_axis == AKVQ_K_PER_TOKEN ? t * NG + ch / G : ch;
-          QMeta m; m.s = s_s[mi]; m.zf = s_z[mi]; m.mode = s_mode[mi];
+          QMeta m = mc;
+          float r = rc;
+          if constexpr (KT) {
+            const int mi = t * NG + ch / G;
+            m.s = s_s[mi]; m.zf = s_z[mi]; m.mode = s_mode[mi]; r = s_rs[mi];
+          }
           const bool sal = (s_bits[t >> 5] >> (t & 31)) & 1u;
-          word |= (sal ? 0u : q_code(xs[t * P + ch], m, 3.f)) << (8 * b + 2 * s2);
+          word |= (sal ? 0u : q_code_fast(xs[t * P + ch], m, r, 3.f)) << (8 * b + 2 * s2);
         }
       }
       dk[wi] = word;
@@ -367,8 +392,9 @@ cudaError_t launch_salient(const DevCache &c, const uint8_t *types, const float 
 template <int D, int G, int DT>
 static cudaError_t launch_q(const DevCache &c, const QuantSrc &src, int block0, int nblocks,
                             int last_block, cudaStream_t st) {
-  const size_t smem = (size_t)G * (D + 4) * sizeof(float);
-  auto kern = k_quantize_blocks<D, G, DT>;
+  const size_t smem = ((size_t)G * (D + 4) + 2 * (size_t)kQThreads) * sizeof(float);
+  auto kern = c.k_axis == AKVQ_K_PER_TOKEN ? k_quantize_blocks<D, G, DT, true>
+                                           : k_quantize_blocks<D, G, DT, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(nblocks, c.U);
   kern<<<grid, kQThreads, smem, st>>>(c, src, block0, last_block);
