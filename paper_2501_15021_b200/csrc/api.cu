@@ -139,8 +139,9 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
       }
       while (r < NR) lp.tab[k++] = row_item(r++);
     }
+    lp.hg = layer_head_groups(f.q_per_kv);
     if (p.fast && lp.per_u > 0) {
-      const long long T = (long long)f.n_units * lp.per_u;
+      const long long T = (long long)f.n_units * lp.hg * lp.per_u;
       const int ctas = pg_ctas_override() > 0 ? pg_ctas_override() : layer_ctas_per_sm(f.q_per_kv);
       const long long wmax = (long long)sms * ctas * layer_warps_per_cta();
       lp.T = (int)T;
@@ -161,7 +162,10 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
 
 size_t ws_bytes_for(const akvq_cache *c, const DecodePlan &p) {
   const size_t g = c->cfg.q_per_kv, d = c->cfg.head_dim;
-  if (p.fast) return (size_t)p.lp.W * p.lp.maxseg * g * (2 * d + 4) * sizeof(float);
+  if (p.fast) {   // NH heads per record: g for g <= 2, 4 for head groups
+    const size_t nh = g <= 2 ? g : 4;
+    return (size_t)p.lp.W * p.lp.maxseg * nh * (2 * d + 4) * sizeof(float);
+  }
   return (size_t)c->cfg.n_units * p.S * g * (d + 2) * sizeof(float);
 }
 
@@ -209,7 +213,7 @@ akvq_status akvq_cache_layout(const akvq_config *f, akvq_layout *y) {
   y->side_cnt_off = t; t = align_up(t + U * 4, 256);
   y->side_entry_bytes = f->kind == AKVQ_PSA ? 4 * d : align_up(d + 16 * ng, 16);
   y->side_off = t;     t = align_up(t + U * y->side_cap * y->side_entry_bytes, 256);
-  y->ticket_off = t;   t = align_up(t + U * 4, 256);
+  y->ticket_off = t;   t = align_up(t + U * 4 * 4, 256);   // per virtual unit (<= 4 head groups)
   y->total_bytes = t;
   return AKVQ_OK;
 }
@@ -238,7 +242,7 @@ akvq_status akvq_cache_init(akvq_cache *c, const akvq_config *f, void *dev_buf, 
   uint8_t *b = static_cast<uint8_t *>(dev_buf);
   cudaMemsetAsync(b + y.bitmask_off, 0, (size_t)f->n_units * y.bitmask_words * 4, s);
   cudaMemsetAsync(b + y.side_cnt_off, 0, (size_t)f->n_units * 4, s);
-  cudaMemsetAsync(b + y.ticket_off, 0, (size_t)f->n_units * 4, s);
+  cudaMemsetAsync(b + y.ticket_off, 0, (size_t)f->n_units * 4 * 4, s);
   if (y.side_cap > 0)
     cudaMemsetAsync(b + y.side_idx_off, 0xff, (size_t)f->n_units * y.side_cap * 4, s);
   return cuda_status(cudaGetLastError());

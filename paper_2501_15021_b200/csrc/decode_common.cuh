@@ -96,7 +96,7 @@ __device__ __forceinline__ void seg_range(int T, int W, int per, int u, int &w_l
 // fetches segment j's (m, l) so the loads overlap.
 template <int D, int NH>
 __device__ __noinline__ void merge_layer_unit(const DevCache &c, const LayerPlan &lp, const float *part, int u,
-                                 float *out, uint32_t flags, int lane) {
+                                 float *out_u, int nh, uint32_t flags, int lane) {
   constexpr int CPL = D / 32;
   int w0, w1;
   seg_range(lp.T, lp.W, lp.per_u, u, w0, w1);
@@ -109,6 +109,7 @@ __device__ __noinline__ void merge_layer_unit(const DevCache &c, const LayerPlan
   };
 #pragma unroll
   for (int h = 0; h < NH; ++h) {
+    if (h >= nh) break;                            // padded head of the last GQA group
     float M = -INFINITY;
     for (int b0 = 0; b0 < nseg; b0 += 32) {
       const float ms = b0 + lane < nseg ? __ldcg(seg_rec(b0 + lane, h) + 2 * D) : -INFINITY;
@@ -162,7 +163,7 @@ __device__ __noinline__ void merge_layer_unit(const DevCache &c, const LayerPlan
       }
     }
     const float inv = 1.f / lsum;
-    float *dst = out + ((size_t)u * c.g + h) * D + CPL * lane;
+    float *dst = out_u + (size_t)h * D + CPL * lane;
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       const float tr = x[k] * c.inv_sqrt_d;

@@ -214,6 +214,9 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   const int ib = seg_begin(lp.T, lp.W, gw), ie = seg_begin(lp.T, lp.W, gw + 1);
   if (ib >= ie) return;
   constexpr bool tsa = TSA;                     // layer kind (Table I): TSA has 4-bit text rows
+  // GQA (NEXT-3): a unit's g query heads are processed in HG groups of NH heads;
+  // work items, partials and tickets are per virtual unit vu = u * HG + group
+  const int HG = lp.hg;
   const float alpha_k = kLog2e / (float)D;     // (q.H_s) . K^ / d in log2 units
   const float alpha_o = kLog2e * c.inv_sqrt_d; // q.k / sqrt d in log2 units
   const uint32_t kbytes = c.pg_vscale, vbytes = c.page_bytes - c.pg_vscale;
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       } else if (kind == 2) {                     // ring chunk (rows n of it)
         sb.kind = 2; sb.ring = 1; sb.a = a; sb.n = n;
       } else {                                    // side split a: entries [lo, hi), runtime count
-        const int cnt = __ldg(c.side_cnt + pu);
+        const int cnt = __ldg(c.side_cnt + pu / HG);
         const int lo = a * cnt / lp.Sc, hi = (a + 1) * cnt / lp.Sc;   // 32-bit: cnt <= capacity
         const int per = tsa ? kRows4 : kRows;
         sb.kind = tsa ? 3 : 2;
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     if (sb.kind < 0) return;
     uint8_t *dst = wsm + (size_t)st * SB;
     if (sb.kind <= 1) {
-      const uint8_t *src = page_ptr(c, sb.u, sb.a) + (sb.kind ? kbytes : 0u);
+      const uint8_t *src = page_ptr(c, sb.u / HG, sb.a) + (sb.kind ? kbytes : 0u);
       const uint32_t nb = sb.kind ? vbytes : kbytes;
       mbar_expect_tx(&bar[st], nb);
       bulk_g2s(dst, src, nb, &bar[st]);
@@ -273,13 +276,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       const int n1 = min(sb.n, c.slots - s0);
       const uint32_t rowb = 4 * D;
       mbar_expect_tx(&bar[st], (uint32_t)sb.n * rowb);
-      bulk_g2s(dst, ring_row(c, sb.u, s0), (uint32_t)n1 * rowb, &bar[st]);
+      bulk_g2s(dst, ring_row(c, sb.u / HG, s0), (uint32_t)n1 * rowb, &bar[st]);
       if (n1 < sb.n)
-        bulk_g2s(dst + (size_t)n1 * rowb, ring_row(c, sb.u, 0), (uint32_t)(sb.n - n1) * rowb, &bar[st]);
+        bulk_g2s(dst + (size_t)n1 * rowb, ring_row(c, sb.u / HG, 0), (uint32_t)(sb.n - n1) * rowb, &bar[st]);
     } else {
       const uint32_t eb = c.side_entry;
       mbar_expect_tx(&bar[st], (uint32_t)sb.n * eb);
-      bulk_g2s(dst, side_ptr(c, sb.u, sb.a), (uint32_t)sb.n * eb, &bar[st]);
+      bulk_g2s(dst, side_ptr(c, sb.u / HG, sb.a), (uint32_t)sb.n * eb, &bar[st]);
     }
   };
   if (lane == 0)
@@ -320,7 +323,9 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     int w_lo, w_hi;
     seg_range(lp.T, lp.W, lp.per_u, u, w_lo, w_hi);
     if (take_ticket(c, u, w_hi - w_lo + 1, lane)) {
-      merge_layer_unit<D, NH>(c, lp, part, u, out, flags, lane);
+      const int hg = u % HG, nh = min(NH, c.g - hg * NH);
+      merge_layer_unit<D, NH>(c, lp, part, u, out + ((size_t)(u / HG) * c.g + hg * NH) * D, nh,
+                              flags, lane);
       if (lane == 0) c.ticket[u] = 0u;
     }
   };
@@ -430,7 +435,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       for (int h = 0; h < NH; ++h) {
         constexpr int CPL = D / 32;
         float x[CPL];
-        const uint16_t *qs = q + ((size_t)s.u * c.g + h) * D + CPL * lane;
+        const uint16_t *qs = q + ((size_t)(s.u / HG) * c.g + min((s.u % HG) * NH + h, c.g - 1)) * D + CPL * lane;
         if constexpr (CPL == 4) {
           const uint2 v = *reinterpret_cast<const uint2 *>(qs);
           cvt2<DT>(v.x, x[0], x[1]);
@@ -458,7 +463,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       __syncwarp();
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
-        const uint2 v = *reinterpret_cast<const uint2 *>(q + ((size_t)s.u * c.g + h) * D + 4 * vcq);
+        const uint2 v = *reinterpret_cast<const uint2 *>(
+            q + ((size_t)(s.u / HG) * c.g + min((s.u % HG) * NH + h, c.g - 1)) * D + 4 * vcq);
         cvt2<DT>(v.x, qk[h][0], qk[h][1]);
         cvt2<DT>(v.y, qk[h][2], qk[h][3]);
         const float4 t4 = reinterpret_cast<const float4 *>(qh + h * D)[vcq];
@@ -475,7 +481,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     if (s.kind == 0) {
       // ================= page K half: logits of the page's G tokens
       const uint32_t sbits =
-          (__ldg(c.bitmask + (size_t)s.u * c.bm_words + (size_t)s.a * (G / 32) + (ktq >> 3)) >>
+          (__ldg(c.bitmask + (size_t)(s.u / HG) * c.bm_words + (size_t)s.a * (G / 32) + (ktq >> 3)) >>
            (4 * (ktq & 7))) & 15u;
       mbar_wait(&bar[st], par);
       const float4 *ks4 = reinterpret_cast<const float4 *>(B + c.pg_kscale);
@@ -754,10 +760,11 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         // the caller's row, append it to the ring and set its TSA text bit
         const int tl = lp.L - 1 - (lp.n_q + s.a);
         if (tl >= 0 && tl < s.n) {
-          const uint4 *sk = reinterpret_cast<const uint4 *>(app_k + (size_t)s.u * D);
-          const uint4 *sv = reinterpret_cast<const uint4 *>(app_v + (size_t)s.u * D);
+          const int uu = s.u / HG;                   // (every head group appends: benign, identical)
+          const uint4 *sk = reinterpret_cast<const uint4 *>(app_k + (size_t)uu * D);
+          const uint4 *sv = reinterpret_cast<const uint4 *>(app_v + (size_t)uu * D);
           uint8_t *Bw = B + (size_t)tl * 4 * D;
-          uint4 *rrow = reinterpret_cast<uint4 *>(ring_row(c, s.u, (lp.L - 1) % c.slots));
+          uint4 *rrow = reinterpret_cast<uint4 *>(ring_row(c, uu, (lp.L - 1) % c.slots));
           for (int i = lane; i < D / 8; i += 32) {
             const uint4 kv = sk[i], vv = sv[i];
             reinterpret_cast<uint4 *>(Bw)[i] = kv;
@@ -765,8 +772,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
             rrow[i] = kv;
             rrow[D / 8 + i] = vv;
           }
-          if (lane == 0 && tsa && app_types != nullptr && app_types[s.u] == 1)
-            atomicOr(&c.bitmask[(size_t)s.u * c.bm_words + (lp.L - 1) / 32], 1u << ((lp.L - 1) % 32));
+          if (lane == 0 && tsa && app_types != nullptr && app_types[uu] == 1)
+            atomicOr(&c.bitmask[(size_t)uu * c.bm_words + (lp.L - 1) / 32], 1u << ((lp.L - 1) % 32));
           __syncwarp();
         }
       }
@@ -819,8 +826,9 @@ static cudaError_t launch_ly(const DevCache &c, const LayerPlan &lp, const void 
 }
 
 int layer_supported(int d, int G, int g) {
-  return (d == 128 || d == 64) && G >= 32 && G <= d && (g == 1 || g == 2 || g == 4);
+  return (d == 128 || d == 64) && G >= 32 && G <= d && g >= 1 && g <= 16;
 }
+int layer_head_groups(int g) { return g <= 2 ? 1 : (g + 3) / 4; }
 int layer_warps_per_cta() { return kLyWarps; }
 int layer_ctas_per_sm(int g) { return ly_ctas_per_sm(g); }
 int layer_rows_per_chunk() { return kRows; }
@@ -832,6 +840,7 @@ static cudaError_t launch_ly_g(const DevCache &c, const LayerPlan &lp, const voi
                                uint32_t flags, cudaStream_t st) {
   if (c.g == 1) return launch_ly<D, G, DT, 1>(c, lp, q, k, v, types, part, out, flags, st);
   if (c.g == 2) return launch_ly<D, G, DT, 2>(c, lp, q, k, v, types, part, out, flags, st);
+  // g == 4 or GQA head groups of 4 (lp.hg = ceil(g / 4))
   return launch_ly<D, G, DT, 4>(c, lp, q, k, v, types, part, out, flags, st);
 }
 

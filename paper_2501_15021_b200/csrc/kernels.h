@@ -27,6 +27,7 @@ struct LayerPlan {
   int T, W;
   int per_u;
   int P, Rc, Sc;
+  int hg;               // GQA head groups per unit (virtual units u * hg + group)
   int maxseg;
   int L, n_q, nq_mod;   // nq_mod = n_q % ring slots
   int stream_only;      // AKVQ_OPT_STREAM_ONLY (profiling)
@@ -59,6 +60,7 @@ cudaError_t launch_decode_layer(const DevCache &c, int dtype16, const LayerPlan 
                                 const void *k, const void *v, const uint8_t *types, float *part,
                                 float *out, uint32_t flags, cudaStream_t st);
 int layer_supported(int d, int G, int g);
+int layer_head_groups(int g);
 int layer_warps_per_cta();
 int layer_ctas_per_sm(int g);
 int layer_rows_per_chunk();

@@ -322,3 +322,15 @@ def test_prefill_with_detected_pivots(ak, orc, sy, name, layer):
         ref = oc.decode(f16_bits(do["q"]))
         err = np.abs(out[us].double().cpu().numpy() - ref).max()
         assert err <= OUT_TOL, f"step {step}: {err}"
+
+
+# ----------------------------------------------------------------- NEXT-3 GQA head groups
+@pytest.mark.parametrize("g", [3, 5, 7, 8])
+@pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
+def test_gqa_head_groups(ak, orc, sy, g, kind):
+    """q_per_kv not in {1, 2}: the layer kernel runs ceil(g/4) head groups of 4
+    per kv head (virtual units, a padded head in the last group); parity with
+    the oracle over prefill, a flush and 12 decode steps (fused and split)."""
+    import dataclasses
+    w = dataclasses.replace(sy.TINY, name=f"tiny_g{g}", hq=4 * g, hkv=4)
+    _run_case(ak, orc, sy, w, 0, kind=kind, steps=12)
