@@ -66,6 +66,10 @@ int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return v && *v ? atoi(v) : dflt;
 }
+int min_items_per_warp() {
+  static const int v = env_int("AKVQ_MIN_ITEMS", 4);
+  return v < 1 ? 1 : v;
+}
 int pg_ctas_override() {
   static const int v = env_int("AKVQ_PG_CTAS", 0);
   return v;
@@ -145,7 +149,10 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
       const int ctas = pg_ctas_override() > 0 ? pg_ctas_override() : layer_ctas_per_sm(f.q_per_kv);
       const long long wmax = (long long)sms * ctas * layer_warps_per_cta();
       lp.T = (int)T;
-      long long W = T < wmax ? T : wmax;
+      // at least min_items items per warp: fewer segments per unit to merge and
+      // fewer tickets when the layer is small (W = T would give one item each)
+      const long long wmin_items = (T + min_items_per_warp() - 1) / min_items_per_warp();
+      long long W = wmin_items < wmax ? wmin_items : wmax;
       if (T * W >= (1LL << 31)) W = ((1LL << 31) - 1) / T;   // 32-bit segment arithmetic
       lp.W = (int)(W < 1 ? 1 : W);
       const long long per = (T + lp.W - 1) / lp.W;

@@ -79,14 +79,12 @@ __device__ __forceinline__ void seg_range(int T, int W, int per, int u, int &w_l
   w_lo = 0;
   w_hi = -1;
   if (T <= 0 || W <= 0) return;
-  const int i0 = u * per, i1 = i0 + per;
-  // first warp whose range ends after i0: ceil((i0 + 1) * W / T) - 1
-  w_lo = (int)(((unsigned)(i0 + 1) * (unsigned)W + (unsigned)T - 1) / (unsigned)T) - 1;
-  if (w_lo < 0) w_lo = 0;
-  while (w_lo > 0 && seg_begin(T, W, w_lo) > i0) --w_lo;
-  while (seg_begin(T, W, w_lo + 1) <= i0) ++w_lo;
-  w_hi = w_lo;
-  while (w_hi + 1 < W && seg_begin(T, W, w_hi + 1) < i1) ++w_hi;
+  const unsigned i0 = (unsigned)(u * per), i1 = i0 + (unsigned)per;
+  // seg_begin(w) = floor(w T / W): the largest w with seg_begin(w) <= i0 is
+  // ceil((i0 + 1) W / T) - 1, the largest with seg_begin(w) < i1 is ceil(i1 W / T) - 1
+  w_lo = (int)(((i0 + 1u) * (unsigned)W + (unsigned)T - 1u) / (unsigned)T) - 1;
+  w_hi = (int)((i1 * (unsigned)W + (unsigned)T - 1u) / (unsigned)T) - 1;
+  if (w_hi > W - 1) w_hi = W - 1;
 }
 
 // Per-unit merge by one warp: log-sum-exp over all segments of unit u, then
@@ -130,17 +128,32 @@ __device__ __noinline__ void merge_layer_unit(const DevCache &c, const LayerPlan
         }
         lsum += warp_sum(f * ls);
         const int nb = min(32, nseg - b0);
-        for (int j = 0; j < nb; ++j) {
-          const float fj = __shfl_sync(0xffffffffu, f, j);
-          const unsigned long long pj =
-              __shfl_sync(0xffffffffu, (unsigned long long)(uintptr_t)rh, j);
-          if (fj == 0.f) continue;
-          const float *r = reinterpret_cast<const float *>((uintptr_t)pj);
+        // 4 segments per round: their loads are independent and issue together
+        // (segments with weight 0 -- empty softmax -- read a valid record, add 0)
+        for (int j0 = 0; j0 < nb; j0 += 4) {
+          float fj[4], vo[4][CPL], vr[4][CPL];
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            org[k] = fmaf(fj, __ldcg(r + CPL * lane + k), org[k]);
-            rot[k] = fmaf(fj, __ldcg(r + D + CPL * lane + k), rot[k]);
+          for (int jj = 0; jj < 4; ++jj) {
+            const int j = min(j0 + jj, nb - 1);
+            fj[jj] = j0 + jj < nb ? __shfl_sync(0xffffffffu, f, j) : 0.f;
+            const unsigned long long pj =
+                __shfl_sync(0xffffffffu, (unsigned long long)(uintptr_t)rh, j);
+            const float *r = reinterpret_cast<const float *>((uintptr_t)pj);
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              vo[jj][k] = __ldcg(r + CPL * lane + k);
+              vr[jj][k] = __ldcg(r + D + CPL * lane + k);
+            }
           }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              if (fj[jj] != 0.f) {
+                org[k] = fmaf(fj[jj], vo[jj][k], org[k]);
+                rot[k] = fmaf(fj[jj], vr[jj][k], rot[k]);
+              }
+            }
         }
       }
     }

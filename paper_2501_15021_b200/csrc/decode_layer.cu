@@ -46,7 +46,7 @@ constexpr int kRows = 8;           // 16-bit rows per ring chunk / side sub-load
 constexpr int kRows4 = 32;         // 4-bit TSA rows per side sub-load
 constexpr int kQMax = 32767;       // K-side fixed point: |Q| <= 2^15 - 1 (2 limbs)
 constexpr int kWMax = 65535;       // V-side fixed point: W <= 2^16 - 1 (2 limbs)
-__host__ __device__ constexpr int ly_ctas_per_sm(int nh) { return nh >= 4 ? 2 : (nh >= 2 ? 3 : 5); }
+__host__ __device__ constexpr int ly_ctas_per_sm(int nh) { return nh >= 4 ? 2 : (nh >= 2 ? 3 : 4); }
 
 // Per-warp shared memory (bytes):
 //   stages [kLyStages][SB] | qh [NH][D] f32 (q~ = q.H_s) | limbs: K [NH][D/16][8]
@@ -130,7 +130,8 @@ __device__ __forceinline__ float rs_reduce(float (&v)[NV], int cq, int &mine) {
 // One sub-load of the pipeline: an item split into stage-sized pieces.  The
 // producer lane records it in the warp's descriptor ring (one per stage).
 struct LySub {
-  int u, kind;   // kind: 0 page K half, 1 page V half, 2 16-bit rows, 3 4-bit rows, -1 none
+  int u, kind;   // u: (virtual) unit; kind: 0 page K half, 1 page V half, 2 16-bit rows, 3 4-bit rows, -1 none
+  int pu;        // physical unit (u / head groups), producer side only
   int a, n;      // page index | first row (ring offset from n_q / side entry) and row count
   int ring;      // 1 if ring rows
 };
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   }
   // producer state: unit, table entry, sub-load within a side split
   int pu = ib / lp.per_u, pj = ib - (ib / lp.per_u) * lp.per_u, left = ie - ib, part_i = 0;
+  int pphys = pu / HG, phg = pu - (pu / HG) * HG;   // physical unit / head group of pu
   auto produce = [&](int st) {                  // lane 0 only
     LySub sb;
     sb.kind = -1;
@@ -237,6 +239,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       const int a = (int)(e >> 8), n = (int)((e >> 2) & 63u);
       bool ok = true, next = true;
       sb.u = pu;
+      sb.pu = pphys;
       sb.ring = 0;
       if (kind == 0) {                            // page: K half then V half
         sb.kind = part_i; sb.a = a; sb.n = 0;      // (n unused for pages; 6-bit field)
@@ -245,7 +248,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       } else if (kind == 2) {                     // ring chunk (rows n of it)
         sb.kind = 2; sb.ring = 1; sb.a = a; sb.n = n;
       } else {                                    // side split a: entries [lo, hi), runtime count
-        const int cnt = __ldg(c.side_cnt + pu / HG);
+        const int cnt = __ldg(c.side_cnt + pphys);
         const int lo = a * cnt / lp.Sc, hi = (a + 1) * cnt / lp.Sc;   // 32-bit: cnt <= capacity
         const int per = tsa ? kRows4 : kRows;
         sb.kind = tsa ? 3 : 2;
@@ -256,7 +259,11 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         part_i = ok ? part_i + 1 : 0;
       }
       if (next) {
-        if (++pj == lp.per_u) { pj = 0; ++pu; }
+        if (++pj == lp.per_u) {
+          pj = 0;
+          ++pu;
+          if (++phg == HG) { phg = 0; ++pphys; }
+        }
         --left;
       }
       if (ok) break;
@@ -266,7 +273,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     if (sb.kind < 0) return;
     uint8_t *dst = wsm + (size_t)st * SB;
     if (sb.kind <= 1) {
-      const uint8_t *src = page_ptr(c, sb.u / HG, sb.a) + (sb.kind ? kbytes : 0u);
+      const uint8_t *src = page_ptr(c, sb.pu, sb.a) + (sb.kind ? kbytes : 0u);
       const uint32_t nb = sb.kind ? vbytes : kbytes;
       mbar_expect_tx(&bar[st], nb);
       bulk_g2s(dst, src, nb, &bar[st]);
@@ -276,13 +283,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       const int n1 = min(sb.n, c.slots - s0);
       const uint32_t rowb = 4 * D;
       mbar_expect_tx(&bar[st], (uint32_t)sb.n * rowb);
-      bulk_g2s(dst, ring_row(c, sb.u / HG, s0), (uint32_t)n1 * rowb, &bar[st]);
+      bulk_g2s(dst, ring_row(c, sb.pu, s0), (uint32_t)n1 * rowb, &bar[st]);
       if (n1 < sb.n)
-        bulk_g2s(dst + (size_t)n1 * rowb, ring_row(c, sb.u / HG, 0), (uint32_t)(sb.n - n1) * rowb, &bar[st]);
+        bulk_g2s(dst + (size_t)n1 * rowb, ring_row(c, sb.pu, 0), (uint32_t)(sb.n - n1) * rowb, &bar[st]);
     } else {
       const uint32_t eb = c.side_entry;
       mbar_expect_tx(&bar[st], (uint32_t)sb.n * eb);
-      bulk_g2s(dst, side_ptr(c, sb.u / HG, sb.a), (uint32_t)sb.n * eb, &bar[st]);
+      bulk_g2s(dst, side_ptr(c, sb.pu, sb.a), (uint32_t)sb.n * eb, &bar[st]);
     }
   };
   if (lane == 0)
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   float m_run[NH], l_run[NH], o_rot[NH][4], o_org[NH][4];
   float qk[NH][4], qt[NH][4], qsum[NH];               // q (orig) * alpha_o; q~ * alpha_k; sum
   float lg[NH][4];                                    // page logits of the lane's token quad
-  int cur_u = -1;
+  int cur_u = -1, cur_pu = 0, cur_hg = 0;      // virtual unit, its physical unit and head group
   const int u_first = ib / lp.per_u;
 
   auto flush = [&](int u) {
@@ -430,12 +437,14 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     if (s.u != cur_u) {
       if (cur_u >= 0) flush(cur_u);
       cur_u = s.u;
+      cur_pu = s.u / HG;
+      cur_hg = s.u - cur_pu * HG;
       // q~ = q . H_s (unnormalized FWHT: in-register then shuffle butterflies)
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
         constexpr int CPL = D / 32;
         float x[CPL];
-        const uint16_t *qs = q + ((size_t)(s.u / HG) * c.g + min((s.u % HG) * NH + h, c.g - 1)) * D + CPL * lane;
+        const uint16_t *qs = q + ((size_t)cur_pu * c.g + min(cur_hg * NH + h, c.g - 1)) * D + CPL * lane;
         if constexpr (CPL == 4) {
           const uint2 v = *reinterpret_cast<const uint2 *>(qs);
           cvt2<DT>(v.x, x[0], x[1]);
@@ -464,7 +473,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
         const uint2 v = *reinterpret_cast<const uint2 *>(
-            q + ((size_t)(s.u / HG) * c.g + min((s.u % HG) * NH + h, c.g - 1)) * D + 4 * vcq);
+            q + ((size_t)cur_pu * c.g + min(cur_hg * NH + h, c.g - 1)) * D + 4 * vcq);
         cvt2<DT>(v.x, qk[h][0], qk[h][1]);
         cvt2<DT>(v.y, qk[h][2], qk[h][3]);
         const float4 t4 = reinterpret_cast<const float4 *>(qh + h * D)[vcq];
@@ -481,7 +490,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     if (s.kind == 0) {
       // ================= page K half: logits of the page's G tokens
       const uint32_t sbits =
-          (__ldg(c.bitmask + (size_t)(s.u / HG) * c.bm_words + (size_t)s.a * (G / 32) + (ktq >> 3)) >>
+          (__ldg(c.bitmask + (size_t)cur_pu * c.bm_words + (size_t)s.a * (G / 32) + (ktq >> 3)) >>
            (4 * (ktq & 7))) & 15u;
       mbar_wait(&bar[st], par);
       const float4 *ks4 = reinterpret_cast<const float4 *>(B + c.pg_kscale);
@@ -760,7 +769,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         // the caller's row, append it to the ring and set its TSA text bit
         const int tl = lp.L - 1 - (lp.n_q + s.a);
         if (tl >= 0 && tl < s.n) {
-          const int uu = s.u / HG;                   // (every head group appends: benign, identical)
+          const int uu = cur_pu;                     // (every head group appends: benign, identical)
           const uint4 *sk = reinterpret_cast<const uint4 *>(app_k + (size_t)uu * D);
           const uint4 *sv = reinterpret_cast<const uint4 *>(app_v + (size_t)uu * D);
           uint8_t *Bw = B + (size_t)tl * 4 * D;
