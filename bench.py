@@ -16,8 +16,10 @@ configuration BASELINE.json's metric is quoted on that fits one GPU.  Synthetic
 inputs (paper_2501_15021_b200/synth.py) stand in for MileBench prompts.
 
 Multi-GPU: launched by torchrun; rank r owns a contiguous slice of the global
-units (batch x kv-head, BJ:5), so the global batch is fixed ("strong" scaling);
-outputs are all-gathered with NCCL once per step (shard.OutputGather).  Timing: CUDA events on the
+units (batch x kv-head, BJ:5).  Units are independent (no data-path collective),
+so by default every rank runs the full per-GPU workload on its own batch rows
+("weak" scaling: global batch = N x 64); --scaling strong splits a fixed batch.
+Outputs are all-gathered with NCCL once per step (shard.OutputGather, row a8).  Timing: CUDA events on the
 launching stream with a barrier + synchronize on both sides, max over ranks.
 """
 from __future__ import annotations
@@ -222,6 +224,10 @@ def main():
     ap.add_argument("--workload", default="sweep@b64")
     ap.add_argument("--impl", default="akvq", choices=["akvq", "reference"])
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank runs the full per-GPU workload on its own batch "
+                         "rows (units are independent, task rule 5); strong: the global "
+                         "batch is fixed and split")
     ap.add_argument("--pivots", default="colsum", choices=["colsum", "massive"],
                     help="PSA saliency: column-sum top-k (BJ:5, graded) or massive-activation "
                          "pivots from a synthetic residual stream (P:209-213, NEXT-2)")
@@ -242,6 +248,9 @@ def main():
     if args.impl == "reference":
         run_reference(args, w, rank)
         return
+    w1 = w                                              # per-GPU workload (the N = 1 config)
+    if args.scaling == "weak" and world > 1:
+        w = w1.with_batch(w1.batch * world)             # global: N x the batch rows
 
     from paper_2501_15021_b200 import akvq as ak
 
@@ -508,10 +517,12 @@ def main():
         line = {
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "u8-dp4a+f32", "data": "synthetic",
-            "config": {"workload": w.name, "source": "BJ:9 batch sweep at LLaVA-1.5-7B shape",
-                       "layers": n_layers, "global_batch": w.batch, "heads": w.hq,
+            "config": {"workload": w1.name, "source": "BJ:9 batch sweep at LLaVA-1.5-7B shape",
+                       "layers": n_layers, "global_batch": w.batch,
+                       "per_gpu_batch": w.batch // world if args.scaling == "weak" else None,
+                       "heads": w.hq,
                        "kv_heads": w.hkv, "head_dim": w.d, "prompt_tokens": w.L0,
                        "group": w.G, "residual": w.R, "top_k": w.top_k,
                        "tsa_layers": list(w.tsa_layers), "kv_bits": 2,
