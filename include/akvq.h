@@ -136,6 +136,10 @@ typedef struct {
   int32_t options;     /* AKVQ_OPT_* bits, 0 by default (set after init)      */
   int32_t launches;    /* kernels enqueued by the last call on this cache
                           (host counter, for launch accounting in bench.py)  */
+  uint64_t last_write; /* library launch sequence number of the last launch
+                          that wrote this cache (host; decides whether the
+                          decode kernel may stream cache pages before the
+                          preceding grid has completed)                       */
 } akvq_cache;
 
 /* akvq_cache.options: route 2-bit pages through the generic split-K kernel

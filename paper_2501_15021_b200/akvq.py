@@ -60,7 +60,7 @@ class akvq_layout(C.Structure):
 class akvq_cache(C.Structure):
     _fields_ = [("cfg", akvq_config), ("lay", akvq_layout), ("base", C.c_void_p),
                 ("L", C.c_int32), ("n_q", C.c_int32), ("sm_count", C.c_int32),
-                ("options", C.c_int32), ("launches", C.c_int32)]
+                ("options", C.c_int32), ("launches", C.c_int32), ("last_write", C.c_uint64)]
 
 
 class akvq_mem_report(C.Structure):

@@ -6,6 +6,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "akvq.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -59,6 +61,14 @@ DevCache make_dev(const akvq_cache *c) {
 }
 
 akvq_status cuda_status(cudaError_t e) { return e == cudaSuccess ? AKVQ_OK : AKVQ_ECUDA; }
+
+// Library-wide launch sequence (host).  A cache records the sequence number of
+// its last writing launch; a decode launch may prefetch cache pages before
+// griddepcontrol.wait only if some launch came after that write (then, by PDL
+// ordering, the writer has completed when the decode grid starts).
+std::atomic<unsigned long long> g_seq{0};
+unsigned long long next_seq() { return g_seq.fetch_add(1) + 1; }
+void mark_write(akvq_cache *c) { c->last_write = next_seq(); }
 
 // Persistent-grid sizes (CTAs per SM) of the two decode kernels; tuning
 // overrides AKVQ_ROW_CTAS / AKVQ_PG_CTAS are read once (experiments only).
@@ -177,13 +187,20 @@ size_t ws_bytes_for(const akvq_cache *c, const DecodePlan &p) {
 }
 
 // Fast-path launch: one k_decode_layer (+ append when k != NULL).
-akvq_status launch_fast(const akvq_cache *c, const DecodePlan &p, const void *q, const void *k,
+akvq_status launch_fast(const akvq_cache *c, DecodePlan &p, const void *q, const void *k,
                         const void *v, const uint8_t *types, float *out, void *ws,
                         uint32_t flags, cudaStream_t s) {
   const DevCache d = make_dev(c);
   if (p.lp.T > 0) const_cast<akvq_cache *>(c)->launches += 1;
-  return cuda_status(launch_decode_layer(d, c->cfg.dtype16, p.lp, q, k, v, types,
-                                         static_cast<float *>(ws), out, flags, s));
+  // prologue prefetch: not right after a write of this cache, and no append in
+  // this launch's own first sub-loads is needed before the wait (the new row is
+  // patched in after the wait)
+  p.lp.prologue = (c->last_write < g_seq.load()) && !(c->options & AKVQ_OPT_STREAM_ONLY) ? 1 : 0;
+  const cudaError_t e = launch_decode_layer(d, c->cfg.dtype16, p.lp, q, k, v, types,
+                                            static_cast<float *>(ws), out, flags, s);
+  if (k != nullptr) mark_write(const_cast<akvq_cache *>(c));   // the fused step appends
+  else next_seq();
+  return cuda_status(e);
 }
 
 }  // namespace
@@ -252,6 +269,7 @@ akvq_status akvq_cache_init(akvq_cache *c, const akvq_config *f, void *dev_buf, 
   cudaMemsetAsync(b + y.ticket_off, 0, (size_t)f->n_units * 4 * 4, s);
   if (y.side_cap > 0)
     cudaMemsetAsync(b + y.side_idx_off, 0xff, (size_t)f->n_units * y.side_cap * 4, s);
+  mark_write(c);
   return cuda_status(cudaGetLastError());
 }
 
@@ -267,6 +285,7 @@ akvq_status akvq_select_salient(akvq_cache *c, const uint8_t *types, const float
     if (L0 > AKVQ_MAX_PSA_PROMPT) return AKVQ_EUNSUPPORTED;
   }
   const DevCache d = make_dev(c);
+  mark_write(c);
   return cuda_status(launch_salient(d, types, colsum, L0, c->cfg.top_k,
                                     reinterpret_cast<cudaStream_t>(stream)));
 }
@@ -337,6 +356,7 @@ static akvq_status quantize_prompt(akvq_cache *c, const void *K, const void *V, 
   cudaError_t e = launch_quantize_blocks(d, f.dtype16, src, 0, nb, nb - 1, s);
   if (e == cudaSuccess) e = launch_ring_fill(d, K, V, L0, n_q, L0, s);
   c->launches += (nb > 0) + (L0 > n_q);
+  mark_write(c);
   if (e != cudaSuccess) return AKVQ_ECUDA;
   c->L = L0;
   c->n_q = n_q;
@@ -353,6 +373,7 @@ static akvq_status append_impl(akvq_cache *c, const void *k, const void *v, cons
   cudaError_t e = launch_append(d, k, v, types, c->L, s);
   if (e != cudaSuccess) return AKVQ_ECUDA;
   c->launches += 1;
+  mark_write(c);
   c->L += 1;
   if (c->L - f.residual - c->n_q >= f.group) {        // block leaves the window (R9)
     QuantSrc src;
@@ -365,6 +386,7 @@ static akvq_status append_impl(akvq_cache *c, const void *k, const void *v, cons
     e = launch_quantize_blocks(d, f.dtype16, src, j, 1, j, s);
     if (e != cudaSuccess) return AKVQ_ECUDA;
     c->launches += 1;
+    mark_write(c);
     c->n_q += f.group;
   }
   return AKVQ_OK;
@@ -399,12 +421,13 @@ static akvq_status decode_impl(const akvq_cache *c, const void *q, float *out, v
                         size_t ws_bytes, uint32_t flags, akvq_stream_t stream) {
   if (!c || !c->base || !q || !out || !ws) return AKVQ_EINVAL;
   if (c->L == 0) return AKVQ_ESTATE;
-  const DecodePlan p = plan_decode(c, c->L, c->n_q);
+  DecodePlan p = plan_decode(c, c->L, c->n_q);
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
   const DevCache d = make_dev(c);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (p.fast) return launch_fast(c, p, q, nullptr, nullptr, nullptr, out, ws, flags, s);
   const_cast<akvq_cache *>(c)->launches += 2;         // split + combine
+  next_seq();
   return cuda_status(launch_decode(d, c->cfg.dtype16, p, q, out, ws, flags, s));
 }
 
@@ -423,7 +446,7 @@ akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const 
   if (c->L >= f.capacity) return AKVQ_ECAPACITY;
   const int L1 = c->L + 1;
   const bool flush = L1 - f.residual - c->n_q >= f.group;
-  const DecodePlan p = plan_decode(c, L1, flush ? c->n_q + f.group : c->n_q);
+  DecodePlan p = plan_decode(c, L1, flush ? c->n_q + f.group : c->n_q);
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
   if (flush || !p.fast || p.lp.T <= 0) {   // flush step (every G tokens) or generic path
     akvq_status st = append_impl(c, k, v, types, stream);

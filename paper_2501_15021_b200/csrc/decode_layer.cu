@@ -208,8 +208,14 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   uint2 *desc = reinterpret_cast<uint2 *>(wsm + S::ds_off(SB));
   uint64_t *bar = reinterpret_cast<uint64_t *>(wsm + S::bar_off(SB));
 
-  pdl_wait();                                   // q, k, v and the cache come from preceding work
-  pdl_launch_dependents();                      // the next layer's kernel may queue up
+  // Programmatic dependent launch: q, k, v (and, after a flush or append, the
+  // cache) come from the preceding grid.  When the host knows the preceding grid
+  // does not write this cache (lp.prologue), the first cache sub-loads are
+  // issued before griddepcontrol.wait, overlapping the previous layer's tail.
+  if (!lp.prologue) {
+    pdl_wait();
+    pdl_launch_dependents();                    // the next layer's kernel may queue up
+  }
   const int gw = blockIdx.x * kLyWarps + warp;
   if (gw >= lp.W) return;
   const int ib = seg_begin(lp.T, lp.W, gw), ie = seg_begin(lp.T, lp.W, gw + 1);
@@ -294,6 +300,10 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   };
   if (lane == 0)
     for (int s = 0; s < kLyStages; ++s) produce(s);
+  if (lp.prologue) {                            // inputs from the preceding grid from here on
+    pdl_wait();
+    pdl_launch_dependents();
+  }
   __syncwarp();
 
   // lane roles

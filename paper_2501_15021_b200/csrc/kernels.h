@@ -31,6 +31,8 @@ struct LayerPlan {
   int maxseg;
   int L, n_q, nq_mod;   // nq_mod = n_q % ring slots
   int stream_only;      // AKVQ_OPT_STREAM_ONLY (profiling)
+  int prologue;         // 1: the preceding grid does not write this cache, so the
+                        // first TMA sub-loads may be issued before griddepcontrol.wait
   uint32_t tab[kLyMaxTab];
 };
 
