@@ -334,3 +334,31 @@ def test_gqa_head_groups(ak, orc, sy, g, kind):
     import dataclasses
     w = dataclasses.replace(sy.TINY, name=f"tiny_g{g}", hq=4 * g, hkv=4)
     _run_case(ak, orc, sy, w, 0, kind=kind, steps=12)
+
+
+def test_interleaved_layers_use_prologue(ak, orc, sy):
+    """Two layer caches stepped alternately (as in a model): every decode launch
+    follows a launch on the OTHER cache, so it streams its first pages before the
+    PDL wait (LayerPlan.prologue); outputs must still match the oracle, across a
+    flush, with fused and split steps."""
+    w = sy.TINY
+    caches, oracles = [], []
+    for layer, kind in ((0, 1), (1, 0)):
+        gcfg, ocfg = _configs(ak, orc, w, layer, w.U, kind)
+        lc = ak.LayerCache(gcfg)
+        inp = sy.layer_inputs(w, layer, device="cuda")
+        lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
+        oc = orc.OracleCache(ocfg)
+        io = sy.layer_inputs(w, layer, device="cpu")
+        oc.prefill(f16_bits(io["K"]), f16_bits(io["V"]), io["types"].numpy(), io["colsum"].numpy())
+        caches.append(lc)
+        oracles.append(oc)
+    for step in range(12):
+        for layer, (lc, oc) in enumerate(zip(caches, oracles)):
+            di = sy.decode_inputs(w, layer, step, device="cuda")
+            out = lc.step(di["k"], di["v"], di["q"], di["types"])
+            do = sy.decode_inputs(w, layer, step, device="cpu")
+            oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
+            ref = oc.decode(f16_bits(do["q"]))
+            err = np.abs(out.double().cpu().numpy() - ref).max()
+            assert err <= OUT_TOL, f"layer {layer} step {step}: {err}"
