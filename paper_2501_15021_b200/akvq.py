@@ -14,7 +14,7 @@ from typing import Optional
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libakvq.so")
+LIB_PATH = os.environ.get("AKVQ_LIB") or os.path.join(_PKG, "libakvq.so")   # AKVQ_LIB: experiments only
 
 AKVQ_OK, AKVQ_EINVAL, AKVQ_EUNSUPPORTED, AKVQ_ECAPACITY, AKVQ_ESTATE, AKVQ_ECUDA = range(6)
 AKVQ_TSA, AKVQ_PSA = 0, 1

@@ -41,12 +41,18 @@
 namespace akvq {
 
 constexpr int kLyWarps = 4;        // warps per CTA
-constexpr int kLyStages = 2;       // TMA stages per warp
+#ifndef AKVQ_LY_STAGES
+#define AKVQ_LY_STAGES 2
+#endif
+constexpr int kLyStages = AKVQ_LY_STAGES;   // TMA stages per warp
 constexpr int kRows = 8;           // 16-bit rows per ring chunk / side sub-load
 constexpr int kRows4 = 32;         // 4-bit TSA rows per side sub-load
 constexpr int kQMax = 32767;       // K-side fixed point: |Q| <= 2^15 - 1 (2 limbs)
 constexpr int kWMax = 65535;       // V-side fixed point: W <= 2^16 - 1 (2 limbs)
-__host__ __device__ constexpr int ly_ctas_per_sm(int nh) { return nh >= 4 ? 2 : (nh >= 2 ? 3 : 4); }
+#ifndef AKVQ_LY_CTAS
+#define AKVQ_LY_CTAS 4
+#endif
+__host__ __device__ constexpr int ly_ctas_per_sm(int nh) { return nh >= 4 ? 2 : (nh >= 2 ? 3 : AKVQ_LY_CTAS); }
 
 // Per-warp shared memory (bytes):
 //   stages [kLyStages][SB] | qh [NH][D] f32 (q~ = q.H_s) | limbs: K [NH][D/16][8]
