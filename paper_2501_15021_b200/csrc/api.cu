@@ -156,7 +156,7 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
     lp.hg = layer_head_groups(f.q_per_kv);
     if (p.fast && lp.per_u > 0) {
       const long long T = (long long)f.n_units * lp.hg * lp.per_u;
-      const int ctas = pg_ctas_override() > 0 ? pg_ctas_override() : layer_ctas_per_sm(f.q_per_kv);
+      const int ctas = pg_ctas_override() > 0 ? pg_ctas_override() : layer_ctas_per_sm(layer_group_heads(f.q_per_kv));
       const long long wmax = (long long)sms * ctas * layer_warps_per_cta();
       lp.T = (int)T;
       // at least min_items items per warp: fewer segments per unit to merge and
@@ -180,7 +180,7 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
 size_t ws_bytes_for(const akvq_cache *c, const DecodePlan &p) {
   const size_t g = c->cfg.q_per_kv, d = c->cfg.head_dim;
   if (p.fast) {   // NH heads per record: g for g <= 2, 4 for head groups
-    const size_t nh = g <= 2 ? g : 4;
+    const size_t nh = (size_t)layer_group_heads((int)g);
     return (size_t)p.lp.W * p.lp.maxseg * nh * (2 * d + 4) * sizeof(float);
   }
   return (size_t)c->cfg.n_units * p.S * g * (d + 2) * sizeof(float);

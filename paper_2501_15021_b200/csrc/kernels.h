@@ -63,6 +63,7 @@ cudaError_t launch_decode_layer(const DevCache &c, int dtype16, const LayerPlan 
                                 float *out, uint32_t flags, cudaStream_t st);
 int layer_supported(int d, int G, int g);
 int layer_head_groups(int g);
+int layer_group_heads(int g);
 int layer_warps_per_cta();
 int layer_ctas_per_sm(int g);
 int layer_rows_per_chunk();
