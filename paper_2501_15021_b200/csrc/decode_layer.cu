@@ -318,7 +318,9 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   const int vgam = (4 * vcq) / G;                     // channel group of the lane's quad
 
   // per-unit segment state
-  float m_run[NH], l_run[NH], o_rot[NH][4], o_org[NH][4];
+  // l_run and zl are per-lane partials (each lane adds its own tokens / rows),
+  // reduced across the warp once per segment in flush
+  float m_run[NH], l_run[NH], o_rot[NH][4], o_org[NH][4], zl[NH][NG];
   float qk[NH][4], qt[NH][4], qsum[NH];               // q (orig) * alpha_o; q~ * alpha_k; sum
   float lg[NH][4];                                    // page logits of the lane's token quad
   int cur_u = -1, cur_pu = 0, cur_hg = 0;      // virtual unit, its physical unit and head group
@@ -336,6 +338,17 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           o_org[h][s] += __shfl_xor_sync(0xffffffffu, o_org[h][s], off);
         }
       }
+      // page zero-point terms: sum_t W_t z_t of every page (rescaled like o_rot),
+      // subtracted once from every channel of its group
+      float zg = 0.f;
+#pragma unroll
+      for (int gi = 0; gi < NG; ++gi) {
+        const float z = warp_sum(zl[h][gi]);
+        if (gi == vgam) zg = z;
+      }
+#pragma unroll
+      for (int s = 0; s < 4; ++s) o_rot[h][s] -= zg;
+      l_run[h] = warp_sum(l_run[h]);
       float *rec = part + (slot * NH + h) * Rec<D>::R;
       if (vts == 0) {
         reinterpret_cast<float4 *>(rec)[vcq] = make_float4(o_org[h][0], o_org[h][1], o_org[h][2], o_org[h][3]);
@@ -394,11 +407,11 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       const float m_new = fmaxf(m_run[h], mx);
       const float sc = ex2(m_run[h] - m_new);
       const float p = ex2(t - m_new);
-      float ps = p;
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
-      l_run[h] = fmaf(l_run[h], sc, ps);
+      // one lane per row (vcq & 3 == 0) adds its row's p to the lane partial
+      l_run[h] = fmaf(l_run[h], sc, (vcq & 3) == 0 ? p : 0.f);
       m_run[h] = m_new;
+#pragma unroll
+      for (int gi = 0; gi < NG; ++gi) zl[h][gi] *= sc;
       if (r16) {
         float2 oa = __fmul2_rn(make_float2(o_org[h][0], o_org[h][1]), make_float2(sc, sc));
         float2 ob = __fmul2_rn(make_float2(o_org[h][2], o_org[h][3]), make_float2(sc, sc));
@@ -500,6 +513,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         for (int k = 0; k < 4; ++k) { qk[h][k] *= alpha_o; o_rot[h][k] = 0.f; o_org[h][k] = 0.f; }
         m_run[h] = -INFINITY;
         l_run[h] = 0.f;
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) zl[h][gi] = 0.f;
       }
     }
 
@@ -684,7 +699,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       const float *vs = reinterpret_cast<const float *>(B);
       const int32_t *vz = reinterpret_cast<const int32_t *>(B + (c.pg_vzero - c.pg_vscale));
       const uint4 *vc4 = reinterpret_cast<const uint4 *>(B + (c.pg_vcodes - c.pg_vscale));
-      float dwv[NH][NG], zwv[NH][NG];
+      float dwv[NH][NG];
       bool live[NH];
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
@@ -692,7 +707,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         const float m_new = fmaxf(m_run[h], mloc);
         live[h] = m_new != -INFINITY;                 // warp-uniform
 #pragma unroll
-        for (int gi = 0; gi < NG; ++gi) { dwv[h][gi] = 0.f; zwv[h][gi] = 0.f; }
+        for (int gi = 0; gi < NG; ++gi) dwv[h][gi] = 0.f;
         if (!live[h]) continue;
         const float sc = ex2(m_run[h] - m_new);
         m_run[h] = m_new;
@@ -701,8 +716,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         float pr[4], psum = 0.f;
 #pragma unroll
         for (int k = 0; k < 4; ++k) { pr[k] = ex2(lg[h][k] - m_new); psum += pr[k]; }
-        psum = warp_sum(kcs == 0 ? psum : 0.f);
-        l_run[h] = l_run[h] * sc + psum;
+        l_run[h] = fmaf(l_run[h], sc, kcs == 0 ? psum : 0.f);   // lane partial
 #pragma unroll
         for (int gi = 0; gi < NG; ++gi) {
           float wv[4], wmax = 0.f;
@@ -722,8 +736,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
             W[k] = min(__float2uint_rn(wv[k] * invw), (uint32_t)kWMax);
             zs = fmaf((float)W[k], (float)vz[(4 * ktq + k) * NG + gi], zs);
           }
-          zwv[h][gi] = warp_sum(kcs == 0 ? zs : 0.f);
           dwv[h][gi] = wmax * (1.0f / (float)kWMax);
+          zl[h][gi] = fmaf(zl[h][gi], sc, kcs == 0 ? dwv[h][gi] * zs : 0.f);   // lane partial
           if (kcs == 0) {
             const uint32_t lo = prmt(prmt(W[0], W[1], 0x0040), prmt(W[2], W[3], 0x0040), 0x5410);
             const uint32_t hi = prmt(prmt(W[0], W[1], 0x0051), prmt(W[2], W[3], 0x0051), 0x5410);
@@ -764,15 +778,14 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
         if (!live[h]) continue;
-        float dw = dwv[h][0], zw = zwv[h][0];
+        float dw = dwv[h][0];
 #pragma unroll
-        for (int gi = 1; gi < NG; ++gi) if (gi == vgam) { dw = dwv[h][gi]; zw = zwv[h][gi]; }
-        if (vts != 0) zw = 0.f;                        // the zero term once per channel
+        for (int gi = 1; gi < NG; ++gi) if (gi == vgam) dw = dwv[h][gi];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           // < 2^31: 128 tokens x 4 x 192 x 255 per limb
           const float val = (float)(acc[h][k][1] * 256 + acc[h][k][0]) * (1.0f / (float)(1 << (2 * k)));
-          o_rot[h][k] = fmaf(dw, val - zw, o_rot[h][k]);
+          o_rot[h][k] = fmaf(dw, val, o_rot[h][k]);     // zero term: zl, subtracted at flush
         }
       }
     } else {
