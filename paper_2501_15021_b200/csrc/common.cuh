@@ -168,6 +168,34 @@ __device__ __forceinline__ uint32_t q_code_fast(float x, const QMeta &m, float r
 
 __device__ __forceinline__ int32_t zero_i32(float zf) { return __float2int_rz(zf); }
 
+// N codes of one group (same meta) packed at 2 * i bits, i < N: branch-free
+// except once per group.  Equal, bit for bit, to q_code on each element: the
+// product x * rs lies within 2 ulp of the IEEE quotient x / s, so both round to
+// the same integer unless the product is within 1e-6 (|y| + 1) of a half-integer;
+// if any element of the group is that close, the group is redone with IEEE
+// division (rare).  mode 1 / 2 groups (degenerate / empty) are uniform.
+template <int N>
+__device__ __forceinline__ uint32_t q_codes2(const float (&x)[N], const QMeta &m, float rs) {
+  if (m.mode == 2) return 0u;
+  if (m.mode == 1) return 0x55555555u & ((N >= 16) ? 0xffffffffu : ((1u << (2 * N)) - 1u));
+  uint32_t w = 0;
+  bool near = false;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const float y = __fmul_rn(x[i], rs);
+    const float r = rintf(y);
+    near |= fabsf(__fsub_rn(y, r)) > __fsub_rn(0.5f, __fmul_rn(1e-6f, __fadd_rn(fabsf(y), 1.f)));
+    const float q = fminf(fmaxf(__fadd_rn(r, m.zf), 0.f), 3.f);
+    w |= (uint32_t)q << (2 * i);
+  }
+  if (near) {
+    w = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) w |= q_code(x[i], m, 3.f) << (2 * i);
+  }
+  return w;
+}
+
 // ---- warp helpers --------------------------------------------------------
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll

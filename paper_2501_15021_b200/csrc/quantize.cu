@@ -205,8 +205,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
       static_assert(CPL == 8 || CPL == 16, "channels per lane");
       uint32_t w = 0;                         // the lane's CPL/4 S:146 bytes
       const float rs = m.mode == 0 ? __frcp_rn(m.s) : 0.f;
-#pragma unroll
-      for (int i = 0; i < CPL; ++i) w |= (sal ? 0u : q_code_fast(v[i], m, rs, 3.f)) << (2 * i);
+      w = q_codes2<CPL>(v, m, rs);            // salient row: m.mode == 2 -> codes 0
       if constexpr (CPL == 16) *reinterpret_cast<uint32_t *>(vb8 + t * (D / 4) + cl * 4) = w;
       else *reinterpret_cast<uint16_t *>(vb8 + t * (D / 4) + cl * 2) = (uint16_t)w;
     }
@@ -301,24 +300,32 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
     for (int wi = tid; wi < CQ * TQ; wi += kQThreads) {   // K word wi -> (cq, tq)
       const int cq = (wi & 3) + 4 * (wi / (4 * TQ)), tq = (wi / 4) % TQ;
       uint32_t word = 0;
+      // salient tokens of this token quad: their codes are 0 (mask per byte)
+      const uint32_t sb4 = (s_bits[(4 * tq) >> 5] >> ((4 * tq) & 31)) & 15u;
+      uint32_t keep = 0;
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) keep |= ((sb4 >> s2) & 1u) ? 0u : (3u << (2 * s2));
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int ch = 4 * cq + b;
-        QMeta mc;                                    // per-channel meta, hoisted
-        float rc = 0.f;
-        if constexpr (!KT) { mc.s = s_s[ch]; mc.zf = s_z[ch]; mc.mode = s_mode[ch]; rc = s_rs[ch]; }
+        float xv[4];
 #pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) {
-          const int t = 4 * tq + s2;
-          QMeta m = mc;
-          float r = rc;
-          if constexpr (KT) {
-            const int mi = t * NG + ch / G;
-            m.s = s_s[mi]; m.zf = s_z[mi]; m.mode = s_mode[mi]; r = s_rs[mi];
+        for (int s2 = 0; s2 < 4; ++s2) xv[s2] = xs[(4 * tq + s2) * P + ch];
+        uint32_t c4;
+        if constexpr (!KT) {                         // one channel's meta for the 4 tokens
+          QMeta m; m.s = s_s[ch]; m.zf = s_z[ch]; m.mode = s_mode[ch];
+          c4 = q_codes2<4>(xv, m, s_rs[ch]);
+        } else {                                     // per-token meta
+          c4 = 0;
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2) {
+            const int mi = (4 * tq + s2) * NG + ch / G;
+            QMeta m; m.s = s_s[mi]; m.zf = s_z[mi]; m.mode = s_mode[mi];
+            const float x1[1] = {xv[s2]};
+            c4 |= q_codes2<1>(x1, m, s_rs[mi]) << (2 * s2);
           }
-          const bool sal = (s_bits[t >> 5] >> (t & 31)) & 1u;
-          word |= (sal ? 0u : q_code_fast(xs[t * P + ch], m, r, 3.f)) << (8 * b + 2 * s2);
         }
+        word |= (c4 & keep) << (8 * b);
       }
       dk[wi] = word;
     }
