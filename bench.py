@@ -195,7 +195,7 @@ def run_reference(args, w, rank):
     """--impl reference: the oracle as the reference arm, rank 0 only."""
     if rank != 0:
         return
-    smp = OracleSample(w, n_units=8)
+    smp = OracleSample(w, n_units=32)
     n = min(args.warmup + args.steps, w.capacity - smp.oc.L)
     times = []
     for i in range(n):
@@ -206,7 +206,7 @@ def run_reference(args, w, rank):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
             "ms_per_step": 1000.0 * w.batch / val, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name},
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": smp.cores,
                              "kind": "oracle", "sample": smp.describe()},
