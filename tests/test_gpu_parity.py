@@ -131,11 +131,13 @@ def test_llava7b_layer_full(ak, orc, sy, layer, options):
 
 # ----------------------------------------------------------------- sampled, full size
 @pytest.mark.parametrize("name,layer", [("sweep@b16", 2), ("video13b", 3), ("qwen_gqa", 5),
-                                        ("qwen_gqa", 1)])
+                                        ("qwen_gqa", 1), ("sweep@b64", 2), ("sweep@b64", 0)])
 def test_full_size_sampled_units(ak, orc, sy, name, layer):
+    """Full BJ sizes in bench.py's launch configuration (sweep@b64 is the bench
+    workload), sampled units checked against the oracle."""
     w = sy.get(name)
     U = w.U
-    _run_case(ak, orc, sy, w, layer, steps=2, units=[0, U // 2, U - 1])
+    _run_case(ak, orc, sy, w, layer, steps=2, units=[0, U // 3, U // 2, U - 1])
 
 
 # ----------------------------------------------------------------- edge cases
