@@ -153,9 +153,24 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
       }
       while (r < NR) lp.tab[k++] = row_item(r++);
     }
+    // item costs (~ warp instructions, profiles/r01_final_summary.md): a page is
+    // two 5 KB sub-loads of dp4a work (~1440), a ring chunk of 8 16-bit rows and a
+    // PSA side split ~400, a TSA side split (up to 32 4-bit rows each pass) ~1200
+    const int c_page = 7, c_rows = 2, c_side = f.kind == AKVQ_TSA ? 6 : 2;
+    lp.cu = lp.P * c_page + lp.Rc * c_rows + lp.Sc * c_side;   // <= 2048 * 7 < 2^16
+    if (build_tab && lp.per_u <= kLyMaxTab) {
+      int acc = 0;
+      lp.cpre[0] = 0;
+      for (int j = 0; j < lp.per_u; ++j) {
+        const uint32_t kd = lp.tab[j] & 3u;
+        acc += kd == 0 ? c_page : (kd == 2 ? c_rows : c_side);
+        lp.cpre[j + 1] = (uint16_t)acc;
+      }
+    }
     lp.hg = layer_head_groups(f.q_per_kv);
     if (p.fast && lp.per_u > 0) {
       const long long T = (long long)f.n_units * lp.hg * lp.per_u;
+      const long long CT = (long long)f.n_units * lp.hg * lp.cu;
       const int ctas = pg_ctas_override() > 0 ? pg_ctas_override() : layer_ctas_per_sm(layer_group_heads(f.q_per_kv));
       const long long wmax = (long long)sms * ctas * layer_warps_per_cta();
       lp.T = (int)T;
@@ -163,10 +178,15 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
       // fewer tickets when the layer is small (W = T would give one item each)
       const long long wmin_items = (T + min_items_per_warp() - 1) / min_items_per_warp();
       long long W = wmin_items < wmax ? wmin_items : wmax;
-      if (T * W >= (1LL << 31)) W = ((1LL << 31) - 1) / T;   // 32-bit segment arithmetic
+      const int cmax = c_page > c_side ? c_page : c_side;
+      if (W > CT / cmax) W = CT / cmax;                   // every warp gets >= 1 item
+      if (CT * W >= (1LL << 31)) W = ((1LL << 31) - 1) / CT;   // 32-bit cost arithmetic
       lp.W = (int)(W < 1 ? 1 : W);
-      const long long per = (T + lp.W - 1) / lp.W;
-      lp.maxseg = (int)((per + lp.per_u - 1) / lp.per_u + 1);
+      lp.CT = (int)CT;
+      // units one warp can touch: its cost share spans <= share / (cost of the
+      // cheapest unit) + 2 units
+      const long long share = (CT + lp.W - 1) / lp.W;
+      lp.maxseg = (int)(share / (lp.cu > 0 ? lp.cu : 1) + 2);
     } else {
       lp.per_u = 1;
     }

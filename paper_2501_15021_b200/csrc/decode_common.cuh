@@ -87,6 +87,31 @@ __device__ __forceinline__ void seg_range(int T, int W, int per, int u, int &w_l
   if (w_hi > W - 1) w_hi = W - 1;
 }
 
+// Cost-weighted segments of the layer plan (kernels.h LayerPlan): item i = (u, k)
+// starts at cost u * cu + cpre[k]; warp(i) = floor(start * W / CT).
+__device__ __forceinline__ int ly_warp_of(const LayerPlan &lp, int u, int k) {
+  return (int)(((unsigned)(u * lp.cu + lp.cpre[k]) * (unsigned)lp.W) / (unsigned)lp.CT);
+}
+// first item (flattened u * per_u + k) of warp w: the first start cost >= c0
+__device__ __forceinline__ int ly_first_item(const LayerPlan &lp, int w) {
+  const unsigned c0 = ((unsigned)w * (unsigned)lp.CT + (unsigned)lp.W - 1u) / (unsigned)lp.W;
+  int u = (int)(c0 / (unsigned)lp.cu);
+  const int r = (int)(c0 - (unsigned)u * (unsigned)lp.cu);
+  int lo = 0, hi = lp.per_u;                          // smallest k with cpre[k] >= r
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (lp.cpre[mid] >= r) hi = mid; else lo = mid + 1;
+  }
+  if (lo == lp.per_u) { ++u; lo = 0; }
+  return u * lp.per_u + lo;
+}
+// unit of warp w's first item (O(1): c0 falls in unit c0 / cu unless past its last start)
+__device__ __forceinline__ int ly_first_unit(const LayerPlan &lp, int w) {
+  const unsigned c0 = ((unsigned)w * (unsigned)lp.CT + (unsigned)lp.W - 1u) / (unsigned)lp.W;
+  const int u = (int)(c0 / (unsigned)lp.cu);
+  return (int)(c0 - (unsigned)u * (unsigned)lp.cu) > (int)lp.cpre[lp.per_u - 1] ? u + 1 : u;
+}
+
 // Per-unit merge by one warp: log-sum-exp over all segments of unit u, then
 // out = (o_rot . H + o_org) / l (or o_rot + o_org . H with AKVQ_OUT_ROTATED),
 // H applied as an unnormalized FWHT times 1/sqrt d (Fig. 7, R4).  Partials are
@@ -96,13 +121,12 @@ template <int D, int NH>
 __device__ __noinline__ void merge_layer_unit(const DevCache &c, const LayerPlan &lp, const float *part, int u,
                                  float *out_u, int nh, uint32_t flags, int lane) {
   constexpr int CPL = D / 32;
-  int w0, w1;
-  seg_range(lp.T, lp.W, lp.per_u, u, w0, w1);
+  const int w0 = ly_warp_of(lp, u, 0), w1 = ly_warp_of(lp, u, lp.per_u - 1);
   const int nseg = w1 - w0 + 1;
   const bool out_rot = flags & AKVQ_OUT_ROTATED;
   auto seg_rec = [&](int j, int h) -> const float * {
     const int w = w0 + j;
-    const int slot = w * lp.maxseg + (u - seg_begin(lp.T, lp.W, w) / lp.per_u);
+    const int slot = w * lp.maxseg + (u - ly_first_unit(lp, w));
     return part + ((size_t)slot * NH + h) * Rec<D>::R;
   };
 #pragma unroll

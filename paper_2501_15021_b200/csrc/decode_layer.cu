@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   }
   const int gw = blockIdx.x * kLyWarps + warp;
   if (gw >= lp.W) return;
-  const int ib = seg_begin(lp.T, lp.W, gw), ie = seg_begin(lp.T, lp.W, gw + 1);
+  const int ib = ly_first_item(lp, gw);
+  const int ie = gw + 1 < lp.W ? ly_first_item(lp, gw + 1) : lp.T;
   if (ib >= ie) return;
   constexpr bool tsa = TSA;                     // layer kind (Table I): TSA has 4-bit text rows
   // GQA (NEXT-3): a unit's g query heads are processed in HG groups of NH heads;
@@ -356,8 +357,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       }
       if (lane == 0) { rec[2 * D] = m_run[h]; rec[2 * D + 1] = l_run[h]; }
     }
-    int w_lo, w_hi;
-    seg_range(lp.T, lp.W, lp.per_u, u, w_lo, w_hi);
+    const int w_lo = ly_warp_of(lp, u, 0), w_hi = ly_warp_of(lp, u, lp.per_u - 1);
     if (take_ticket(c, u, w_hi - w_lo + 1, lane)) {
       const int hg = u % HG, nh = min(NH, c.g - hg * NH);
       merge_layer_unit<D, NH>(c, lp, part, u, out + ((size_t)(u / HG) * c.g + hg * NH) * D, nh,

@@ -31,9 +31,14 @@ struct LayerPlan {
   int maxseg;
   int L, n_q, nq_mod;   // nq_mod = n_q % ring slots
   int stream_only;      // AKVQ_OPT_STREAM_ONLY (profiling)
+  // cost-weighted split: item k of a unit starts at cost cpre[k] (cpre[per_u] =
+  // cu, the unit's cost); CT = units * cu; warp w owns the items whose start cost
+  // c satisfies floor(c W / CT) == w (host: CT * W < 2^31, CT / W >= max cost)
+  int cu, CT;
   int prologue;         // 1: the preceding grid does not write this cache, so the
                         // first TMA sub-loads may be issued before griddepcontrol.wait
   uint32_t tab[kLyMaxTab];
+  uint16_t cpre[kLyMaxTab + 1];
 };
 
 // Decode split plan (host-computed, uniform across units).
