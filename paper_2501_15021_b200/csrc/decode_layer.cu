@@ -188,7 +188,7 @@ __device__ __forceinline__ constexpr int rs_enc(int m) {
   return e;
 }
 
-template <int D, int G, int DT, int NH, bool TSA>
+template <int D, int G, int DT, int NH, bool TSA, bool KT>
 __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     k_decode_layer(const __grid_constant__ DevCache c, const __grid_constant__ LayerPlan lp, const uint16_t *__restrict__ q,
                    const uint16_t *__restrict__ app_k, const uint16_t *__restrict__ app_v,
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       const float4 *ks4 = reinterpret_cast<const float4 *>(B + c.pg_kscale);
       const int4 *kz4 = reinterpret_cast<const int4 *>(B + c.pg_kzero);
       const uint4 *kc4 = reinterpret_cast<const uint4 *>(B + c.pg_kcodes);
-      if (c.k_axis == AKVQ_K_PER_TOKEN) {
+      if constexpr (KT) {                      // per-token K variant (compile time)
         // ---- per-token K (NEXT-1): Q_c = rn(q~_c / delta) once per page,
         // logit_t = alpha delta sum_g s_tg (sum_{c in g} Q_c code_tc - z_tg SQ_g)
         const float *ksT = reinterpret_cast<const float *>(B + c.pg_kscale);    // [G][NG]
@@ -847,7 +847,9 @@ static cudaError_t launch_ly(const DevCache &c, const LayerPlan &lp, const void 
                              const void *v, const uint8_t *types, float *part, float *out,
                              uint32_t flags, cudaStream_t st) {
   const size_t smem = ly_smem<D, G, NH>(c);
-  auto kern = c.kind == AKVQ_TSA ? k_decode_layer<D, G, DT, NH, true> : k_decode_layer<D, G, DT, NH, false>;
+  const bool kt = c.k_axis == AKVQ_K_PER_TOKEN;
+  auto kern = c.kind == AKVQ_TSA ? (kt ? k_decode_layer<D, G, DT, NH, true, true> : k_decode_layer<D, G, DT, NH, true, false>)
+                                 : (kt ? k_decode_layer<D, G, DT, NH, false, true> : k_decode_layer<D, G, DT, NH, false, false>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((lp.W + kLyWarps - 1) / kLyWarps));
