@@ -145,9 +145,11 @@ typedef struct {
 /* akvq_cache.options: route 2-bit pages through the generic split-K kernel
  * instead of the persistent dp4a page kernel (test hook for cross-checks). */
 #define AKVQ_OPT_GENERIC_PAGES 1
-/* Profiling hook: the fast decode kernels stream every byte they would read
- * (same TMA pipeline) but skip all arithmetic; outputs are garbage.  Used
- * only to measure the memory pipeline's ceiling (bench.py --stream-only). */
+/* Profiling hook: the fast decode kernel streams every byte it would read
+ * (same TMA pipeline) but skips all arithmetic; outputs are garbage.  Used
+ * only to measure the memory pipeline's ceiling (bench.py --stream-only).
+ * A separate compile-time kernel variant, built for g == 1 caches only; with
+ * g > 1 the decode call fails with AKVQ_ECUDA. */
 #define AKVQ_OPT_STREAM_ONLY 2
 /* Profiling hooks: skip the row kernel / the page kernel entirely (outputs are
  * garbage); used to attribute the decode time (bench.py --skip-rows/pages). */

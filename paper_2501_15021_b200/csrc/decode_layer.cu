@@ -188,13 +188,15 @@ __device__ __forceinline__ constexpr int rs_enc(int m) {
   return e;
 }
 
-template <int D, int G, int DT, int NH, bool TSA, bool KT>
+template <int D, int G, int DT, int NH, bool TSA, int KM>
 __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     k_decode_layer(const __grid_constant__ DevCache c, const __grid_constant__ LayerPlan lp, const uint16_t *__restrict__ q,
                    const uint16_t *__restrict__ app_k, const uint16_t *__restrict__ app_v,
                    const uint8_t *__restrict__ app_types, float *__restrict__ part,
                    float *__restrict__ out, uint32_t flags) {
   using S = LySmem<D, G, NH>;
+  constexpr bool KT = KM == 1;              // per-token K (AKVQ_K_PER_TOKEN)
+  constexpr bool SO = KM == 2;              // profiling: TMA pipeline only (LayerPlan::stream_only)
   constexpr int NG = D / G;
   constexpr int CQ = D / 4, TQ = G / 4;     // channel quads, token quads
   constexpr int CG = D / 16, TG = G / 16;   // 4-quad groups (one LDS.128 of tile words)
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     const LySub s = unpack_sub(desc[st]);
     if (s.kind < 0) break;
     uint8_t *B = wsm + (size_t)st * SB;
-    if (lp.stream_only) {                           // profiling: pipeline only
+    if constexpr (SO) {                             // profiling: pipeline only
       mbar_wait(&bar[st], par);
       __syncwarp();
       if (lane == 0) produce(st);
@@ -834,7 +836,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     __syncwarp();
     if (++st == kLyStages) { st = 0; par ^= 1u; }
   }
-  if (cur_u >= 0 && !lp.stream_only) flush(cur_u);
+  if constexpr (!SO)
+    if (cur_u >= 0) flush(cur_u);
 }
 
 template <int D, int G, int NH>
@@ -847,9 +850,15 @@ static cudaError_t launch_ly(const DevCache &c, const LayerPlan &lp, const void 
                              const void *v, const uint8_t *types, float *part, float *out,
                              uint32_t flags, cudaStream_t st) {
   const size_t smem = ly_smem<D, G, NH>(c);
-  const bool kt = c.k_axis == AKVQ_K_PER_TOKEN;
-  auto kern = c.kind == AKVQ_TSA ? (kt ? k_decode_layer<D, G, DT, NH, true, true> : k_decode_layer<D, G, DT, NH, true, false>)
-                                 : (kt ? k_decode_layer<D, G, DT, NH, false, true> : k_decode_layer<D, G, DT, NH, false, false>);
+  const int km = c.k_axis == AKVQ_K_PER_TOKEN ? 1 : 0;
+  auto kern = c.kind == AKVQ_TSA ? (km ? k_decode_layer<D, G, DT, NH, true, 1> : k_decode_layer<D, G, DT, NH, true, 0>)
+                                 : (km ? k_decode_layer<D, G, DT, NH, false, 1> : k_decode_layer<D, G, DT, NH, false, 0>);
+  if (lp.stream_only) {                      // profiling variant: single-head MHA caches only
+    if constexpr (NH == 1)
+      kern = c.kind == AKVQ_TSA ? k_decode_layer<D, G, DT, NH, true, 2> : k_decode_layer<D, G, DT, NH, false, 2>;
+    else
+      return cudaErrorNotSupported;
+  }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((lp.W + kLyWarps - 1) / kLyWarps));
