@@ -47,7 +47,7 @@ constexpr int kLyWarps = 4;        // warps per CTA
 constexpr int kLyStages = AKVQ_LY_STAGES;   // TMA stages per warp
 constexpr int kRows = 8;           // 16-bit rows per ring chunk / side sub-load
 constexpr int kRows4 = 32;         // 4-bit TSA rows per side sub-load
-constexpr int kQMax = 32767;       // K-side fixed point: |Q| <= 2^15 - 1 (2 limbs)
+constexpr int kQMax = 32639;       // K-side fixed point: |Q| <= 127 * 257 (2 signed limbs)
 constexpr int kWMax = 65535;       // V-side fixed point: W <= 2^16 - 1 (2 limbs)
 #ifndef AKVQ_LY_CTAS
 #define AKVQ_LY_CTAS 4
@@ -65,7 +65,9 @@ struct LySmem {
   static constexpr size_t KL = (size_t)NH * (D / 16) * 32, VL = (size_t)NH * NG * (G / 16) * 32;
   static __host__ __device__ size_t kl_off(size_t sb) { return qh_off(sb) + NH * D * 4; }
   static __host__ __device__ size_t vl_off(size_t sb) { return kl_off(sb); }   // shared
-  static __host__ __device__ size_t ds_off(size_t sb) { return kl_off(sb) + (KL > VL ? KL : VL); }
+  // page logits [NH][G] / page V sums [NH][D] (fp32, one at a time)
+  static __host__ __device__ size_t lv_off(size_t sb) { return kl_off(sb) + (KL > VL ? KL : VL); }
+  static __host__ __device__ size_t ds_off(size_t sb) { return lv_off(sb) + (size_t)NH * D * 4; }
   static __host__ __device__ size_t bar_off(size_t sb) { return ds_off(sb) + kLyStages * 32; }
   static __host__ __device__ size_t warp_bytes(size_t sb) {
     return (bar_off(sb) + kLyStages * 8 + 127) / 128 * 128;
@@ -94,6 +96,26 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 __device__ __forceinline__ uint32_t fmask(uint32_t w, int s) { return w & (0x03030303u << (2 * s)); }
+
+// Legacy warp MMA m16n8k32 (IMMA, int32 accumulate): A 16x32 u8 row-major, B
+// 32x8 s8 / u8 column-major.  Fragments (lane = 4 * grp + tig): a0 / a1 hold
+// rows grp / grp + 8, columns 4 tig .. 4 tig + 3; a2 / a3 the same rows,
+// columns 16 + 4 tig ..; b0 / b1 rows 4 tig .. / 16 + 4 tig .. of column grp;
+// c0, c1 row grp, columns 2 tig, 2 tig + 1; c2, c3 row grp + 8.
+__device__ __forceinline__ void mma_u8s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_u8u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 
 template <int DT>
 __device__ __forceinline__ void cvt2(uint32_t w, float &a, float &b) {
@@ -319,6 +341,11 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   const int ktq = lane % TQ, kcs = lane / TQ;         // page K phase
   const int vcq = lane % CQ, vts = lane / CQ;         // page V phase and rows
   const int vgam = (4 * vcq) / G;                     // channel group of the lane's quad
+  const int mg = lane >> 2, mt = lane & 3;            // page MMA: fragment group / thread in group
+  const int mcol = min(mg, 2 * NH - 1);               // B column of the lane (padded columns repeat)
+  uint32_t *qlimb = klimb;                            // [2 NH][CQ] Q limbs (page MMA layout)
+  uint32_t *wlimb = vlimb;                            // [NG][2 NH][TQ] W limbs
+  float *lgs = reinterpret_cast<float *>(wsm + S::lv_off(SB));   // [NH][G] logits / [NH][D] V sums
 
   // per-unit segment state
   // l_run and zl are per-lane partials (each lane adds its own tokens / rows),
@@ -623,7 +650,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       } else {
       float dA[NH], bA[NH];
 #pragma unroll
-      for (int h = 0; h < NH; ++h) {      // limbs of Q_c = rn(q~_c s^K_c / delta): lane = channel quad
+      for (int h = 0; h < NH; ++h) {      // Q_c = rn(q~_c s^K_c / delta): lane = channel quad
         float qsb[4] = {0.f, 0.f, 0.f, 0.f}, am = 0.f;
         int4 zq = make_int4(0, 0, 0, 0);
         if (lane < CQ) {
@@ -650,50 +677,59 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         dA[h] = alpha_k * delta;
         bA[h] = alpha_k * delta * bq;
         if (lane < CQ) {
-          const uint32_t lo = prmt(prmt(Qv[0], Qv[1], 0x0040), prmt(Qv[2], Qv[3], 0x0040), 0x5410);
-          const uint32_t hi = prmt(prmt(Qv[0], Qv[1], 0x0051), prmt(Qv[2], Qv[3], 0x0051), 0x5410);
-          uint32_t *kl = klimb + (h * CG + (lane >> 2)) * 8 + (lane & 3);
-          kl[0] = lo;
-          kl[4] = hi;
+          // signed limbs Q = 256 hi + lo, lo, hi in [-128, 127]: x = Q + 128,
+          // hi = x >> 8 (byte 1 of x), lo = (x & 255) - 128 (byte 0 of x ^ 0x80)
+          const uint32_t x0 = Qv[0] + 128, x1 = Qv[1] + 128, x2 = Qv[2] + 128, x3 = Qv[3] + 128;
+          qlimb[(2 * h) * CQ + lane] = prmt(prmt(x0, x1, 0x0040), prmt(x2, x3, 0x0040), 0x5410) ^ 0x80808080u;
+          qlimb[(2 * h + 1) * CQ + lane] = prmt(prmt(x0, x1, 0x0051), prmt(x2, x3, 0x0051), 0x5410);
         }
       }
       __syncwarp();
-      int acc[NH][4][2];
+      // logits by warp MMA: rows = tokens (row grp: token 4 tq + k0, grp + 8:
+      // 4 tq + k1, tq = 8 blk + grp), K = 32 channels per chunk, columns = Q limbs
+      // (2 h, 2 h + 1).  The masked code word (code << 2k per byte) is the A
+      // fragment of 4 channels of one token; rows carry the 4^k factor.
+      constexpr int KC = D / 32;
+      uint32_t bq[KC][2];
 #pragma unroll
-      for (int h = 0; h < NH; ++h)
+      for (int cc = 0; cc < KC; ++cc) {
+        const uint2 b = *reinterpret_cast<const uint2 *>(qlimb + mcol * CQ + 8 * cc + 2 * mt);
+        bq[cc][0] = b.x;
+        bq[cc][1] = b.y;
+      }
+      float dsel = dA[0], bsel = bA[0];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { acc[h][k][0] = 0; acc[h][k][1] = 0; }
+      for (int h = 1; h < NH; ++h)
+        if (mt == h) { dsel = dA[h]; bsel = bA[h]; }
+      const uint32_t *kcw = reinterpret_cast<const uint32_t *>(B + c.pg_kcodes);
 #pragma unroll 2
-      for (int i = 0; i < CG / KCS; ++i) {
-        const int cg = kcs + KCS * i;
-        const uint4 w4 = kc4[cg * TQ + ktq];
-        const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
+      for (int blk = 0; blk < TQ / 8; ++blk) {
+        const int tq = 8 * blk + mg;
+        int c01[4] = {0, 0, 0, 0}, c23[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          const uint4 lo4 = reinterpret_cast<const uint4 *>(klimb + (h * CG + cg) * 8)[0];
-          const uint4 hi4 = reinterpret_cast<const uint4 *>(klimb + (h * CG + cg) * 8)[1];
-          const uint32_t lo[4] = {lo4.x, lo4.y, lo4.z, lo4.w};
-          const uint32_t hi[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t x = fmask(wd[j], k);
-              acc[h][k][0] = dp4a_uu(x, lo[j], acc[h][k][0]);
-              acc[h][k][1] = dp4a_us(x, hi[j], acc[h][k][1]);
-            }
+        for (int cc = 0; cc < KC; ++cc) {
+          const uint2 w = *reinterpret_cast<const uint2 *>(kcw + kword_idx(8 * cc + 2 * mt, tq, TQ));
+          mma_u8s8(c01, fmask(w.x, 0), fmask(w.x, 1), fmask(w.y, 0), fmask(w.y, 1), bq[cc][0], bq[cc][1]);
+          mma_u8s8(c23, fmask(w.x, 2), fmask(w.x, 3), fmask(w.y, 2), fmask(w.y, 3), bq[cc][0], bq[cc][1]);
+        }
+        if (mt < NH) {
+          float4 r;
+          r.x = fmaf((float)(c01[1] * 256 + c01[0]), dsel, -bsel);
+          r.y = fmaf((float)(c01[3] * 256 + c01[2]), dsel * 0.25f, -bsel);
+          r.z = fmaf((float)(c23[1] * 256 + c23[0]), dsel * 0.0625f, -bsel);
+          r.w = fmaf((float)(c23[3] * 256 + c23[2]), dsel * 0.015625f, -bsel);
+          reinterpret_cast<float4 *>(lgs + mt * G)[tq] = r;
         }
       }
+      __syncwarp();
 #pragma unroll
-      for (int h = 0; h < NH; ++h)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          int tot = acc[h][k][1] * 256 + acc[h][k][0];      // sum_c Q_c code_tc * 4^k
-#pragma unroll
-          for (int off = TQ; off < 32; off <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-          const float sc4 = dA[h] * (1.0f / (float)(1 << (2 * k)));
-          lg[h][k] = ((sbits >> k) & 1u) ? -INFINITY : fmaf((float)tot, sc4, -bA[h]);
-        }
+      for (int h = 0; h < NH; ++h) {
+        const float4 r = reinterpret_cast<const float4 *>(lgs + h * G)[ktq];
+        lg[h][0] = (sbits & 1u) ? -INFINITY : r.x;
+        lg[h][1] = (sbits & 2u) ? -INFINITY : r.y;
+        lg[h][2] = (sbits & 4u) ? -INFINITY : r.z;
+        lg[h][3] = (sbits & 8u) ? -INFINITY : r.w;
+      }
       }   // per-channel K
     } else if (s.kind == 1) {
       // ================= page V half: softmax update, value accumulation
@@ -743,51 +779,52 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           if (kcs == 0) {
             const uint32_t lo = prmt(prmt(W[0], W[1], 0x0040), prmt(W[2], W[3], 0x0040), 0x5410);
             const uint32_t hi = prmt(prmt(W[0], W[1], 0x0051), prmt(W[2], W[3], 0x0051), 0x5410);
-            uint32_t *vl = vlimb + ((h * NG + gi) * TG + (ktq >> 2)) * 8 + (ktq & 3);
-            vl[0] = lo;
-            vl[4] = hi;
+            wlimb[(gi * 2 * NH + 2 * h) * TQ + ktq] = lo;
+            wlimb[(gi * 2 * NH + 2 * h + 1) * TQ + ktq] = hi;
           }
         }
       }
       __syncwarp();
-      int acc[NH][4][2];
+      // sum_t W_t code_tc by warp MMA: rows = channels (row grp: 4 cq + k0, grp + 8:
+      // 4 cq + k1, cq = 8 cb + grp), K = 32 tokens per chunk, columns = W limbs
+      // (2 h, 2 h + 1) of the chunk's channel group.  Integer sums go through
+      // smem to the lane layout of o_rot (lane vcq: channels 4 vcq ..).
+      constexpr int TC = G / 32;
+      const uint32_t *vcw = reinterpret_cast<const uint32_t *>(vc4);
 #pragma unroll
-      for (int h = 0; h < NH; ++h)
+      for (int cb = 0; cb < D / 32; ++cb) {
+        const int cq = 8 * cb + mg, gi = (32 * cb) / G;
+        int c01[4] = {0, 0, 0, 0}, c23[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { acc[h][k][0] = 0; acc[h][k][1] = 0; }
-#pragma unroll 2
-      for (int i = 0; i < TG / VTS; ++i) {
-        const int tg = vts + VTS * i;
-        const uint4 w4 = vc4[tg * CQ + vcq];
-        const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          const uint32_t *vl = vlimb + ((h * NG + vgam) * TG + tg) * 8;
-          const uint4 lo4 = reinterpret_cast<const uint4 *>(vl)[0];
-          const uint4 hi4 = reinterpret_cast<const uint4 *>(vl)[1];
-          const uint32_t lo[4] = {lo4.x, lo4.y, lo4.z, lo4.w};
-          const uint32_t hi[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t x = fmask(wd[j], k);
-              acc[h][k][0] = dp4a_uu(x, lo[j], acc[h][k][0]);
-              acc[h][k][1] = dp4a_uu(x, hi[j], acc[h][k][1]);
-            }
+        for (int cc = 0; cc < TC; ++cc) {
+          const uint2 b = *reinterpret_cast<const uint2 *>(wlimb + (gi * 2 * NH + mcol) * TQ + 8 * cc + 2 * mt);
+          const uint2 w = *reinterpret_cast<const uint2 *>(vcw + vword_idx(cq, 8 * cc + 2 * mt, CQ));
+          mma_u8u8(c01, fmask(w.x, 0), fmask(w.x, 1), fmask(w.y, 0), fmask(w.y, 1), b.x, b.y);
+          mma_u8u8(c23, fmask(w.x, 2), fmask(w.x, 3), fmask(w.y, 2), fmask(w.y, 3), b.x, b.y);
+        }
+        if (mt < NH) {
+          // < 2^31: G tokens x 192 x 255 x 257 per column pair
+          float4 r;
+          r.x = (float)(c01[1] * 256 + c01[0]);
+          r.y = (float)(c01[3] * 256 + c01[2]) * 0.25f;
+          r.z = (float)(c23[1] * 256 + c23[0]) * 0.0625f;
+          r.w = (float)(c23[3] * 256 + c23[2]) * 0.015625f;
+          reinterpret_cast<float4 *>(lgs + mt * D)[cq] = r;
         }
       }
+      __syncwarp();
+      if (vts == 0) {
 #pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        if (!live[h]) continue;
-        float dw = dwv[h][0];
+        for (int h = 0; h < NH; ++h) {
+          if (!live[h]) continue;
+          float dw = dwv[h][0];
 #pragma unroll
-        for (int gi = 1; gi < NG; ++gi) if (gi == vgam) dw = dwv[h][gi];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          // < 2^31: 128 tokens x 4 x 192 x 255 per limb
-          const float val = (float)(acc[h][k][1] * 256 + acc[h][k][0]) * (1.0f / (float)(1 << (2 * k)));
-          o_rot[h][k] = fmaf(dw, val, o_rot[h][k]);     // zero term: zl, subtracted at flush
+          for (int gi = 1; gi < NG; ++gi) if (gi == vgam) dw = dwv[h][gi];
+          const float4 r = reinterpret_cast<const float4 *>(lgs + h * D)[vcq];
+          o_rot[h][0] = fmaf(dw, r.x, o_rot[h][0]);     // zero term: zl, subtracted at flush
+          o_rot[h][1] = fmaf(dw, r.y, o_rot[h][1]);
+          o_rot[h][2] = fmaf(dw, r.z, o_rot[h][2]);
+          o_rot[h][3] = fmaf(dw, r.w, o_rot[h][3]);
         }
       }
     } else {
