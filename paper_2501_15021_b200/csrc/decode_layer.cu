@@ -47,6 +47,15 @@ constexpr int kLyWarps = 4;        // warps per CTA
 constexpr int kLyStages = AKVQ_LY_STAGES;   // TMA stages per warp
 constexpr int kRows = 8;           // 16-bit rows per ring chunk / side sub-load
 constexpr int kRows4 = 32;         // 4-bit TSA rows per side sub-load
+// unroll factors of the page MMA loops (K: token blocks, V: channel blocks)
+#ifndef AKVQ_KU
+#define AKVQ_KU 4
+#endif
+#ifndef AKVQ_VU
+#define AKVQ_VU 4
+#endif
+#define AKVQ_PRAGMA(x) _Pragma(#x)
+#define AKVQ_UNROLL(n) AKVQ_PRAGMA(unroll n)
 constexpr int kQMax = 32639;       // K-side fixed point: |Q| <= 127 * 257 (2 signed limbs)
 constexpr int kWMax = 65535;       // V-side fixed point: W <= 2^16 - 1 (2 limbs)
 #ifndef AKVQ_LY_CTAS
@@ -702,7 +711,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       for (int h = 1; h < NH; ++h)
         if (mt == h) { dsel = dA[h]; bsel = bA[h]; }
       const uint32_t *kcw = reinterpret_cast<const uint32_t *>(B + c.pg_kcodes);
-#pragma unroll 2
+      AKVQ_UNROLL(AKVQ_KU)
       for (int blk = 0; blk < TQ / 8; ++blk) {
         const int tq = 8 * blk + mg;
         int c01[4] = {0, 0, 0, 0}, c23[4] = {0, 0, 0, 0};
@@ -791,7 +800,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       // smem to the lane layout of o_rot (lane vcq: channels 4 vcq ..).
       constexpr int TC = G / 32;
       const uint32_t *vcw = reinterpret_cast<const uint32_t *>(vc4);
-#pragma unroll
+      AKVQ_UNROLL(AKVQ_VU)
       for (int cb = 0; cb < D / 32; ++cb) {
         const int cq = 8 * cb + mg, gi = (32 * cb) / G;
         int c01[4] = {0, 0, 0, 0}, c23[4] = {0, 0, 0, 0};
