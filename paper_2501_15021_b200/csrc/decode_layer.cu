@@ -748,6 +748,22 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       const uint4 *vc4 = reinterpret_cast<const uint4 *>(B + (c.pg_vcodes - c.pg_vscale));
       float dwv[NH][NG];
       bool live[NH];
+      // the lane's 4 tokens' V scales / zero points (shared by the heads)
+      float vsv[NG][4], vzv[NG][4];
+      if constexpr (NG == 1) {
+        const float4 a = reinterpret_cast<const float4 *>(vs)[ktq];
+        const int4 b = reinterpret_cast<const int4 *>(vz)[ktq];
+        vsv[0][0] = a.x; vsv[0][1] = a.y; vsv[0][2] = a.z; vsv[0][3] = a.w;
+        vzv[0][0] = (float)b.x; vzv[0][1] = (float)b.y; vzv[0][2] = (float)b.z; vzv[0][3] = (float)b.w;
+      } else {
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            vsv[gi][k] = vs[(4 * ktq + k) * NG + gi];
+            vzv[gi][k] = (float)vz[(4 * ktq + k) * NG + gi];
+          }
+      }
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
         const float mloc = warp_max(fmaxf(fmaxf(lg[h][0], lg[h][1]), fmaxf(lg[h][2], lg[h][3])));
@@ -769,7 +785,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           float wv[4], wmax = 0.f;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            wv[k] = pr[k] * vs[(4 * ktq + k) * NG + gi];
+            wv[k] = pr[k] * vsv[gi][k];
             wmax = fmaxf(wmax, wv[k]);
           }
           wmax = warp_max(wmax);
@@ -781,7 +797,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             W[k] = min(__float2uint_rn(wv[k] * invw), (uint32_t)kWMax);
-            zs = fmaf((float)W[k], (float)vz[(4 * ktq + k) * NG + gi], zs);
+            zs = fmaf((float)W[k], vzv[gi][k], zs);
           }
           dwv[h][gi] = wmax * (1.0f / (float)kWMax);
           zl[h][gi] = fmaf(zl[h][gi], sc, kcs == 0 ? dwv[h][gi] * zs : 0.f);   // lane partial
