@@ -518,7 +518,7 @@ def main():
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-            "dtype": "u8-dp4a+f32", "data": "synthetic",
+            "dtype": "u8-imma+f32", "data": "synthetic",
             "config": {"workload": w1.name, "source": "BJ:9 batch sweep at LLaVA-1.5-7B shape",
                        "layers": n_layers, "global_batch": w.batch,
                        "per_gpu_batch": w.batch // world if args.scaling == "weak" else None,

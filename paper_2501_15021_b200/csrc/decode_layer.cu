@@ -18,14 +18,15 @@
 // take several sub-loads.
 //
 // Arithmetic (profiles/r01_microbench_pipes.md):
-//  pages, logits: lane = token quad; q~ * s^K rounded once per page to a 16-bit
-//    fixed point Q_c (two int8 limbs); one LOP3 mask per token of every K tile
-//    word (4 channels x 4 tokens) feeds dp4a against 4 channels' limbs:
-//    sum_c Q_c code_tc exact in int32; logit = delta (sum - sum_c Q_c z_c).
-//  pages, values: lane = channel quad; w_t = p_t s^V_t rounded to a 16-bit fixed
-//    point of the page's largest weight (two uint8 limbs); one mask per channel
-//    of every V tile word (4 tokens x 4 channels) feeds dp4a against 4 tokens'
-//    limbs: o'_c += dw (sum_t W_t code_tc - sum_t W_t z_t).
+//  pages, logits: q~ * s^K rounded once per page to a 16-bit fixed point Q_c
+//    (two signed int8 limbs); sum_c Q_c code_tc for all G tokens is one warp-MMA
+//    contraction (IMMA m16n8k32: A = LOP3-masked K tile words, rows = tokens;
+//    B = the limbs, columns = 2 per head), exact in int32;
+//    logit = delta (sum - sum_c Q_c z_c).  (Per-token K keeps dp4a.)
+//  pages, values: w_t = p_t s^V_t rounded to a 16-bit fixed point of the page's
+//    largest weight (two uint8 limbs); sum_t W_t code_tc is the second warp-MMA
+//    contraction (A = masked V tile words, rows = channels):
+//    o'_c += dw (sum_t W_t code_tc - sum_t W_t z_t).
 //  rows: lane = channel quad (8-byte slices, conflict-free LDS.64); per-row dot
 //    products are reduced across lanes with a reduce-scatter.
 // One online softmax (base 2) per (warp, unit) segment with two accumulators:
