@@ -98,7 +98,7 @@ def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every
 
 
 # ----------------------------------------------------------------- tiny (BJ:7)
-@pytest.mark.parametrize("options", [0, 1], ids=["dp4a-pages", "generic-pages"])
+@pytest.mark.parametrize("options", [0, 1], ids=["layer-pages", "generic-pages"])
 @pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
 def test_tiny_prefill_decode_and_flush(ak, orc, sy, kind, options):
     """Quantize once, 4 decode steps, extended to 16 steps across the L = 104 flush."""
@@ -118,7 +118,7 @@ def test_tiny_view_and_rotated_output(ak, orc, sy):
 
 
 # ----------------------------------------------------------------- 7B shape (BJ:8)
-@pytest.mark.parametrize("options", [0, 1], ids=["dp4a-pages", "generic-pages"])
+@pytest.mark.parametrize("options", [0, 1], ids=["layer-pages", "generic-pages"])
 @pytest.mark.parametrize("layer", [0, 2], ids=["TSA-L0", "PSA-L2"])
 def test_llava7b_layer_full(ak, orc, sy, layer, options):
     """All 32 units; decode across the L = 672 flush (n_q 512 -> 640)."""
@@ -229,7 +229,7 @@ def test_determinism_and_errors(ak, orc, sy):
 
 
 # ----------------------------------------------------------------- per-token K (NEXT-1)
-@pytest.mark.parametrize("options", [0, 1], ids=["dp4a-pages", "generic-pages"])
+@pytest.mark.parametrize("options", [0, 1], ids=["layer-pages", "generic-pages"])
 @pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
 def test_tiny_per_token_k(ak, orc, sy, kind, options):
     """k_axis = 1: codes, per-token K meta, view and decode vs the oracle,
@@ -327,11 +327,13 @@ def test_prefill_with_detected_pivots(ak, orc, sy, name, layer):
 
 
 # ----------------------------------------------------------------- NEXT-3 GQA head groups
-@pytest.mark.parametrize("g", [3, 5, 7, 8])
+@pytest.mark.parametrize("g", [2, 3, 5, 7, 8])
 @pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
 def test_gqa_head_groups(ak, orc, sy, g, kind):
-    """q_per_kv not in {1, 2}: the layer kernel runs ceil(g/4) head groups of 4
-    per kv head (virtual units, a padded head in the last group); parity with
+    """q_per_kv > 1: g = 2 is one group of 2 heads (page MMA columns 0-3); for
+    g > 2 the layer kernel runs ceil(g/2) head groups of 2
+    (AKVQ_GQA_NH) per kv head (virtual units, a padded head in the last group
+    for odd g); parity with
     the oracle over prefill, a flush and 12 decode steps (fused and split)."""
     import dataclasses
     w = dataclasses.replace(sy.TINY, name=f"tiny_g{g}", hq=4 * g, hkv=4)
