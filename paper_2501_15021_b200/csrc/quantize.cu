@@ -92,6 +92,12 @@ __global__ void __launch_bounds__(1024) k_salient_psa(DevCache c, const float *_
 // Source rows come from the prefill inputs or, for a flush, from the ring.
 constexpr int kQThreads = 256;
 
+// Staged K rows xs[t][P]: 16-byte chunk c of a row is stored at chunk
+// c ^ ((c >> 2) & 7), so the 8 lanes of a row (16 consecutive channels each)
+// store to distinct banks and a warp reading 32 consecutive chunks stays
+// conflict-free.
+__device__ __forceinline__ int xs_col(int ch) { return ((((ch >> 2) ^ (ch >> 4)) & 7) | ((ch >> 2) & ~7)) * 4 + (ch & 3); }
+
 template <int CPL>
 __device__ __forceinline__ void fwht_lanes8(float (&x)[CPL], int cl) {
 #pragma unroll
@@ -171,9 +177,10 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
     for (int i = 0; i < CPL / 8; ++i) { cvt8<DT>(kraw[i], k + 8 * i); cvt8<DT>(vraw[i], v + 8 * i); }
     fwht_lanes8<CPL>(k, cl);
     fwht_lanes8<CPL>(v, cl);
-    float4 *xk = reinterpret_cast<float4 *>(xs + t * P + cl * CPL);
 #pragma unroll
-    for (int i = 0; i < CPL / 4; ++i) xk[i] = make_float4(k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]);
+    for (int i = 0; i < CPL / 4; ++i)
+      *reinterpret_cast<float4 *>(xs + t * P + xs_col(cl * CPL + 4 * i)) =
+          make_float4(k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]);
     if constexpr (KT) {                   // K per token over G-channel groups (NEXT-1)
       const int gi = (cl * CPL) / G;
       float mn = k[0], mx = k[0];
@@ -272,7 +279,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
     float mn = INFINITY, mx = -INFINITY;
     for (int i = part * (G / NS); i < (part + 1) * (G / NS); ++i) {
       if ((s_bits[i >> 5] >> (i & 31)) & 1u) continue;
-      const float x = xs[i * P + ch];
+      const float x = xs[i * P + xs_col(ch)];
       mn = fminf(mn, x);
       mx = fmaxf(mx, x);
     }
@@ -297,20 +304,24 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
   {
     constexpr int TQ = G / 4, CQ = D / 4;
     uint32_t *dk = reinterpret_cast<uint32_t *>(pg + c.pg_kcodes);
-    for (int wi = tid; wi < CQ * TQ; wi += kQThreads) {   // K word wi -> (cq, tq)
-      const int cq = (wi & 3) + 4 * (wi / (4 * TQ)), tq = (wi / 4) % TQ;
+    for (int wi = tid; wi < CQ * TQ; wi += kQThreads) {   // K word (cq, tq), cq fastest
+      const int cq = wi % CQ, tq = wi / CQ;
       uint32_t word = 0;
       // salient tokens of this token quad: their codes are 0 (mask per byte)
       const uint32_t sb4 = (s_bits[(4 * tq) >> 5] >> ((4 * tq) & 31)) & 15u;
       uint32_t keep = 0;
 #pragma unroll
       for (int s2 = 0; s2 < 4; ++s2) keep |= ((sb4 >> s2) & 1u) ? 0u : (3u << (2 * s2));
+      float xq[4][4];                                // [token s2][channel b]
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) {
+        const float4 x4 = *reinterpret_cast<const float4 *>(xs + (4 * tq + s2) * P + xs_col(4 * cq));
+        xq[s2][0] = x4.x; xq[s2][1] = x4.y; xq[s2][2] = x4.z; xq[s2][3] = x4.w;
+      }
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int ch = 4 * cq + b;
-        float xv[4];
-#pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) xv[s2] = xs[(4 * tq + s2) * P + ch];
+        const float xv[4] = {xq[0][b], xq[1][b], xq[2][b], xq[3][b]};
         uint32_t c4;
         if constexpr (!KT) {                         // one channel's meta for the 4 tokens
           QMeta m; m.s = s_s[ch]; m.zf = s_z[ch]; m.mode = s_mode[ch];
@@ -327,7 +338,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
         }
         word |= (c4 & keep) << (8 * b);
       }
-      dk[wi] = word;
+      dk[kword_idx(cq, tq, TQ)] = word;
     }
     uint32_t *dv = reinterpret_cast<uint32_t *>(pg + c.pg_vcodes);
     for (int wi = tid; wi < CQ * TQ; wi += kQThreads) {   // V word wi -> (cq, tq)
