@@ -22,7 +22,10 @@ struct QuantSrc {
 // Item encoding: kind (bits 0-1: 0 page (K and V halves), 2 ring chunk,
 // 3 side split) | rows (bits 2-7, ring chunk) | index (bits 8-31: page, first
 // ring row relative to n_q, or side split).
-constexpr int kLyMaxTab = 2048;
+#ifndef AKVQ_MAX_TAB
+#define AKVQ_MAX_TAB 2048
+#endif
+constexpr int kLyMaxTab = AKVQ_MAX_TAB;
 struct LayerPlan {
   int T, W;
   int per_u;

@@ -19,8 +19,8 @@ def one(spec):
     objs = []
     for s in b.SOURCES:
         o = os.path.join(b.BUILD, s.replace(".cu", ".o"))
-        if s == "decode_layer.cu":
-            o = os.path.join(out, "decode_layer.o")
+        if s == "decode_layer.cu" or (s == "api.cu" and "AKVQ_MAX_TAB" in flags):
+            o = os.path.join(out, s.replace(".cu", ".o"))
             subprocess.run([b.NVCC, *b.FLAGS, *flags.split(), "-c", os.path.join(b.CSRC, s), "-o", o], check=True)
         objs.append(o)
     lib = os.path.join(ROOT, "build_exp", f"lib_{name}.so")
