@@ -92,10 +92,16 @@ typedef struct {
  *            +pg_kscale  f32 [d]     K scale per channel (normalized basis);
  *                                    per token: f32 [G][ng] (same bytes)
  *            +pg_kzero   i32 [d]     K zero point per channel; per token [G][ng]
- *            +pg_kcodes  u8  [G][d/4] K codes, 4 per byte along channels
+ *            +pg_kcodes  u32 [G*d/16] K codes (2 bits each, G*d/4 bytes) as
+ *                                    4x4 (token x channel) tile words: word
+ *                                    ((cq>>2)*G/4 + tq)*4 + (cq&3), byte b =
+ *                                    channel 4cq+b, bits 2s = token 4tq+s
  *            +pg_vscale  f32 [G][ng] V scale per token and channel group
  *            +pg_vzero   i32 [G][ng]
- *            +pg_vcodes  u8  [G][d/4]
+ *            +pg_vcodes  u32 [G*d/16] V codes as tile words: word
+ *                                    ((tq>>2)*d/4 + cq)*4 + (tq&3), byte b =
+ *                                    token 4tq+b's S:146 byte for channels
+ *                                    4cq..4cq+3 (bits 2s = channel 4cq+s)
  *  ring    [U][slots][2][d] 16-bit     recent-window rows, ORIGINAL basis
  *                                      (R10); token t lives in slot t % slots
  *  bitmask [U][bitmask_words] u32      bit t = token t salient (R2, R11, R12)
