@@ -22,7 +22,8 @@
 //    (two signed int8 limbs); sum_c Q_c code_tc for all G tokens is one warp-MMA
 //    contraction (IMMA m16n8k32: A = LOP3-masked K tile words, rows = tokens;
 //    B = the limbs, columns = 2 per head), exact in int32;
-//    logit = delta (sum - sum_c Q_c z_c).  (Per-token K keeps dp4a.)
+//    logit = delta (sum - sum_c Q_c z_c).  Per-token K: the same MMA, folded per
+//    channel group with the token's scale and zero point.
 //  pages, values: w_t = p_t s^V_t rounded to a 16-bit fixed point of the page's
 //    largest weight (two uint8 limbs); sum_t W_t code_tc is the second warp-MMA
 //    contraction (A = masked V tile words, rows = channels):
@@ -565,15 +566,14 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       mbar_wait(&bar[st], par);
       const float4 *ks4 = reinterpret_cast<const float4 *>(B + c.pg_kscale);
       const int4 *kz4 = reinterpret_cast<const int4 *>(B + c.pg_kzero);
-      const uint4 *kc4 = reinterpret_cast<const uint4 *>(B + c.pg_kcodes);
       if constexpr (KT) {                      // per-token K variant (compile time)
         // ---- per-token K (NEXT-1): Q_c = rn(q~_c / delta) once per page,
-        // logit_t = alpha delta sum_g s_tg (sum_{c in g} Q_c code_tc - z_tg SQ_g)
+        // logit_t = alpha delta sum_g s_tg (sum_{c in g} Q_c code_tc - z_tg SQ_g);
+        // the inner sums by the same warp MMA as the per-channel path, folded
+        // per channel group (a 32-channel chunk lies in one group: G >= 32)
         const float *ksT = reinterpret_cast<const float *>(B + c.pg_kscale);    // [G][NG]
         const int32_t *kzT = reinterpret_cast<const int32_t *>(B + c.pg_kzero);
-        constexpr int IPG = (G / 16) / KCS > 0 ? (G / 16) / KCS : 1;   // K iterations per group
-        float dT[NH];
-        int sq16[NH];                                // lanes 4cg..4cg+3: sum of Q over cg's 16 channels
+        float dT[NH], sqg[NH][NG];
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
           float qv4[4] = {0.f, 0.f, 0.f, 0.f}, am = 0.f;
@@ -588,75 +588,79 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           int Qv[4];
 #pragma unroll
           for (int b = 0; b < 4; ++b) Qv[b] = __float2int_rn(qv4[b] * inv);
+          // SQ_g = sum of Q over channel group g (lanes g*G/4 .. (g+1)*G/4 - 1)
           int sq = (Qv[0] + Qv[1]) + (Qv[2] + Qv[3]);
-          sq += __shfl_xor_sync(0xffffffffu, sq, 1);
-          sq += __shfl_xor_sync(0xffffffffu, sq, 2);
-          sq16[h] = sq;
+#pragma unroll
+          for (int o = 1; o < G / 4 && o < 32; o <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+#pragma unroll
+          for (int gi = 0; gi < NG; ++gi) sqg[h][gi] = (float)__shfl_sync(0xffffffffu, sq, (gi * (G / 4)) & 31);
           if (lane < CQ) {
-            const uint32_t lo = prmt(prmt(Qv[0], Qv[1], 0x0040), prmt(Qv[2], Qv[3], 0x0040), 0x5410);
-            const uint32_t hi = prmt(prmt(Qv[0], Qv[1], 0x0051), prmt(Qv[2], Qv[3], 0x0051), 0x5410);
-            uint32_t *kl = klimb + (h * CG + (lane >> 2)) * 8 + (lane & 3);
-            kl[0] = lo;
-            kl[4] = hi;
+            const uint32_t x0 = Qv[0] + 128, x1 = Qv[1] + 128, x2 = Qv[2] + 128, x3 = Qv[3] + 128;
+            qlimb[(2 * h) * CQ + lane] = prmt(prmt(x0, x1, 0x0040), prmt(x2, x3, 0x0040), 0x5410) ^ 0x80808080u;
+            qlimb[(2 * h + 1) * CQ + lane] = prmt(prmt(x0, x1, 0x0051), prmt(x2, x3, 0x0051), 0x5410);
           }
         }
         __syncwarp();
-        int acc[NH][4][2], zacc[NH];                // zacc: sum of Q over the folded cgs
-        float part[NH][4];
+        constexpr int KC = D / 32, CPG = G / 32;     // chunks, chunks per channel group
+        uint32_t bq[KC][2];
 #pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          zacc[h] = 0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) { acc[h][k][0] = 0; acc[h][k][1] = 0; part[h][k] = 0.f; }
+        for (int cc = 0; cc < KC; ++cc) {
+          const uint2 b = *reinterpret_cast<const uint2 *>(qlimb + mcol * CQ + 8 * cc + 2 * mt);
+          bq[cc][0] = b.x;
+          bq[cc][1] = b.y;
         }
+        float dsel = dT[0], ssel[NG];
 #pragma unroll
-        for (int i = 0; i < CG / KCS; ++i) {
-          const int cg = kcs + KCS * i;
-          const uint4 w4 = kc4[cg * TQ + ktq];
-          const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
+        for (int gi = 0; gi < NG; ++gi) ssel[gi] = sqg[0][gi];
 #pragma unroll
-          for (int h = 0; h < NH; ++h) {
-            const uint4 lo4 = reinterpret_cast<const uint4 *>(klimb + (h * CG + cg) * 8)[0];
-            const uint4 hi4 = reinterpret_cast<const uint4 *>(klimb + (h * CG + cg) * 8)[1];
-            const uint32_t lo[4] = {lo4.x, lo4.y, lo4.z, lo4.w};
-            const uint32_t hi[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
+        for (int h = 1; h < NH; ++h)
+          if (mt == h) {
+            dsel = dT[h];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint32_t x = fmask(wd[j], k);
-                acc[h][k][0] = dp4a_uu(x, lo[j], acc[h][k][0]);
-                acc[h][k][1] = dp4a_us(x, hi[j], acc[h][k][1]);
-              }
+            for (int gi = 0; gi < NG; ++gi) ssel[gi] = sqg[h][gi];
           }
+        const uint32_t *kcw = reinterpret_cast<const uint32_t *>(B + c.pg_kcodes);
+        AKVQ_UNROLL(AKVQ_KU)
+        for (int blk = 0; blk < TQ / 8; ++blk) {
+          const int tq = 8 * blk + mg;
+          float part[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int h = 0; h < NH; ++h) zacc[h] += __shfl_sync(0xffffffffu, sq16[h], 4 * cg);
-          if ((i + 1) % IPG == 0) {                  // group of cg ends: fold with s_tg, z_tg
-            const int gi = (cg * 16) / G;
+          for (int gi = 0; gi < NG; ++gi) {
+            int c01[4] = {0, 0, 0, 0}, c23[4] = {0, 0, 0, 0};
 #pragma unroll
-            for (int h = 0; h < NH; ++h) {
-              const float sqg = (float)zacc[h];
-              zacc[h] = 0;
+            for (int j = 0; j < CPG; ++j) {
+              const int cc = gi * CPG + j;
+              const uint2 w = *reinterpret_cast<const uint2 *>(kcw + kword_idx(8 * cc + 2 * mt, tq, TQ));
+              mma_u8s8(c01, fmask(w.x, 0), fmask(w.x, 1), fmask(w.y, 0), fmask(w.y, 1), bq[cc][0], bq[cc][1]);
+              mma_u8s8(c23, fmask(w.x, 2), fmask(w.x, 3), fmask(w.y, 2), fmask(w.y, 3), bq[cc][0], bq[cc][1]);
+            }
+            const int tot[4] = {c01[1] * 256 + c01[0], c23[1] * 256 + c23[0], c01[3] * 256 + c01[2],
+                                c23[3] * 256 + c23[2]};
+            // tot[0]: token 4tq+0 (x1), tot[2]: 4tq+1 (x4), tot[1]: 4tq+2 (x16), tot[3]: 4tq+3 (x64)
+            const float t0 = (float)tot[0], t1 = (float)tot[2] * 0.25f, t2 = (float)tot[1] * 0.0625f,
+                        t3 = (float)tot[3] * 0.015625f;
+            const float tk[4] = {t0, t1, t2, t3};
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int mi = (4 * ktq + k) * NG + gi;
-                const float tot = (float)(acc[h][k][1] * 256 + acc[h][k][0]) * (1.0f / (float)(1 << (2 * k)));
-                part[h][k] = fmaf(ksT[mi], tot - (float)kzT[mi] * sqg, part[h][k]);
-                acc[h][k][0] = 0;
-                acc[h][k][1] = 0;
-              }
+            for (int k = 0; k < 4; ++k) {
+              const int mi = (4 * tq + k) * NG + gi;
+              part[k] = fmaf(ksT[mi], tk[k] - (float)kzT[mi] * ssel[gi], part[k]);
             }
           }
-        }
-#pragma unroll
-        for (int h = 0; h < NH; ++h)
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            float tot = part[h][k];
-#pragma unroll
-            for (int off = TQ; off < 32; off <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-            lg[h][k] = ((sbits >> k) & 1u) ? -INFINITY : tot * dT[h];
+          if (mt < NH) {
+            float4 r;
+            r.x = part[0] * dsel; r.y = part[1] * dsel; r.z = part[2] * dsel; r.w = part[3] * dsel;
+            reinterpret_cast<float4 *>(lgs + mt * G)[tq] = r;
           }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const float4 r = reinterpret_cast<const float4 *>(lgs + h * G)[ktq];
+          lg[h][0] = (sbits & 1u) ? -INFINITY : r.x;
+          lg[h][1] = (sbits & 2u) ? -INFINITY : r.y;
+          lg[h][2] = (sbits & 4u) ? -INFINITY : r.z;
+          lg[h][3] = (sbits & 8u) ? -INFINITY : r.w;
+        }
       } else {
       float dA[NH], bA[NH];
 #pragma unroll
