@@ -153,10 +153,16 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
       }
       while (r < NR) lp.tab[k++] = row_item(r++);
     }
-    // item costs (~ warp instructions, profiles/r01_final_summary.md): a page is
-    // two 5 KB sub-loads of dp4a work (~1440), a ring chunk of 8 16-bit rows and a
-    // PSA side split ~400, a TSA side split (up to 32 4-bit rows each pass) ~1200
-    const int c_page = 7, c_rows = 2, c_side = f.kind == AKVQ_TSA ? 6 : 2;
+    // item costs (relative time; profiles/r01_final_summary.md): a page (two 5 KB
+    // sub-loads of MMA work), a ring chunk of 8 16-bit rows and a PSA side split,
+    // a TSA side split (up to 32 4-bit rows each pass)
+#ifndef AKVQ_CPAGE
+#define AKVQ_CPAGE 7
+#endif
+#ifndef AKVQ_CROWS
+#define AKVQ_CROWS 2
+#endif
+    const int c_page = AKVQ_CPAGE, c_rows = AKVQ_CROWS, c_side = f.kind == AKVQ_TSA ? 6 : 2;
     lp.cu = lp.P * c_page + lp.Rc * c_rows + lp.Sc * c_side;   // <= 2048 * 7 < 2^16
     if (build_tab && lp.per_u <= kLyMaxTab) {
       int acc = 0;

@@ -44,11 +44,12 @@ __device__ __forceinline__ uint8_t *side_ptr(const DevCache &c, int u, int e) {
 // channel) codes; TQ = G/4 token quads, CQ = d/4 channel quads.
 //  K word ((cq>>2)*TQ + tq)*4 + (cq&3): byte b = channel 4cq+b, bits 2s..2s+1 of
 //    that byte = token 4tq+s.  A mask w & (3<<2s per byte) yields the 4 channels'
-//    codes (x4^s) of ONE token: dp4a against 4 channels of q~ is a partial logit.
+//    codes (x4^s) of ONE token: one A-fragment register of the page MMA (rows =
+//    tokens, K = channels).
 //  V word ((tq>>2)*CQ + cq)*4 + (tq&3): byte b = token 4tq+b (that byte is the
 //    token's S:146 byte for channels 4cq..4cq+3), bits 2s = channel 4cq+s.  A
-//    mask yields 4 tokens' codes (x4^s) of ONE channel: dp4a against 4 tokens'
-//    softmax weights is a partial output.
+//    mask yields 4 tokens' codes (x4^s) of ONE channel: one A-fragment register
+//    of the value MMA (rows = channels, K = tokens).
 // Codes themselves are exactly the paper's (Eqs. 3-6); only their byte order is
 // chosen for the decode kernel.
 __host__ __device__ __forceinline__ int kword_idx(int cq, int tq, int TQ) {

@@ -1,5 +1,5 @@
 // decode_common.cuh -- pieces of the persistent decode kernel (k_decode_layer):
-// TMA bulk / mbarrier / dp4a / PDL wrappers, the partial-record layout, the
+// TMA bulk / mbarrier / PDL wrappers, the partial-record layout, the
 // (warp, unit) segment mapping and the per-unit merge (log-sum-exp over
 // segments, output Walsh-Hadamard, Fig. 7 / R4).
 #pragma once
@@ -42,16 +42,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(s));
-  return r;
-}
-__device__ __forceinline__ int dp4a_uu(uint32_t a, uint32_t b, int c) {
-  int r;
-  asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-  return r;
-}
-__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {   // a unsigned, b signed
-  int r;
-  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
   return r;
 }
 // Programmatic dependent launch (PDL) controls.

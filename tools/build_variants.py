@@ -19,7 +19,8 @@ def one(spec):
     objs = []
     for s in b.SOURCES:
         o = os.path.join(b.BUILD, s.replace(".cu", ".o"))
-        if s == "decode_layer.cu" or (s == "api.cu" and "AKVQ_MAX_TAB" in flags):
+        api_only = "AKVQ_C" in flags and "AKVQ_MAX_TAB" not in flags
+        if (s == "decode_layer.cu" and not api_only) or (s == "api.cu" and ("AKVQ_MAX_TAB" in flags or api_only)):
             o = os.path.join(out, s.replace(".cu", ".o"))
             subprocess.run([b.NVCC, *b.FLAGS, *flags.split(), "-c", os.path.join(b.CSRC, s), "-o", o], check=True)
         objs.append(o)
