@@ -113,8 +113,9 @@ typedef struct {
  *            TSA: +0 kscale f32[ng], kzero i32[ng], vscale f32[ng],
  *                 vzero i32[ng], then K codes u8[d/2], V codes u8[d/2]
  *                 (4-bit, 2 per byte, low nibble first; clip4, R11)
- *  ticket  [U] u32                     per-unit merge tickets of the fused
- *                                      decode (zeroed at init, self-resetting)
+ *  ticket  [U * hg] u32                merge tickets of the fused decode, one
+ *                                      per unit and GQA head group hg (zeroed
+ *                                      at init, self-resetting)
  *  side_cap = top_k (PSA) or cap (TSA).
  */
 typedef struct {
@@ -276,8 +277,10 @@ akvq_status akvq_dequantize_view(const akvq_cache *c, float *K, float *V,
                                  akvq_stream_t stream);
 
 /* memory_report: host arithmetic over the current L, n_q and the
- * given number of side entries per unit (host value; pass the count the
- * caller read back, or -1 to use top_k for PSA / 0 for TSA). */
+ * given number of side entries per unit (host value, <= n_q; the mean over
+ * units if they differ).  -1 uses min(top_k, n_q) for PSA; a TSA cache must
+ * pass its text-token count (read back from the side_cnt region): -1 is
+ * EINVAL there, because the count lives on the device. */
 akvq_status akvq_memory_report(const akvq_cache *c, int32_t side_entries,
                                akvq_mem_report *host_out);
 

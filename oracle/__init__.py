@@ -46,14 +46,15 @@ class _Cfg(C.Structure):
     _fields_ = [("U", C.c_int), ("g", C.c_int), ("d", C.c_int), ("G", C.c_int),
                 ("R", C.c_int), ("capacity", C.c_int), ("top_k", C.c_int),
                 ("kind", C.c_int), ("dtype16", C.c_int), ("clip2", C.c_float),
-                ("clip4", C.c_float), ("k_axis", C.c_int)]
+                ("clip4", C.c_float), ("k_axis", C.c_int), ("decide64", C.c_int)]
 
 
 class _Export(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in (
-        "kcodes", "vcodes", "kscale", "kzero", "vscale", "vzero", "kscale32",
-        "vscale32", "salient", "side_index", "side_count", "side16", "side4",
-        "side4_scale", "side4_zero", "xs_k", "xs_v")]
+        "kcodes", "vcodes", "kscale", "kzero", "vscale", "vzero", "kscale_raw",
+        "vscale_raw", "kzpre", "vzpre", "kpre", "vpre", "salient", "side_index",
+        "side_count", "side16", "side4", "side4_scale", "side4_zero", "side4_zpre",
+        "side4_pre", "xs_k", "xs_v")]
 
 
 _lib = None
@@ -70,6 +71,8 @@ def lib():
         L.orc_quantize_group.argtypes = [P, P, C.c_int, C.c_int, C.c_int, C.c_float,
                                          P, P, P, C.c_int]
         L.orc_quantize_group.restype = None
+        L.orc_quantize_group64.argtypes = [P, P, C.c_int, C.c_int, C.c_float, P, P, P, P]
+        L.orc_quantize_group64.restype = None
         L.orc_pack.argtypes = [P, C.c_int, C.c_int, P]
         L.orc_pack.restype = None
         L.orc_unpack.argtypes = [P, C.c_int, C.c_int, P]
@@ -141,6 +144,20 @@ def quantize_group(x, bits: int, clip: float, skip=None):
     return float(s[0]), int(z[0]), codes
 
 
+def quantize_group64(x, bits: int, clip: float, skip=None):
+    """Eqs. 3,5,6 with fp64 decisions; returns (scale, zero, codes, zpre)."""
+    x = np.ascontiguousarray(x, np.float64)
+    n = x.shape[0]
+    sk = None if skip is None else np.ascontiguousarray(skip, np.uint8)
+    s = np.zeros(1, np.float64)
+    z = np.zeros(1, np.int32)
+    zp = np.zeros(1, np.float64)
+    codes = np.zeros(n, np.uint8)
+    lib().orc_quantize_group64(_p(x), _p(sk), n, bits, float(clip), _p(s), _p(z), _p(zp),
+                               _p(codes))
+    return float(s[0]), int(z[0]), codes, float(zp[0])
+
+
 def pack(codes, bits: int) -> np.ndarray:
     codes = np.ascontiguousarray(codes, np.uint8)
     per = 8 // bits
@@ -189,6 +206,7 @@ class OracleConfig:
     clip2: float = 0.8
     clip4: float = 1.0
     k_axis: int = 0          # 0 per channel (R1), 1 per token (NEXT-1)
+    decide64: int = 1        # quantizer decisions in fp64; 0: fp32 (R6)
 
 
 class OracleCache:
@@ -197,7 +215,7 @@ class OracleCache:
     def __init__(self, cfg: OracleConfig):
         self.cfg = cfg
         c = _Cfg(cfg.U, cfg.g, cfg.d, cfg.G, cfg.R, cfg.capacity, cfg.top_k, cfg.kind,
-                 cfg.dtype16, cfg.clip2, cfg.clip4, cfg.k_axis)
+                 cfg.dtype16, cfg.clip2, cfg.clip4, cfg.k_axis, cfg.decide64)
         st = C.c_int(0)
         self._h = lib().orc_new(C.byref(c), C.byref(st))
         if not self._h:
@@ -263,7 +281,10 @@ class OracleCache:
         lib().orc_view(self._h, _p(K), _p(V))
         return K, V
 
-    def export(self) -> dict:
+    def export(self, pre: bool = True) -> dict:
+        """The packed state in the oracle's natural layout (akvq_oracle.h).  With
+        pre=False the per-element pre-round arrays (kpre, vpre, side4_pre) are
+        skipped (they are the size of the cache in fp64)."""
         cfg = self.cfg
         U, d, G, cap, sc = cfg.U, cfg.d, cfg.G, self.cap, self.side_cap
         ng = d // G
@@ -275,8 +296,10 @@ class OracleCache:
             kzero=np.zeros((U, cap // G, d), np.int32),
             vscale=np.zeros((U, cap, ng), np.float64),
             vzero=np.zeros((U, cap, ng), np.int32),
-            kscale32=np.zeros((U, cap // G, d), np.float32),
-            vscale32=np.zeros((U, cap, ng), np.float32),
+            kscale_raw=np.zeros((U, cap // G, d), np.float64),
+            vscale_raw=np.zeros((U, cap, ng), np.float64),
+            kzpre=np.zeros((U, cap // G, d), np.float64),
+            vzpre=np.zeros((U, cap, ng), np.float64),
             salient=np.zeros((U, cap), np.uint8),
             side_index=np.zeros((U, scx), np.int32),
             side_count=np.zeros((U,), np.int32),
@@ -284,14 +307,21 @@ class OracleCache:
             side4=np.zeros((U, scx, 2, d // 2), np.uint8),
             side4_scale=np.zeros((U, scx, 2, ng), np.float64),
             side4_zero=np.zeros((U, scx, 2, ng), np.int32),
-            xs_k=np.zeros((U, cap, d), np.float32),
-            xs_v=np.zeros((U, cap, d), np.float32),
+            side4_zpre=np.zeros((U, scx, 2, ng), np.float64),
+            xs_k=np.zeros((U, cap, d), np.float64),
+            xs_v=np.zeros((U, cap, d), np.float64),
         )
-        ex = _Export(*[_p(a[n]) for n, _ in _Export._fields_])
+        if pre:
+            a["kpre"] = np.zeros((U, cap, d), np.float64)
+            a["vpre"] = np.zeros((U, cap, d), np.float64)
+            a["side4_pre"] = np.zeros((U, scx, 2, d), np.float64)
+        ex = _Export(*[_p(a.get(n)) for n, _ in _Export._fields_])
         lib().orc_export(self._h, C.byref(ex))
-        for k in ("side_index", "side16", "side4", "side4_scale", "side4_zero"):
-            a[k] = a[k][:, :sc]
+        for k in ("side_index", "side16", "side4", "side4_scale", "side4_zero", "side4_zpre",
+                  "side4_pre"):
+            if k in a:
+                a[k] = a[k][:, :sc]
         if cfg.k_axis == 1:      # per-token K meta: [U][cap][d/G] (same element count)
-            for k in ("kscale", "kzero", "kscale32"):
+            for k in ("kscale", "kzero", "kscale_raw", "kzpre"):
                 a[k] = a[k].reshape(U, cap, ng)
         return a

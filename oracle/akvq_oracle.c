@@ -40,18 +40,22 @@ struct orc_cache {
   double *Hs;     /* +-1 Walsh-Hadamard matrix H_s = sqrt(d) H            */
   uint16_t *K, *V;      /* [U][cap][d] original 16-bit rows, every token  */
   uint8_t *sal;         /* [U][cap] salient flag                           */
-  float *xk, *xv;       /* [U][cap][d] fp32 K.H_s, V.H_s (decision inputs) */
+  double *xk, *xv;      /* [U][cap][d] K.H_s, V.H_s decision inputs: fp64, or
+                           rounded once to fp32 in the fp32-decision mode  */
   uint8_t *kc, *vc;     /* [U][cap][d] unpacked 2-bit codes                */
-  float *ks32;          /* [U][cap/G][d] K scale (unnormalized units)      */
+  double *ks;           /* [U][cap/G][d] K scale (unnormalized units)      */
   int32_t *kz;          /* [U][cap/G][d] K zero point                      */
-  float *vs32;          /* [U][cap][d/G] V scale (unnormalized units)      */
+  double *kzp;          /* [U][cap/G][d] clipped_min / scale before rounding */
+  double *vs;           /* [U][cap][d/G] V scale (unnormalized units)      */
   int32_t *vz;          /* [U][cap][d/G] V zero point                      */
+  double *vzp;          /* [U][cap][d/G] clipped_min / scale before rounding */
   int32_t *side_idx;    /* [U][side_cap] token index of each side entry    */
   int32_t *side_cnt;    /* [U]                                             */
   int32_t *side_pos;    /* [U][cap] side entry of token t (or -1)          */
   uint8_t *s4c;         /* [U][side_cap][2][d] unpacked 4-bit codes (TSA)  */
-  float *s4s32;         /* [U][side_cap][2][d/G]                           */
+  double *s4s;          /* [U][side_cap][2][d/G]                           */
   int32_t *s4z;         /* [U][side_cap][2][d/G]                           */
+  double *s4zp;         /* [U][side_cap][2][d/G]                           */
 };
 
 static int is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
@@ -131,21 +135,75 @@ double orc_half_to_double(uint16_t h, int dtype16) {
 /* round = round-half-to-even (R7).  Degenerate group (clipped range <  */
 /* 1e-12): scale = the constant, zero 0, codes 1 (R8).  Empty    */
 /* group (all elements skipped): scale 0, zero 0, codes 0 (R8).         */
-/* Every step is an fp32 IEEE operation (R6); skipped elements get 0.   */
-void orc_quantize_group(const float *x, const uint8_t *skip, int n, int stride,
-                        int bits, float clip, float *scale, int32_t *zero,
-                        uint8_t *codes, int code_stride) {
+/* Skipped (salient) elements get code 0.                                */
+/* Two decision precisions (R6): fp64 (the default of the cache, SURVEY  */
+/* 8(c)) and IEEE fp32 (the kernel's precision, used as a second,        */
+/* bit-exact cross-check).  The clip ratio is the fp32 constant widened  */
+/* exactly in both.  zpre receives clipped_min / scale before rounding   */
+/* (the zero-point tie test of the parity checker).                      */
+static int32_t zero_to_i32(double zf) {
+  if (zf > 2147483647.0) return 2147483647;
+  if (zf < -2147483648.0) return (int32_t)0x80000000u;
+  return (int32_t)zf;
+}
+
+static void qgroup64(const double *x, const uint8_t *skip, int n, int stride, int bits,
+                     double clip, double *scale, int32_t *zero, double *zpre,
+                     uint8_t *codes, int code_stride) {
+  const int levels = (1 << bits) - 1;
+  int any = 0;
+  double mx = 0.0, mn = 0.0;
+  for (int i = 0; i < n; ++i) {
+    if (skip && skip[i]) continue;
+    const double v = x[(long)i * stride];
+    if (!any) { mx = v; mn = v; any = 1; }
+    else { if (v > mx) mx = v; if (v < mn) mn = v; }
+  }
+  *zpre = NAN;                               /* no rounding decision      */
+  if (!any) {
+    *scale = 0.0; *zero = 0;
+    for (int i = 0; i < n; ++i) codes[(long)i * code_stride] = 0;
+    return;
+  }
+  const double cmx = clip * mx;              /* clipped_max(X) */
+  const double cmn = clip * mn;              /* clipped_min(X) */
+  const double range = cmx - cmn;
+  if (range < 1e-12) {                       /* degenerate constant group */
+    *scale = mx; *zero = 0;
+    for (int i = 0; i < n; ++i)
+      codes[(long)i * code_stride] = (skip && skip[i]) ? 0 : 1;
+    return;
+  }
+  const double s = range / (double)levels;   /* Eq. 5 */
+  *zpre = cmn / s;
+  const double zf = -rint(cmn / s);          /* Eq. 6 */
+  for (int i = 0; i < n; ++i) {
+    if (skip && skip[i]) { codes[(long)i * code_stride] = 0; continue; }
+    double q = rint(x[(long)i * stride] / s) + zf;               /* Eq. 3 */
+    if (q < 0.0) q = 0.0;
+    if (q > (double)levels) q = (double)levels;
+    codes[(long)i * code_stride] = (uint8_t)q;
+  }
+  *scale = s;
+  *zero = zero_to_i32(zf);
+}
+
+/* The same steps with every operation an IEEE fp32 operation (R6). */
+static void qgroup32(const double *x, const uint8_t *skip, int n, int stride, int bits,
+                     float clip, double *scale, int32_t *zero, double *zpre,
+                     uint8_t *codes, int code_stride) {
   const int levels = (1 << bits) - 1;
   int any = 0;
   float mx = 0.0f, mn = 0.0f;
   for (int i = 0; i < n; ++i) {
     if (skip && skip[i]) continue;
-    const float v = x[(long)i * stride];
+    const float v = (float)x[(long)i * stride];
     if (!any) { mx = v; mn = v; any = 1; }
     else { if (v > mx) mx = v; if (v < mn) mn = v; }
   }
+  *zpre = NAN;                               /* no rounding decision      */
   if (!any) {
-    *scale = 0.0f; *zero = 0;
+    *scale = 0.0; *zero = 0;
     for (int i = 0; i < n; ++i) codes[(long)i * code_stride] = 0;
     return;
   }
@@ -159,19 +217,44 @@ void orc_quantize_group(const float *x, const uint8_t *skip, int n, int stride,
     return;
   }
   const float s = range / (float)levels;     /* Eq. 5 */
-  const float zf = -rintf(cmn / s);          /* Eq. 6 */
+  const float zq = cmn / s;
+  *zpre = zq;
+  const float zf = -rintf(zq);               /* Eq. 6 */
   for (int i = 0; i < n; ++i) {
     if (skip && skip[i]) { codes[(long)i * code_stride] = 0; continue; }
-    const float r = rintf(x[(long)i * stride] / s);            /* Eq. 3 */
+    const float r = rintf((float)x[(long)i * stride] / s);      /* Eq. 3 */
     double q = (double)r + (double)zf;
     if (q < 0.0) q = 0.0;
     if (q > (double)levels) q = (double)levels;
     codes[(long)i * code_stride] = (uint8_t)q;
   }
   *scale = s;
-  if (zf > 2147483520.0f) *zero = 2147483647;
-  else if (zf < -2147483648.0f) *zero = (int32_t)0x80000000u;
-  else *zero = (int32_t)zf;
+  *zero = zero_to_i32(zf);
+}
+
+static void qgroup(int decide64, const double *x, const uint8_t *skip, int n, int stride,
+                   int bits, float clip, double *scale, int32_t *zero, double *zpre,
+                   uint8_t *codes, int code_stride) {
+  if (decide64)
+    qgroup64(x, skip, n, stride, bits, (double)clip, scale, zero, zpre, codes, code_stride);
+  else
+    qgroup32(x, skip, n, stride, bits, clip, scale, zero, zpre, codes, code_stride);
+}
+
+void orc_quantize_group(const float *x, const uint8_t *skip, int n, int stride,
+                        int bits, float clip, float *scale, int32_t *zero,
+                        uint8_t *codes, int code_stride) {
+  double *xd = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
+  for (int i = 0; i < n; ++i) xd[i] = (double)x[(long)i * stride];
+  double s, zp;
+  qgroup32(xd, skip, n, 1, bits, clip, &s, zero, &zp, codes, code_stride);
+  *scale = (float)s;
+  free(xd);
+}
+
+void orc_quantize_group64(const double *x, const uint8_t *skip, int n, int bits, float clip,
+                          double *scale, int32_t *zero, double *zpre, uint8_t *codes) {
+  qgroup64(x, skip, n, 1, bits, (double)clip, scale, zero, zpre, codes, 1);
 }
 
 /* 2-bit code i -> bits [2(i mod 4), 2(i mod 4)+1] of byte i/4;
@@ -293,7 +376,8 @@ orc_cache *orc_new(const orc_config *cfg, int *status) {
       !(cfg->clip2 > 0.0f && cfg->clip2 <= 1.0f) ||
       !(cfg->clip4 > 0.0f && cfg->clip4 <= 1.0f) ||
       (cfg->kind != ORC_TSA && cfg->kind != ORC_PSA) ||
-      (cfg->k_axis != 0 && cfg->k_axis != 1)) {
+      (cfg->k_axis != 0 && cfg->k_axis != 1) ||
+      (cfg->decide64 != 0 && cfg->decide64 != 1)) {
     if (status) *status = ORC_EINVAL;
     return NULL;
   }
@@ -309,21 +393,24 @@ orc_cache *orc_new(const orc_config *cfg, int *status) {
   c->K = (uint16_t *)calloc((size_t)(U * cap * d), 2);
   c->V = (uint16_t *)calloc((size_t)(U * cap * d), 2);
   c->sal = (uint8_t *)calloc((size_t)(U * cap), 1);
-  c->xk = (float *)calloc((size_t)(U * cap * d), 4);
-  c->xv = (float *)calloc((size_t)(U * cap * d), 4);
+  c->xk = (double *)calloc((size_t)(U * cap * d), 8);
+  c->xv = (double *)calloc((size_t)(U * cap * d), 8);
   c->kc = (uint8_t *)calloc((size_t)(U * cap * d), 1);
   c->vc = (uint8_t *)calloc((size_t)(U * cap * d), 1);
-  c->ks32 = (float *)calloc((size_t)(U * (cap / G) * d), 4);
+  c->ks = (double *)calloc((size_t)(U * (cap / G) * d), 8);
   c->kz = (int32_t *)calloc((size_t)(U * (cap / G) * d), 4);
-  c->vs32 = (float *)calloc((size_t)(U * cap * (d / G)), 4);
+  c->kzp = (double *)calloc((size_t)(U * (cap / G) * d), 8);
+  c->vs = (double *)calloc((size_t)(U * cap * (d / G)), 8);
   c->vz = (int32_t *)calloc((size_t)(U * cap * (d / G)), 4);
+  c->vzp = (double *)calloc((size_t)(U * cap * (d / G)), 8);
   c->side_idx = (int32_t *)calloc((size_t)(U * sc), 4);
   c->side_cnt = (int32_t *)calloc((size_t)U, 4);
   c->side_pos = (int32_t *)malloc(sizeof(int32_t) * U * cap);
   for (long i = 0; i < U * cap; ++i) c->side_pos[i] = -1;
   c->s4c = (uint8_t *)calloc((size_t)(U * sc * 2 * d), 1);
-  c->s4s32 = (float *)calloc((size_t)(U * sc * 2 * (d / G)), 4);
+  c->s4s = (double *)calloc((size_t)(U * sc * 2 * (d / G)), 8);
   c->s4z = (int32_t *)calloc((size_t)(U * sc * 2 * (d / G)), 4);
+  c->s4zp = (double *)calloc((size_t)(U * sc * 2 * (d / G)), 8);
   if (status) *status = ORC_OK;
   return c;
 }
@@ -332,9 +419,9 @@ void orc_free(orc_cache *c) {
   if (!c) return;
   free(c->H); free(c->Hs); free(c->K); free(c->V); free(c->sal);
   free(c->xk); free(c->xv); free(c->kc); free(c->vc);
-  free(c->ks32); free(c->kz); free(c->vs32); free(c->vz);
+  free(c->ks); free(c->kz); free(c->kzp); free(c->vs); free(c->vz); free(c->vzp);
   free(c->side_idx); free(c->side_cnt); free(c->side_pos);
-  free(c->s4c); free(c->s4s32); free(c->s4z);
+  free(c->s4c); free(c->s4s); free(c->s4z); free(c->s4zp);
   free(c);
 }
 
@@ -350,14 +437,14 @@ int orc_nthreads(void) {
 #endif
 }
 
-/* x.H_s of a stored 16-bit row, exact in fp64, then rounded once to fp32
- * (the decision precision, R5/R6). */
-static void rotate_row_fp32(const orc_cache *c, const uint16_t *row, float *out) {
+/* x.H_s of a stored 16-bit row by the explicit fp64 product (R5); in the
+ * fp32-decision mode rounded once to fp32 (R6). */
+static void rotate_row(const orc_cache *c, const uint16_t *row, double *out) {
   const int d = c->cfg.d;
   double x[512], y[512];
   for (int i = 0; i < d; ++i) x[i] = orc_half_to_double(row[i], c->cfg.dtype16);
   matvec(d, c->Hs, x, y);
-  for (int i = 0; i < d; ++i) out[i] = (float)y[i];
+  for (int i = 0; i < d; ++i) out[i] = c->cfg.decide64 ? y[i] : (double)(float)y[i];
 }
 
 /* Quantize block j = tokens [jG, (j+1)G) of unit u (R1):     */
@@ -372,28 +459,28 @@ static void rotate_row_fp32(const orc_cache *c, const uint16_t *row, float *out)
 static void quantize_block(orc_cache *c, int u, int j) {
   const int d = c->cfg.d, G = c->cfg.G, t0 = j * G;
   for (int t = t0; t < t0 + G; ++t) {
-    rotate_row_fp32(c, c->K + ROW(c, u, t), c->xk + ROW(c, u, t));
-    rotate_row_fp32(c, c->V + ROW(c, u, t), c->xv + ROW(c, u, t));
+    rotate_row(c, c->K + ROW(c, u, t), c->xk + ROW(c, u, t));
+    rotate_row(c, c->V + ROW(c, u, t), c->xv + ROW(c, u, t));
   }
   const uint8_t *skip = c->sal + (long)u * c->cap + t0;
   const long mb = ((long)u * (c->cap / G) + j) * d;
-  const int ng = d / G;
+  const int ng = d / G, D64 = c->cfg.decide64;
   if (c->cfg.k_axis == 0) {
     for (int ch = 0; ch < d; ++ch)         /* K per channel over G tokens */
-      orc_quantize_group(c->xk + ROW(c, u, t0) + ch, skip, G, d, 2, c->cfg.clip2,
-                         &c->ks32[mb + ch], &c->kz[mb + ch],
-                         c->kc + ROW(c, u, t0) + ch, d);
+      qgroup(D64, c->xk + ROW(c, u, t0) + ch, skip, G, d, 2, c->cfg.clip2,
+             &c->ks[mb + ch], &c->kz[mb + ch], &c->kzp[mb + ch],
+             c->kc + ROW(c, u, t0) + ch, d);
   } else {
     for (int t = t0; t < t0 + G; ++t) {    /* K per token over G channels */
       const long km = ((long)u * c->cap + t) * ng;
       for (int gi = 0; gi < ng; ++gi) {
         if (c->sal[(long)u * c->cap + t]) {
-          c->ks32[km + gi] = 0.0f; c->kz[km + gi] = 0;
+          c->ks[km + gi] = 0.0; c->kz[km + gi] = 0; c->kzp[km + gi] = NAN;
           memset(c->kc + ROW(c, u, t) + gi * G, 0, (size_t)G);
         } else {
-          orc_quantize_group(c->xk + ROW(c, u, t) + gi * G, NULL, G, 1, 2,
-                             c->cfg.clip2, &c->ks32[km + gi], &c->kz[km + gi],
-                             c->kc + ROW(c, u, t) + gi * G, 1);
+          qgroup(D64, c->xk + ROW(c, u, t) + gi * G, NULL, G, 1, 2, c->cfg.clip2,
+                 &c->ks[km + gi], &c->kz[km + gi], &c->kzp[km + gi],
+                 c->kc + ROW(c, u, t) + gi * G, 1);
         }
       }
     }
@@ -402,12 +489,12 @@ static void quantize_block(orc_cache *c, int u, int j) {
     const long vm = ((long)u * c->cap + t) * ng;
     for (int gi = 0; gi < ng; ++gi) {
       if (c->sal[(long)u * c->cap + t]) {
-        c->vs32[vm + gi] = 0.0f; c->vz[vm + gi] = 0;
+        c->vs[vm + gi] = 0.0; c->vz[vm + gi] = 0; c->vzp[vm + gi] = NAN;
         memset(c->vc + ROW(c, u, t) + gi * G, 0, (size_t)G);
       } else {
-        orc_quantize_group(c->xv + ROW(c, u, t) + gi * G, NULL, G, 1, 2,
-                           c->cfg.clip2, &c->vs32[vm + gi], &c->vz[vm + gi],
-                           c->vc + ROW(c, u, t) + gi * G, 1);
+        qgroup(D64, c->xv + ROW(c, u, t) + gi * G, NULL, G, 1, 2, c->cfg.clip2,
+               &c->vs[vm + gi], &c->vz[vm + gi], &c->vzp[vm + gi],
+               c->vc + ROW(c, u, t) + gi * G, 1);
       }
     }
   }
@@ -418,12 +505,12 @@ static void quantize_block(orc_cache *c, int u, int j) {
     c->side_pos[(long)u * c->cap + t] = e;
     if (c->cfg.kind == ORC_TSA) {
       for (int kv = 0; kv < 2; ++kv) {
-        const float *x = (kv == 0 ? c->xk : c->xv) + ROW(c, u, t);
+        const double *x = (kv == 0 ? c->xk : c->xv) + ROW(c, u, t);
         const long base = (((long)u * c->side_cap + e) * 2 + kv);
         for (int gi = 0; gi < ng; ++gi)
-          orc_quantize_group(x + gi * G, NULL, G, 1, 4, c->cfg.clip4,
-                             &c->s4s32[base * ng + gi], &c->s4z[base * ng + gi],
-                             c->s4c + base * d + gi * G, 1);
+          qgroup(D64, x + gi * G, NULL, G, 1, 4, c->cfg.clip4,
+                 &c->s4s[base * ng + gi], &c->s4z[base * ng + gi], &c->s4zp[base * ng + gi],
+                 c->s4c + base * d + gi * G, 1);
       }
     }
   }
@@ -531,7 +618,7 @@ static void view_row(const orc_cache *c, int u, int t, double *Kh, double *Vh) {
       const long base = ((long)u * c->side_cap + e) * 2 + kv;
       double *out = kv == 0 ? Kh : Vh;
       for (int i = 0; i < d; ++i) {
-        const double s = (double)c->s4s32[base * ng + i / G] * rs;
+        const double s = c->s4s[base * ng + i / G] * rs;
         out[i] = s * ((double)c->s4c[base * d + i] - (double)c->s4z[base * ng + i / G]);
       }
     }
@@ -542,9 +629,9 @@ static void view_row(const orc_cache *c, int u, int t, double *Kh, double *Vh) {
   const long vm = ((long)u * c->cap + t) * ng;
   for (int i = 0; i < d; ++i) {
     const long ki = c->cfg.k_axis == 0 ? mb + i : vm + i / G;   /* per channel | per token */
-    Kh[i] = (double)c->ks32[ki] * rs *
+    Kh[i] = c->ks[ki] * rs *
             ((double)c->kc[ROW(c, u, t) + i] - (double)c->kz[ki]);
-    Vh[i] = (double)c->vs32[vm + i / G] * rs *
+    Vh[i] = c->vs[vm + i / G] * rs *
             ((double)c->vc[ROW(c, u, t) + i] - (double)c->vz[vm + i / G]);
   }
 }
@@ -608,6 +695,13 @@ int orc_decode(const orc_cache *c, const uint16_t *q, double *out,
 }
 
 /* ------------------------------------------------------------------ */
+/* x / scale before rounding, in the decision precision (NaN where no code
+ * was decided: salient slot, empty or degenerate group). */
+static double pre_round(const orc_cache *c, double x, double s, double zpre, int skip) {
+  if (skip || isnan(zpre)) return NAN;
+  return c->cfg.decide64 ? x / s : (double)((float)x / (float)s);
+}
+
 int orc_export(const orc_cache *c, const orc_export_t *ex) {
   const orc_config *f = &c->cfg;
   const long U = f->U, cap = c->cap, d = f->d, G = f->G, ng = d / G;
@@ -618,6 +712,14 @@ int orc_export(const orc_cache *c, const orc_export_t *ex) {
       if (ex->kcodes) orc_pack(c->kc + ROW(c, (int)u, (int)t), (int)d, 2, ex->kcodes + (u * cap + t) * (d / 4));
       if (ex->vcodes) orc_pack(c->vc + ROW(c, (int)u, (int)t), (int)d, 2, ex->vcodes + (u * cap + t) * (d / 4));
       if (ex->salient) ex->salient[u * cap + t] = c->sal[u * cap + t];
+      const int sal = c->sal[u * cap + t];
+      for (long i = 0; i < d; ++i) {
+        const long e = ROW(c, (int)u, (int)t) + i;
+        const long km = f->k_axis == 0 ? (u * (cap / G) + t / G) * d + i : (u * cap + t) * ng + i / G;
+        const long vm = (u * cap + t) * ng + i / G;
+        if (ex->kpre) ex->kpre[e] = pre_round(c, c->xk[e], c->ks[km], c->kzp[km], sal);
+        if (ex->vpre) ex->vpre[e] = pre_round(c, c->xv[e], c->vs[vm], c->vzp[vm], sal);
+      }
     }
     if (ex->side_count) ex->side_count[u] = c->side_cnt[u];
     for (long e = 0; e < sc; ++e) {
@@ -637,24 +739,35 @@ int orc_export(const orc_cache *c, const orc_export_t *ex) {
         const long base = (u * sc + e) * 2 + kv;
         if (ex->side4) orc_pack(c->s4c + base * d, (int)d, 4, ex->side4 + base * (d / 2));
         for (long gi = 0; gi < ng; ++gi) {
-          if (ex->side4_scale) ex->side4_scale[base * ng + gi] = (double)c->s4s32[base * ng + gi] * rs;
+          if (ex->side4_scale) ex->side4_scale[base * ng + gi] = c->s4s[base * ng + gi] * rs;
           if (ex->side4_zero) ex->side4_zero[base * ng + gi] = c->s4z[base * ng + gi];
+          if (ex->side4_zpre) ex->side4_zpre[base * ng + gi] = have ? c->s4zp[base * ng + gi] : NAN;
         }
+        if (ex->side4_pre)
+          for (long i = 0; i < d; ++i) {
+            const double x = have ? (kv == 0 ? c->xk : c->xv)[ROW(c, (int)u, t) + i] : 0.0;
+            ex->side4_pre[base * d + i] =
+                have && f->kind == ORC_TSA
+                    ? pre_round(c, x, c->s4s[base * ng + i / G], c->s4zp[base * ng + i / G], 0)
+                    : NAN;
+          }
       }
     }
   }
   const long nk = U * (cap / G) * d, nv = U * cap * ng;
   for (long i = 0; i < nk; ++i) {
-    if (ex->kscale) ex->kscale[i] = (double)c->ks32[i] * rs;
-    if (ex->kscale32) ex->kscale32[i] = c->ks32[i];
+    if (ex->kscale) ex->kscale[i] = c->ks[i] * rs;
+    if (ex->kscale_raw) ex->kscale_raw[i] = c->ks[i];
     if (ex->kzero) ex->kzero[i] = c->kz[i];
+    if (ex->kzpre) ex->kzpre[i] = c->kzp[i];
   }
   for (long i = 0; i < nv; ++i) {
-    if (ex->vscale) ex->vscale[i] = (double)c->vs32[i] * rs;
-    if (ex->vscale32) ex->vscale32[i] = c->vs32[i];
+    if (ex->vscale) ex->vscale[i] = c->vs[i] * rs;
+    if (ex->vscale_raw) ex->vscale_raw[i] = c->vs[i];
     if (ex->vzero) ex->vzero[i] = c->vz[i];
+    if (ex->vzpre) ex->vzpre[i] = c->vzp[i];
   }
-  if (ex->xs_k) memcpy(ex->xs_k, c->xk, sizeof(float) * U * cap * d);
-  if (ex->xs_v) memcpy(ex->xs_v, c->xv, sizeof(float) * U * cap * d);
+  if (ex->xs_k) memcpy(ex->xs_k, c->xk, sizeof(double) * U * cap * d);
+  if (ex->xs_v) memcpy(ex->xs_v, c->xv, sizeof(double) * U * cap * d);
   return ORC_OK;
 }

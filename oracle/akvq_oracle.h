@@ -12,11 +12,11 @@
  * paper is silent are the DESIGN.md "Readings" list (R1..Rn).
  *
  * Arithmetic: fp64 everywhere, with an explicit d x d Walsh-Hadamard matrix
- * built by the recursion of Eq. 7.  The single exception is the
- * integer decisions of Eqs. 3, 5, 6 -- min/max, clipping,
- * scale, zero point and code -- which are taken in IEEE fp32 on both sides
- * (R6, "decisions in the kernel's precision"), on inputs that are
- * exact in fp32 (K.H_s of 16-bit inputs, R5).
+ * built by the recursion of Eq. 7.  The integer decisions of
+ * Eqs. 3, 5, 6 -- min/max, clipping, scale, zero point and code --
+ * are taken in fp64 by default; orc_config.decide64 = 0 takes
+ * them in IEEE fp32 instead, the kernel's precision (R6), as a second
+ * cross-check in which codes agree bit for bit.
  */
 #ifndef AKVQ_ORACLE_H
 #define AKVQ_ORACLE_H
@@ -46,6 +46,8 @@ typedef struct {
   int k_axis;     /* 0: K per channel over G-token blocks (R1, graded);
                      1: K per token over G-channel groups, the paper-literal
                      "per-token dynamic" rule of P:246       */
+  int decide64;   /* 1: quantizer decisions in fp64 (default); 0: in IEEE
+                     fp32 on the fp32-rounded x.H_s (R6)                     */
 } orc_config;
 
 typedef struct orc_cache orc_cache;
@@ -62,6 +64,10 @@ int  orc_rotate(int d, int normalized, const double *x, double *y);
 void orc_quantize_group(const float *x, const uint8_t *skip, int n, int stride,
                         int bits, float clip, float *scale, int32_t *zero,
                         uint8_t *codes, int code_stride);
+/* The same in fp64 (clip is the fp32 constant widened exactly); zpre =
+ * clipped_min / scale before rounding (NaN for empty / degenerate groups). */
+void orc_quantize_group64(const double *x, const uint8_t *skip, int n, int bits, float clip,
+                          double *scale, int32_t *zero, double *zpre, uint8_t *codes);
 /* S:146 bit layout. */
 void orc_pack(const uint8_t *codes, int n, int bits, uint8_t *out);
 void orc_unpack(const uint8_t *in, int n, int bits, uint8_t *codes);
@@ -104,23 +110,31 @@ int  orc_view(const orc_cache *c, double *K, double *V);
  *  kcodes, vcodes [U][cap][d/4] (S:146 packing along channels)
  *  kscale [U][cap/G][d] (normalized, fp64), kzero [U][cap/G][d]
  *  vscale [U][cap][d/G], vzero [U][cap][d/G]
- *  kscale32 / vscale32: the fp32 unnormalized decision scales (tie checks)
+ *  kscale_raw / vscale_raw: the unnormalized decision scales
+ *  kzpre / vzpre: clipped_min / scale before rounding (zero-point tie test;
+ *      NaN where no zero point was decided)
+ *  kpre, vpre [U][cap][d]: x / scale before rounding (code tie test; NaN for
+ *      salient slots, empty and degenerate groups), in decision precision
  *  salient [U][cap] (0/1)
  *  side_index [U][side_cap], side_count [U]
  *  side16 [U][side_cap][2][d]   (PSA: original 16-bit K row then V row)
- *  side4 [U][side_cap][2][d/2], side4_scale/zero [U][side_cap][2][d/G] (TSA)
- *  xs_k, xs_v [U][cap][d]: the fp32 K.H_s / V.H_s values decisions used.
+ *  side4 [U][side_cap][2][d/2], side4_scale/zero/zpre [U][side_cap][2][d/G],
+ *  side4_pre [U][side_cap][2][d] (TSA)
+ *  xs_k, xs_v [U][cap][d]: the K.H_s / V.H_s values the decisions used.
  * Any pointer may be NULL.  cap is rounded up to a multiple of G.          */
 typedef struct {
   uint8_t *kcodes, *vcodes;
   double *kscale; int32_t *kzero;
   double *vscale; int32_t *vzero;
-  float *kscale32, *vscale32;
+  double *kscale_raw, *vscale_raw;
+  double *kzpre, *vzpre;
+  double *kpre, *vpre;
   uint8_t *salient;
   int32_t *side_index, *side_count;
   uint16_t *side16;
   uint8_t *side4; double *side4_scale; int32_t *side4_zero;
-  float *xs_k, *xs_v;
+  double *side4_zpre, *side4_pre;
+  double *xs_k, *xs_v;
 } orc_export_t;
 int orc_export(const orc_cache *c, const orc_export_t *ex);
 int orc_cap_rounded(const orc_cache *c);

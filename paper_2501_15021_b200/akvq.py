@@ -299,5 +299,15 @@ class LayerCache:
         akvq_dequantize_view(self.handle, K, V, stream)
         return K, V
 
+    def side_counts(self) -> torch.Tensor:
+        """Side-table entries per unit (device -> host read of the side_cnt region)."""
+        y = self.layout
+        return self.buf[y.side_cnt_off: y.side_cnt_off + 4 * self.cfg.n_units].view(
+            torch.int32).cpu()
+
     def memory_report(self, side_entries: int = -1):
+        """S:424-432.  For a TSA cache with side_entries = -1 the text-token
+        count is read back from the device (a synchronizing copy)."""
+        if side_entries < 0 and self.cfg.kind == AKVQ_TSA:
+            side_entries = int(round(float(self.side_counts().double().mean())))
         return akvq_memory_report(self.handle, side_entries)

@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <mutex>
 
 #include "akvq.h"
 #include "common.cuh"
@@ -62,13 +63,40 @@ DevCache make_dev(const akvq_cache *c) {
 
 akvq_status cuda_status(cudaError_t e) { return e == cudaSuccess ? AKVQ_OK : AKVQ_ECUDA; }
 
-// Library-wide launch sequence (host).  A cache records the sequence number of
-// its last writing launch; a decode launch may prefetch cache pages before
-// griddepcontrol.wait only if some launch came after that write (then, by PDL
-// ordering, the writer has completed when the decode grid starts).
+// Per-stream record of the library's last kernel launch on that stream and the
+// cache buffer it wrote (NULL: it wrote no cache).  The decode kernel is
+// launched with programmatic dependent launch, so it may start while the
+// PRECEDING kernel of its stream is still running; it may therefore prefetch
+// cache pages before griddepcontrol.wait only if that preceding kernel is known
+// not to write this cache.  Kernels on other streams are ordered by the
+// caller's events (full dependencies), so only the same stream matters.  An
+// unknown stream (never seen, or evicted from the table) disables the prefetch.
 std::atomic<unsigned long long> g_seq{0};
-unsigned long long next_seq() { return g_seq.fetch_add(1) + 1; }
-void mark_write(akvq_cache *c) { c->last_write = next_seq(); }
+std::mutex g_stream_mu;
+struct StreamLast {
+  cudaStream_t s;
+  const void *wrote;
+  bool used;
+};
+StreamLast g_stream_last[64];
+int g_stream_next = 0;
+
+void note_launch(akvq_cache *c, cudaStream_t s, bool wrote) {
+  if (wrote) c->last_write = g_seq.fetch_add(1) + 1;
+  std::lock_guard<std::mutex> lk(g_stream_mu);
+  for (auto &e : g_stream_last)
+    if (e.used && e.s == s) { e.wrote = wrote ? c->base : nullptr; return; }
+  StreamLast &e = g_stream_last[g_stream_next];
+  g_stream_next = (g_stream_next + 1) % 64;
+  e.s = s; e.wrote = wrote ? c->base : nullptr; e.used = true;
+}
+// true if the last library launch on s is known and did not write c
+bool prefetch_safe(const akvq_cache *c, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_stream_mu);
+  for (auto &e : g_stream_last)
+    if (e.used && e.s == s) return e.wrote != c->base;
+  return false;
+}
 
 // Persistent-grid sizes (CTAs per SM) of the two decode kernels; tuning
 // overrides AKVQ_ROW_CTAS / AKVQ_PG_CTAS are read once (experiments only).
@@ -179,6 +207,12 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
       const long long CT = (long long)f.n_units * lp.hg * lp.cu;
       const int ctas = pg_ctas_override() > 0 ? pg_ctas_override() : layer_ctas_per_sm(layer_group_heads(f.q_per_kv));
       const long long wmax = (long long)sms * ctas * layer_warps_per_cta();
+      if (CT >= (1LL << 31) || T >= (1LL << 31)) {   // beyond the plan's 32-bit counters
+        p.fast = 0;
+        lp.per_u = 1;
+        p.S = p.n_page_splits + p.n_ring_splits + p.n_side_splits;
+        return p;
+      }
       lp.T = (int)T;
       // at least min_items items per warp: fewer segments per unit to merge and
       // fewer tickets when the layer is small (W = T would give one item each)
@@ -186,7 +220,6 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
       long long W = wmin_items < wmax ? wmin_items : wmax;
       const int cmax = c_page > c_side ? c_page : c_side;
       if (W > CT / cmax) W = CT / cmax;                   // every warp gets >= 1 item
-      if (CT * W >= (1LL << 31)) W = ((1LL << 31) - 1) / CT;   // 32-bit cost arithmetic
       lp.W = (int)(W < 1 ? 1 : W);
       lp.CT = (int)CT;
       // units one warp can touch: its cost share spans <= share / (cost of the
@@ -217,15 +250,16 @@ akvq_status launch_fast(const akvq_cache *c, DecodePlan &p, const void *q, const
                         const void *v, const uint8_t *types, float *out, void *ws,
                         uint32_t flags, cudaStream_t s) {
   const DevCache d = make_dev(c);
-  if (p.lp.T > 0) const_cast<akvq_cache *>(c)->launches += 1;
-  // prologue prefetch: not right after a write of this cache, and no append in
-  // this launch's own first sub-loads is needed before the wait (the new row is
-  // patched in after the wait)
-  p.lp.prologue = (c->last_write < g_seq.load()) && !(c->options & AKVQ_OPT_STREAM_ONLY) ? 1 : 0;
+  if (p.lp.T <= 0) return AKVQ_OK;                  // nothing to launch
+  const_cast<akvq_cache *>(c)->launches += 1;
+  // prologue prefetch: only if the preceding kernel of this stream does not
+  // write this cache (the new row of a fused step is patched in after the wait)
+  p.lp.prologue = prefetch_safe(c, s) && !(c->options & AKVQ_OPT_STREAM_ONLY) ? 1 : 0;
   const cudaError_t e = launch_decode_layer(d, c->cfg.dtype16, p.lp, q, k, v, types,
                                             static_cast<float *>(ws), out, flags, s);
-  if (k != nullptr) mark_write(const_cast<akvq_cache *>(c));   // the fused step appends
-  else next_seq();
+  // the fused step appends (writes the ring); a plain decode writes only its
+  // self-resetting tickets, which no prologue reads
+  note_launch(const_cast<akvq_cache *>(c), s, k != nullptr);
   return cuda_status(e);
 }
 
@@ -263,7 +297,8 @@ akvq_status akvq_cache_layout(const akvq_config *f, akvq_layout *y) {
   y->side_cnt_off = t; t = align_up(t + U * 4, 256);
   y->side_entry_bytes = f->kind == AKVQ_PSA ? 4 * d : align_up(d + 16 * ng, 16);
   y->side_off = t;     t = align_up(t + U * y->side_cap * y->side_entry_bytes, 256);
-  y->ticket_off = t;   t = align_up(t + U * 4 * 4, 256);   // per virtual unit (<= 4 head groups)
+  // one merge ticket per virtual unit of the decode kernel (unit x GQA head group)
+  y->ticket_off = t;   t = align_up(t + U * (uint64_t)layer_head_groups(f->q_per_kv) * 4, 256);
   y->total_bytes = t;
   return AKVQ_OK;
 }
@@ -290,13 +325,13 @@ akvq_status akvq_cache_init(akvq_cache *c, const akvq_config *f, void *dev_buf, 
   c->sm_count = sms;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint8_t *b = static_cast<uint8_t *>(dev_buf);
-  cudaMemsetAsync(b + y.bitmask_off, 0, (size_t)f->n_units * y.bitmask_words * 4, s);
-  cudaMemsetAsync(b + y.side_cnt_off, 0, (size_t)f->n_units * 4, s);
-  cudaMemsetAsync(b + y.ticket_off, 0, (size_t)f->n_units * 4 * 4, s);
-  if (y.side_cap > 0)
-    cudaMemsetAsync(b + y.side_idx_off, 0xff, (size_t)f->n_units * y.side_cap * 4, s);
-  mark_write(c);
-  return cuda_status(cudaGetLastError());
+  cudaError_t e = cudaMemsetAsync(b + y.bitmask_off, 0, (size_t)f->n_units * y.bitmask_words * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(b + y.side_cnt_off, 0, (size_t)f->n_units * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(b + y.ticket_off, 0, y.total_bytes - y.ticket_off, s);
+  if (e == cudaSuccess && y.side_cap > 0)
+    e = cudaMemsetAsync(b + y.side_idx_off, 0xff, (size_t)f->n_units * y.side_cap * 4, s);
+  note_launch(c, s, true);
+  return cuda_status(e);
 }
 
 akvq_status akvq_select_salient(akvq_cache *c, const uint8_t *types, const float *colsum,
@@ -311,7 +346,7 @@ akvq_status akvq_select_salient(akvq_cache *c, const uint8_t *types, const float
     if (L0 > AKVQ_MAX_PSA_PROMPT) return AKVQ_EUNSUPPORTED;
   }
   const DevCache d = make_dev(c);
-  mark_write(c);
+  note_launch(c, reinterpret_cast<cudaStream_t>(stream), true);
   return cuda_status(launch_salient(d, types, colsum, L0, c->cfg.top_k,
                                     reinterpret_cast<cudaStream_t>(stream)));
 }
@@ -348,6 +383,7 @@ akvq_status akvq_rotate_quantize_pivots(akvq_cache *c, const void *K, const void
     if (launch_salient_from_pivots(d, pivots, counts, n_max, units_per_row, L0,
                                    reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
       return AKVQ_ECUDA;
+    note_launch(c, reinterpret_cast<cudaStream_t>(stream), true);
     c->launches = 1;
   }
   return quantize_prompt(c, K, V, L0, stream);
@@ -382,7 +418,7 @@ static akvq_status quantize_prompt(akvq_cache *c, const void *K, const void *V, 
   cudaError_t e = launch_quantize_blocks(d, f.dtype16, src, 0, nb, nb - 1, s);
   if (e == cudaSuccess) e = launch_ring_fill(d, K, V, L0, n_q, L0, s);
   c->launches += (nb > 0) + (L0 > n_q);
-  mark_write(c);
+  note_launch(c, s, true);
   if (e != cudaSuccess) return AKVQ_ECUDA;
   c->L = L0;
   c->n_q = n_q;
@@ -399,7 +435,7 @@ static akvq_status append_impl(akvq_cache *c, const void *k, const void *v, cons
   cudaError_t e = launch_append(d, k, v, types, c->L, s);
   if (e != cudaSuccess) return AKVQ_ECUDA;
   c->launches += 1;
-  mark_write(c);
+  note_launch(c, s, true);
   c->L += 1;
   if (c->L - f.residual - c->n_q >= f.group) {        // block leaves the window (R9)
     QuantSrc src;
@@ -412,7 +448,7 @@ static akvq_status append_impl(akvq_cache *c, const void *k, const void *v, cons
     e = launch_quantize_blocks(d, f.dtype16, src, j, 1, j, s);
     if (e != cudaSuccess) return AKVQ_ECUDA;
     c->launches += 1;
-    mark_write(c);
+    note_launch(c, s, true);
     c->n_q += f.group;
   }
   return AKVQ_OK;
@@ -453,8 +489,9 @@ static akvq_status decode_impl(const akvq_cache *c, const void *q, float *out, v
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (p.fast) return launch_fast(c, p, q, nullptr, nullptr, nullptr, out, ws, flags, s);
   const_cast<akvq_cache *>(c)->launches += 2;         // split + combine
-  next_seq();
-  return cuda_status(launch_decode(d, c->cfg.dtype16, p, q, out, ws, flags, s));
+  const cudaError_t e = launch_decode(d, c->cfg.dtype16, p, q, out, ws, flags, s);
+  note_launch(const_cast<akvq_cache *>(c), s, false);
+  return cuda_status(e);
 }
 
 akvq_status akvq_decode_attention(const akvq_cache *c, const void *q, float *out, void *ws,
@@ -505,7 +542,13 @@ akvq_status akvq_memory_report(const akvq_cache *c, int32_t side_entries, akvq_m
   const akvq_config &f = c->cfg;
   const double U = f.n_units, d = f.head_dim, G = f.group, ng = d / G;
   int se = side_entries;
-  if (se < 0) se = f.kind == AKVQ_PSA ? (f.top_k < c->n_q ? f.top_k : c->n_q) : 0;
+  if (se < 0) {
+    // PSA: the pivot count is bounded by top_k; TSA: the text-token count lives
+    // on the device only (side_cnt region), so the caller must pass it
+    if (f.kind != AKVQ_PSA) return AKVQ_EINVAL;
+    se = f.top_k < c->n_q ? f.top_k : c->n_q;
+  }
+  if (se > c->n_q) return AKVQ_EINVAL;
   const double ring = (double)(c->L - c->n_q);
   const double quant = (double)c->n_q - se;
   memset(r, 0, sizeof(*r));

@@ -420,7 +420,10 @@ static cudaError_t launch_dec(const DevCache &c, const DecodePlan &p, const void
   float *ws_o = ws_l + (size_t)c.U * p.S * c.g;
   const size_t smem = Smem<D>::floats(c.g) * sizeof(float);
   auto kern = k_decode_split<D, G, DT, MAXG>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    const cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ea != cudaSuccess) return ea;
+  }
   dim3 grid(p.S, c.U);
   kern<<<grid, kThreads, smem, st>>>(c, p, (const uint16_t *)q, ws_m, ws_l, ws_o);
   k_combine<D><<<c.U, D, 0, st>>>(c, p, ws_m, ws_l, ws_o, out, flags);

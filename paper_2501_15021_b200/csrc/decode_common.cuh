@@ -59,34 +59,22 @@ template <int D> struct Rec {
   static constexpr int R = 2 * D + 4;
 };
 
-// Warps of a persistent plan (T work items, W warps, per = items per unit)
-// whose ranges [w*T/W, (w+1)*T/W) intersect unit u's [u*per, (u+1)*per).
-// 32-bit arithmetic: the host guarantees T * W < 2^31 (api.cu plan_decode).
-__device__ __forceinline__ int seg_begin(int T, int W, int w) {
-  return (int)(((unsigned)w * (unsigned)T) / (unsigned)W);
-}
-__device__ __forceinline__ void seg_range(int T, int W, int per, int u, int &w_lo, int &w_hi) {
-  w_lo = 0;
-  w_hi = -1;
-  if (T <= 0 || W <= 0) return;
-  const unsigned i0 = (unsigned)(u * per), i1 = i0 + (unsigned)per;
-  // seg_begin(w) = floor(w T / W): the largest w with seg_begin(w) <= i0 is
-  // ceil((i0 + 1) W / T) - 1, the largest with seg_begin(w) < i1 is ceil(i1 W / T) - 1
-  w_lo = (int)(((i0 + 1u) * (unsigned)W + (unsigned)T - 1u) / (unsigned)T) - 1;
-  w_hi = (int)((i1 * (unsigned)W + (unsigned)T - 1u) / (unsigned)T) - 1;
-  if (w_hi > W - 1) w_hi = W - 1;
-}
-
 // Cost-weighted segments of the layer plan (kernels.h LayerPlan): item i = (u, k)
-// starts at cost u * cu + cpre[k]; warp(i) = floor(start * W / CT).
+// starts at cost u * cu + cpre[k]; warp(i) = floor(start * W / CT).  Products
+// in 64 bits (CT * W may exceed 2^32 for long contexts and large batches).
 __device__ __forceinline__ int ly_warp_of(const LayerPlan &lp, int u, int k) {
-  return (int)(((unsigned)(u * lp.cu + lp.cpre[k]) * (unsigned)lp.W) / (unsigned)lp.CT);
+  const unsigned long long c = (unsigned long long)u * (unsigned)lp.cu + lp.cpre[k];
+  return (int)((c * (unsigned)lp.W) / (unsigned long long)lp.CT);
+}
+// first cost owned by warp w: ceil(w CT / W)
+__device__ __forceinline__ unsigned long long ly_first_cost(const LayerPlan &lp, int w) {
+  return ((unsigned long long)w * (unsigned long long)lp.CT + (unsigned)lp.W - 1u) / (unsigned)lp.W;
 }
 // first item (flattened u * per_u + k) of warp w: the first start cost >= c0
 __device__ __forceinline__ int ly_first_item(const LayerPlan &lp, int w) {
-  const unsigned c0 = ((unsigned)w * (unsigned)lp.CT + (unsigned)lp.W - 1u) / (unsigned)lp.W;
+  const unsigned long long c0 = ly_first_cost(lp, w);
   int u = (int)(c0 / (unsigned)lp.cu);
-  const int r = (int)(c0 - (unsigned)u * (unsigned)lp.cu);
+  const int r = (int)(c0 - (unsigned long long)u * (unsigned)lp.cu);
   int lo = 0, hi = lp.per_u;                          // smallest k with cpre[k] >= r
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
@@ -97,9 +85,9 @@ __device__ __forceinline__ int ly_first_item(const LayerPlan &lp, int w) {
 }
 // unit of warp w's first item (O(1): c0 falls in unit c0 / cu unless past its last start)
 __device__ __forceinline__ int ly_first_unit(const LayerPlan &lp, int w) {
-  const unsigned c0 = ((unsigned)w * (unsigned)lp.CT + (unsigned)lp.W - 1u) / (unsigned)lp.W;
+  const unsigned long long c0 = ly_first_cost(lp, w);
   const int u = (int)(c0 / (unsigned)lp.cu);
-  return (int)(c0 - (unsigned)u * (unsigned)lp.cu) > (int)lp.cpre[lp.per_u - 1] ? u + 1 : u;
+  return (int)(c0 - (unsigned long long)u * (unsigned)lp.cu) > (int)lp.cpre[lp.per_u - 1] ? u + 1 : u;
 }
 
 // Per-unit merge by one warp: log-sum-exp over all segments of unit u, then

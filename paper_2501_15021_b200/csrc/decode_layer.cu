@@ -926,7 +926,10 @@ static cudaError_t launch_ly(const DevCache &c, const LayerPlan &lp, const void 
     else
       return cudaErrorNotSupported;
   }
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    const cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ea != cudaSuccess) return ea;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((lp.W + kLyWarps - 1) / kLyWarps));
   cfg.blockDim = dim3(kLyWarps * 32);

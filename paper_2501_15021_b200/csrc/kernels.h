@@ -36,7 +36,7 @@ struct LayerPlan {
   int stream_only;      // AKVQ_OPT_STREAM_ONLY (profiling)
   // cost-weighted split: item k of a unit starts at cost cpre[k] (cpre[per_u] =
   // cu, the unit's cost); CT = units * cu; warp w owns the items whose start cost
-  // c satisfies floor(c W / CT) == w (host: CT * W < 2^31, CT / W >= max cost)
+  // c satisfies floor(c W / CT) == w (64-bit products; host: CT / W >= max cost)
   int cu, CT;
   int prologue;         // 1: the preceding grid does not write this cache, so the
                         // first TMA sub-loads may be issued before griddepcontrol.wait

@@ -154,7 +154,10 @@ cudaError_t launch_pivot_detect(const void *res, int n_rows, int L0, int hidden,
   else
     k_pivot_scores<AKVQ_FP16><<<g1, kPvScoreWarps * 32, 0, st>>>((const uint16_t *)res, L0, hidden, score_ws);
   const size_t smem = (size_t)L0 * sizeof(float);
-  cudaFuncSetAttribute(k_pivot_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  {
+    const cudaError_t ea = cudaFuncSetAttribute(k_pivot_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (ea != cudaSuccess) return ea;
+  }
   k_pivot_select<<<n_rows, kPvSelThreads, smem, st>>>(score_ws, L0, tau, n_max, pivots, counts);
   return cudaGetLastError();
 }

@@ -400,7 +400,10 @@ cudaError_t launch_salient(const DevCache &c, const uint8_t *types, const float 
   } else {
     if (top_k <= 0) return cudaSuccess;
     const size_t smem = (size_t)L0 * sizeof(float);
-    cudaFuncSetAttribute(k_salient_psa, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    {
+      const cudaError_t ea = cudaFuncSetAttribute(k_salient_psa, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (ea != cudaSuccess) return ea;
+    }
     const int nt = L0 >= 8192 ? 1024 : (L0 >= 1024 ? 512 : 128);
     k_salient_psa<<<c.U, nt, smem, st>>>(c, colsum, L0, top_k);
   }
@@ -413,7 +416,10 @@ static cudaError_t launch_q(const DevCache &c, const QuantSrc &src, int block0, 
   const size_t smem = ((size_t)G * (D + 4) + 2 * (size_t)kQThreads) * sizeof(float);
   auto kern = c.k_axis == AKVQ_K_PER_TOKEN ? k_quantize_blocks<D, G, DT, true>
                                            : k_quantize_blocks<D, G, DT, false>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    const cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ea != cudaSuccess) return ea;
+  }
   dim3 grid(nblocks, c.U);
   kern<<<grid, kQThreads, smem, st>>>(c, src, block0, last_block);
   return cudaGetLastError();

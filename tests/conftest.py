@@ -18,3 +18,18 @@ def orc():
     import oracle
     oracle.build()
     return oracle
+
+
+def pytest_sessionfinish(session, exitstatus):
+    out = os.environ.get("AKVQ_MARGINS_OUT")
+    if not out:
+        return
+    try:
+        import json
+        import parity
+        if parity.MARGINS:
+            os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+            with open(out, "w") as f:
+                json.dump(parity.MARGINS, f, indent=1, sort_keys=True)
+    except Exception as e:          # never fail the session on the report
+        print("margins report failed:", e)

@@ -8,6 +8,19 @@ import torch
 
 TIE_EPS = 1e-5
 
+# Per-test parity margins (worst decode max-abs error vs the 2e-3 bound, tie
+# counts), written to $AKVQ_MARGINS_OUT at the end of the session (conftest).
+MARGINS: dict = {}
+
+
+def record_margin(case: str, worst: float, tol: float, rep: dict | None = None, **extra):
+    m = MARGINS.setdefault(case, {"worst_out_err": 0.0, "tol": tol})
+    m["worst_out_err"] = max(m["worst_out_err"], float(worst))
+    m["margin"] = tol / m["worst_out_err"] if m["worst_out_err"] > 0 else None
+    for k, v in (rep or {}).items():
+        m[k] = m.get(k, 0) + v
+    m.update(extra)
+
 
 def f16_bits(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
@@ -94,85 +107,101 @@ class GpuState:
             self.side4_v = side[:, :, 16 * ng + d // 2: 16 * ng + d]
 
 
-def _code_mismatch_ok(gc, oc, x, s, zf_tie):
-    """A code mismatch is a documented tie iff the oracle's pre-round value x/s is
-    within TIE_EPS of a half-integer (or the group's zero point was a tie)."""
-    with np.errstate(divide="ignore", invalid="ignore"):
-        r = np.abs(np.abs(np.mod(x / s, 1.0)) - 0.5) <= TIE_EPS
-    return (gc == oc) | r | zf_tie
+def _half_tie(pre):
+    """Documented round-half tie: the oracle's pre-round value (x / scale for a
+    code, clipped_min / scale for a zero point) within TIE_EPS of a half-integer
+    (BJ:5, SURVEY 8(c) agreement rules).  NaN (no decision) is never a tie."""
+    with np.errstate(invalid="ignore"):
+        return np.abs(np.abs(np.mod(pre, 1.0)) - 0.5) <= TIE_EPS
+
+
+def _check_groups(tag, gz, oz, zpre, gcodes, ocodes, pre, gidx, levels, rep):
+    """One quantized tier of one unit under the agreement rules.
+      gz, oz, zpre: GPU / oracle zero points and the oracle's clipped_min/scale
+                    per group (any shape, flattened);
+      gcodes, ocodes, pre: codes and the oracle's x/scale per element;
+      gidx: for every element, the flat index of its group.
+    A zero-point mismatch must be a tie with |dz| = 1.  Each code must then equal
+    clamp(rne(pre) + z_gpu, 0, levels) -- the oracle's code, shifted with the
+    GPU's zero point and clamped -- unless pre itself is a tie; elements with no
+    decision (pre NaN: salient slots, empty / degenerate groups) must match
+    exactly."""
+    gz, oz, zpre = gz.reshape(-1).astype(np.int64), oz.reshape(-1).astype(np.int64), zpre.reshape(-1)
+    dz = gz != oz
+    bad = dz & ~(_half_tie(zpre) & (np.abs(gz - oz) == 1))
+    assert not bad.any(), f"{tag}: {int(bad.sum())} zero-point mismatches that are not ties"
+    rep["zero_ties"] += int(dz.sum())
+    gc, oc, pre = gcodes.reshape(-1).astype(np.int64), ocodes.reshape(-1).astype(np.int64), pre.reshape(-1)
+    gidx = gidx.reshape(-1)
+    nod = np.isnan(pre)
+    with np.errstate(invalid="ignore"):
+        exp = np.clip(np.rint(np.where(nod, 0.0, pre)).astype(np.int64) + gz[gidx], 0, levels)
+    exp = np.where(nod, oc, exp)
+    # sanity: with the oracle's own zero point the rule reproduces its codes
+    with np.errstate(invalid="ignore"):
+        own = np.clip(np.rint(np.where(nod, 0.0, pre)).astype(np.int64) + oz[gidx], 0, levels)
+    assert np.array_equal(np.where(nod, oc, own), oc), f"{tag}: checker/oracle disagree"
+    mism = gc != exp
+    bad = mism & ~(_half_tie(pre) & ~nod)
+    assert not bad.any(), f"{tag}: {int(bad.sum())} code mismatches that are not ties"
+    rep["code_ties"] += int(mism.sum())
+    rep["elements"] += gc.size
+
+
+def _scale_ok(tag, g, o):
+    g, o = np.asarray(g, np.float64), np.asarray(o, np.float64)
+    assert np.all(np.abs(g - o) <= 1e-6 * np.abs(o) + 1e-30), \
+        f"{tag}: max rel err {np.max(np.abs(g - o) / (np.abs(o) + 1e-30)):.3g}"
 
 
 def compare_state(gs: GpuState, ex: dict, cfg, report: dict | None = None, units=None):
-    """Assert GPU cache == oracle export on every region (bit-exact modulo ties;
-    scales within 1e-6 relative).  Returns a dict of tie counts."""
+    """Assert GPU cache == oracle export on every region (bit-exact modulo
+    documented ties; scales within 1e-6 relative).  Returns the tie counts."""
     U, d, G = cfg.n_units, cfg.head_dim, cfg.group
+    ng = d // G
     n_q, L = gs.n_q, gs.L
     nb = n_q // G
-    rep = {"k_code_ties": 0, "v_code_ties": 0, "zero_ties": 0, "elements": 0}
+    rep = {"code_ties": 0, "zero_ties": 0, "elements": 0}
     us = range(U) if units is None else units
+    kt = getattr(cfg, "k_axis", 0) == 1
+    tok = np.arange(n_q)
+    ch = np.arange(d)
+    # group index of every element [n_q, d] of a unit's code array
+    kg = (tok[:, None] * ng + ch[None, :] // G) if kt else ((tok[:, None] // G) * d + ch[None, :])
+    vg = tok[:, None] * ng + ch[None, :] // G
     for ui, u in enumerate(us):
-        # bitmask / salient flags over [0, L)
         assert np.array_equal(gs.salient[u, :L], ex["salient"][ui, :L]), f"bitmask u{u}"
-        # side table
         cnt = int(gs.side_cnt[u])
         assert cnt == int(ex["side_count"][ui]), f"side count u{u}"
         assert np.array_equal(gs.side_idx[u, :cnt], ex["side_index"][ui, :cnt]), f"side idx u{u}"
         if nb == 0:
             continue
-        # K meta: per channel per block [nb, d], or per token per group [n_q, ng]
-        kt = getattr(cfg, "k_axis", 0) == 1
         nm = n_q if kt else nb
-        ks_g, ks_o = gs.kscale[u, :nm], ex["kscale"][ui, :nm]
-        assert np.all(np.abs(ks_g - ks_o) <= 1e-6 * np.abs(ks_o) + 1e-30), f"kscale u{u}"
-        kz_g, kz_o = gs.kzero[u, :nm], ex["kzero"][ui, :nm]
-        kc_g = unpack2(gs.kcodes[u, :n_q]).astype(np.int32)
-        kc_o = unpack2(ex["kcodes"][ui, :n_q]).astype(np.int32)
-        x = ex["xs_k"][ui, :n_q].astype(np.float64)
-        ax = 1 if kt else 0          # expand meta to [n_q, d]
-        s32 = np.repeat(ex["kscale32"][ui, :nm].astype(np.float64), G, axis=ax)
-        zt = np.repeat(kz_g != kz_o, G, axis=ax)
-        if np.any(kz_g != kz_o):
-            # zero-point tie: cmn/scale within TIE_EPS of a half-integer
-            rep["zero_ties"] += int((kz_g != kz_o).sum())
-            assert np.all(np.abs(kz_g - kz_o)[kz_g != kz_o] == 1), f"kzero u{u}"
-        ok = _code_mismatch_ok(kc_g, kc_o, x, s32, zt)
-        assert ok.all(), f"K codes u{u}: {int((~ok).sum())} non-tie mismatches"
-        rep["k_code_ties"] += int((kc_g != kc_o).sum())
-        # V meta per token per group and codes
-        vs_g, vs_o = gs.vscale[u, :n_q], ex["vscale"][ui, :n_q]
-        assert np.all(np.abs(vs_g - vs_o) <= 1e-6 * np.abs(vs_o) + 1e-30), f"vscale u{u}"
-        vz_g, vz_o = gs.vzero[u, :n_q], ex["vzero"][ui, :n_q]
-        vzt = vz_g != vz_o
-        rep["zero_ties"] += int(vzt.sum())
-        vc_g = unpack2(gs.vcodes[u, :n_q]).astype(np.int32)
-        vc_o = unpack2(ex["vcodes"][ui, :n_q]).astype(np.int32)
-        xv = ex["xs_v"][ui, :n_q].astype(np.float64)
-        sv = np.repeat(ex["vscale32"][ui, :n_q].astype(np.float64), G, axis=1)
-        ok = _code_mismatch_ok(vc_g, vc_o, xv, sv, np.repeat(vzt, G, axis=1))
-        assert ok.all(), f"V codes u{u}: {int((~ok).sum())} non-tie mismatches"
-        rep["v_code_ties"] += int((vc_g != vc_o).sum())
-        rep["elements"] += 2 * n_q * d
-        # side rows
+        _scale_ok(f"kscale u{u}", gs.kscale[u, :nm], ex["kscale"][ui, :nm])
+        _check_groups(f"K u{u}", gs.kzero[u, :nm], ex["kzero"][ui, :nm], ex["kzpre"][ui, :nm],
+                      unpack2(gs.kcodes[u, :n_q]), unpack2(ex["kcodes"][ui, :n_q]),
+                      ex["kpre"][ui, :n_q], kg, 3, rep)
+        _scale_ok(f"vscale u{u}", gs.vscale[u, :n_q], ex["vscale"][ui, :n_q])
+        _check_groups(f"V u{u}", gs.vzero[u, :n_q], ex["vzero"][ui, :n_q], ex["vzpre"][ui, :n_q],
+                      unpack2(gs.vcodes[u, :n_q]), unpack2(ex["vcodes"][ui, :n_q]),
+                      ex["vpre"][ui, :n_q], vg, 3, rep)
         if cfg.kind == 1:
             assert np.array_equal(gs.side16[u, :cnt], ex["side16"][ui, :cnt]), f"side16 u{u}"
         elif cnt:
+            e = np.arange(cnt)
+            sg = e[:, None] * ng + ch[None, :] // G
             for kv, (sc_g, z_g, c_g) in enumerate((
                     (gs.side4_kscale, gs.side4_kzero, gs.side4_k),
                     (gs.side4_vscale, gs.side4_vzero, gs.side4_v))):
-                so = ex["side4_scale"][ui, :cnt, kv]
-                assert np.all(np.abs(sc_g[u, :cnt] - so) <= 1e-6 * np.abs(so) + 1e-30), "side4 scale"
-                zo = ex["side4_zero"][ui, :cnt, kv]
-                zg = z_g[u, :cnt]
-                rep["zero_ties"] += int((zg != zo).sum())
-                cg = unpack4(c_g[u, :cnt]).astype(np.int32)
-                co = unpack4(ex["side4"][ui, :cnt, kv]).astype(np.int32)
-                mism = cg != co
-                rep["k_code_ties" if kv == 0 else "v_code_ties"] += int(mism.sum())
-                assert mism.sum() <= max(2, 1e-3 * cg.size), f"side4 codes u{u} kv{kv}"
+                _scale_ok(f"side4 scale u{u} kv{kv}", sc_g[u, :cnt], ex["side4_scale"][ui, :cnt, kv])
+                _check_groups(f"side4 u{u} kv{kv}", z_g[u, :cnt], ex["side4_zero"][ui, :cnt, kv],
+                              ex["side4_zpre"][ui, :cnt, kv], unpack4(c_g[u, :cnt]),
+                              unpack4(ex["side4"][ui, :cnt, kv]), ex["side4_pre"][ui, :cnt, kv],
+                              sg, 15, rep)
     if report is not None:
         for k, v in rep.items():
             report[k] = report.get(k, 0) + v
-    total = rep["k_code_ties"] + rep["v_code_ties"]
+    total = rep["code_ties"] + rep["zero_ties"]
     assert total <= max(4, 1e-4 * max(rep["elements"], 1)), f"too many ties: {rep}"
     return rep
 

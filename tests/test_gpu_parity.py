@@ -5,11 +5,13 @@ Sizes: the tiny config (BJ:7) and the 7B shape (BJ:8) in full; the sweep, video 
 Qwen shapes (BJ:9-11) at full size on the GPU with sampled units checked against
 the oracle (first, middle, last unit), in the launch configuration bench.py uses.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
 
-from parity import GpuState, compare_ring, compare_state, f16_bits
+from parity import GpuState, compare_ring, compare_state, f16_bits, record_margin
 
 pytestmark = pytest.mark.gpu
 
@@ -31,7 +33,11 @@ def sy():
     return synth
 
 
-def _configs(ak, orc, w, layer, units_n, kind=None, cap=None, k_axis=0):
+def _case_name():
+    return os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0].split("::")[-1]
+
+
+def _configs(ak, orc, w, layer, units_n, kind=None, cap=None, k_axis=0, decide64=1):
     kind = w.kind(layer) if kind is None else kind
     dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
     cap = w.capacity if cap is None else cap
@@ -39,38 +45,51 @@ def _configs(ak, orc, w, layer, units_n, kind=None, cap=None, k_axis=0):
                           k_axis)
     ocfg = orc.OracleConfig(units_n, w.g, w.d, w.G, w.R, cap, w.top_k, kind,
                             orc.BF16 if dt == ak.AKVQ_BF16 else orc.FP16, w.clip2, w.clip4,
-                            k_axis)
+                            k_axis, decide64)
     return gcfg, ocfg
 
 
 def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every=1,
-              flags=0, report=None, options=0, fused_step=None, k_axis=0):
+              flags=0, report=None, options=0, fused_step=None, k_axis=0, decide64=1,
+              xf_layer=None, xf_decode=None, case=None):
     """Prefill + `steps` decode steps on the GPU for all units; the oracle runs the
     sampled `units` (default all).  Compares state after prefill and after every
-    flush, outputs every `check_every` steps."""
+    flush, outputs every `check_every` steps.  decide64: the oracle's decision
+    precision (1 = fp64, the contract; 0 = fp32, R6).  xf_layer / xf_decode:
+    input transforms (stress cases) applied identically to the GPU inputs and
+    the oracle's sampled inputs.  The worst output error and the tie counts go
+    to the margins report (parity.MARGINS)."""
     U = w.U
     us = list(range(U)) if units is None else list(units)
     gcfg, _ = _configs(ak, orc, w, layer, U, kind, k_axis=k_axis)
-    _, ocfg = _configs(ak, orc, w, layer, len(us), kind, k_axis=k_axis)
+    _, ocfg = _configs(ak, orc, w, layer, len(us), kind, k_axis=k_axis, decide64=decide64)
+    rep = {} if report is None else report
     dev = "cuda"
     inp = sy.layer_inputs(w, layer, device=dev)
+    if xf_layer:
+        inp = xf_layer(inp)
     lc = ak.LayerCache(gcfg, options=options)
     lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
     oc = orc.OracleCache(ocfg)
     inp_o = sy.layer_inputs(w, layer, units=us, device="cpu")
+    if xf_layer:
+        inp_o = xf_layer(inp_o)
     # the CPU-generated sampled units are the GPU's units (counter-based generator)
     assert torch.equal(inp_o["K"], inp["K"][us].cpu())
+    assert torch.equal(inp_o["V"], inp["V"][us].cpu())
     assert oc.prefill(f16_bits(inp_o["K"]), f16_bits(inp_o["V"]), inp_o["types"].numpy(),
                       inp_o["colsum"].numpy()) == 0
     rows_k = [f16_bits(inp_o["K"])]
     rows_v = [f16_bits(inp_o["V"])]
     gs = GpuState(lc)
     assert (gs.L, gs.n_q) == (oc.L, oc.nq)
-    compare_state(gs, oc.export(), gcfg, report, units=us)
+    compare_state(gs, oc.export(), gcfg, rep, units=us)
     compare_ring(gs, np.concatenate(rows_k, 1), np.concatenate(rows_v, 1), gs.ring.shape[1], us)
     worst = 0.0
     for step in range(steps):
         di = sy.decode_inputs(w, layer, step, device=dev)
+        if xf_decode:
+            di = xf_decode(di)
         nq_before = lc.n_q
         # alternate the fused append+decode call and the two separate calls
         if (step % 2 == 1) if fused_step is None else fused_step:
@@ -79,13 +98,15 @@ def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every
             lc.append(di["k"], di["v"], di["types"])
             out = lc.decode(di["q"], flags=flags)
         do = sy.decode_inputs(w, layer, step, units=us, device="cpu")
+        if xf_decode:
+            do = xf_decode(do)
         oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
         rows_k.append(f16_bits(do["k"])[:, None])
         rows_v.append(f16_bits(do["v"])[:, None])
         assert (lc.L, lc.n_q) == (oc.L, oc.nq)
         if lc.n_q != nq_before:
             gs = GpuState(lc)
-            compare_state(gs, oc.export(), gcfg, report, units=us)
+            compare_state(gs, oc.export(), gcfg, rep, units=us)
             compare_ring(gs, np.concatenate(rows_k, 1), np.concatenate(rows_v, 1),
                          gs.ring.shape[1], us)
         if step % check_every == 0 or step == steps - 1:
@@ -93,7 +114,9 @@ def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every
             got = out[us].double().cpu().numpy()
             err = np.abs(got - ref).max()
             worst = max(worst, err)
+            record_margin(case or _case_name(), worst, OUT_TOL, None, decide64=decide64)
             assert err <= OUT_TOL, f"step {step}: max-abs {err}"
+    record_margin(case or _case_name(), worst, OUT_TOL, rep)
     return lc, oc, worst
 
 
@@ -327,7 +350,7 @@ def test_prefill_with_detected_pivots(ak, orc, sy, name, layer):
 
 
 # ----------------------------------------------------------------- NEXT-3 GQA head groups
-@pytest.mark.parametrize("g", [2, 3, 5, 7, 8])
+@pytest.mark.parametrize("g", [2, 3, 5, 7, 8, 16])
 @pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
 def test_gqa_head_groups(ak, orc, sy, g, kind):
     """q_per_kv > 1: g = 2 is one group of 2 heads (page MMA columns 0-3); for
@@ -366,3 +389,64 @@ def test_interleaved_layers_use_prologue(ak, orc, sy):
             ref = oc.decode(f16_bits(do["q"]))
             err = np.abs(out.double().cpu().numpy() - ref).max()
             assert err <= OUT_TOL, f"layer {layer} step {step}: {err}"
+
+
+# ----------------------------------------------------------------- decision precision
+@pytest.mark.parametrize("layer", [0, 2], ids=["TSA-L0", "PSA-L2"])
+def test_llava7b_fp32_decision_oracle(ak, orc, sy, layer):
+    """The same 7B layer against the oracle's fp32-decision mode (R6, the
+    kernel's precision): codes agree bit for bit unless the GPU's fp32 butterfly
+    sum differs from the correctly rounded x.H_s right at a tie."""
+    _run_case(ak, orc, sy, sy.LLAVA7B, layer, steps=3, decide64=0)
+
+
+# ----------------------------------------------------------------- stress (fixed point)
+def _hadamard_row(d, j):
+    i = np.arange(d)
+    return torch.tensor((-1.0) ** np.vectorize(lambda v: bin(int(v)).count("1"))(i & j))
+
+
+def _xf_q(scale):
+    def f(di):
+        di = dict(di)
+        di["q"] = (di["q"].float() * scale).to(di["q"].dtype)      # exact: power of two
+        return di
+    return f
+
+
+def _xf_v_channel(c, gain):
+    def f(inp):
+        inp = dict(inp)
+        V = inp["V"].float()
+        V[:, :, c] *= gain
+        inp["V"] = V.to(inp["V"].dtype)
+        return inp
+    return f
+
+
+def _xf_k_page_channel(j, amp, t0, t1):
+    """Tokens [t0, t1) get amp * (row j of the +-1 Hadamard matrix) added to K, so
+    in the rotated basis channel j of that page is ~amp * d, the page's fixed-point
+    range is set by one channel."""
+    def f(inp):
+        inp = dict(inp)
+        K = inp["K"].float()
+        h = _hadamard_row(K.shape[-1], j).to(K.device, torch.float32)
+        K[:, t0:t1, :] += amp * h
+        inp["K"] = K.to(inp["K"].dtype)
+        return inp
+    return f
+
+
+@pytest.mark.parametrize("stress", ["q8", "q16", "v100", "kpage"])
+@pytest.mark.parametrize("layer", [2, 0], ids=["PSA-L2", "TSA-L0"])
+def test_stress_fixed_point_sweep64(ak, orc, sy, stress, layer):
+    """Large logit spreads (q x8, x16: peaky attention), a V channel x100 and a
+    page whose rotated K range is dominated by one channel, at sweep@b64 in the
+    bench launch configuration (U = 2048), sampled units vs the oracle.  These
+    load the 16-bit fixed points of the page MMAs hardest."""
+    w = sy.get("sweep@b64")
+    kw = {"q8": dict(xf_decode=_xf_q(8.0)), "q16": dict(xf_decode=_xf_q(16.0)),
+          "v100": dict(xf_layer=_xf_v_channel(5, 100.0)),
+          "kpage": dict(xf_layer=_xf_k_page_channel(37, 8.0, 384, 512))}[stress]
+    _run_case(ak, orc, sy, w, layer, steps=2, units=[0, w.U // 2, w.U - 1], **kw)

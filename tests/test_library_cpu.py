@@ -106,3 +106,28 @@ def test_memory_report_closed_forms(ak):
     n_q = (100000 - 128) // 128 * 128
     r = ak.akvq_memory_report(_host_cache(ak, big, 100000, n_q), 15)
     assert abs(r.effective_bits_per_element - 2.5) < 0.05
+
+
+def test_memory_report_tsa_needs_the_text_count(ak):
+    """A TSA layer's 4-bit text rows are counted from the caller's side
+    count; -1 (unknown, the count lives on the device) is rejected."""
+    cfg = _cfg(ak, kind=ak.AKVQ_TSA, R=172, capacity=300)
+    c = _host_cache(ak, cfg, 300, 128)
+    with pytest.raises(ak.AkvqError) as e:
+        ak.akvq_memory_report(c, -1)
+    assert e.value.status == ak.AKVQ_EINVAL
+    r = ak.akvq_memory_report(c, 100)
+    d = 128
+    assert r.bytes_int4 == pytest.approx(4 * 100 * 2 * (d / 2 + 8))
+    assert r.bytes_int2 == pytest.approx(4 * 28 * 2 * d / 4)
+    assert r.bytes_fp16 == pytest.approx(4 * 172 * 2 * d * 2)
+    with pytest.raises(ak.AkvqError):
+        ak.akvq_memory_report(c, 129)                   # more side rows than n_q
+
+
+@pytest.mark.parametrize("g", [1, 2, 7, 16])
+def test_ticket_region_covers_every_head_group(ak, g):
+    """The merge-ticket region holds one ticket per (unit, GQA head group) of the
+    decode kernel for every supported q_per_kv (g up to 16)."""
+    y = ak.akvq_cache_layout(_cfg(ak, g=g))
+    assert y.total_bytes - y.ticket_off >= 4 * 4 * max(1, g)      # U = 4 units, <= g groups

@@ -228,7 +228,7 @@ def test_per_channel_block_hand_worked(orc):
             cs[0, 0, sal_tok] = 1.0
         assert c.prefill(K, K, colsum=cs) == 0 and c.nq == 4
         e = c.export()
-        assert np.allclose(e["kscale32"][0, 0], [1, -1, 0, 0]) and e["kzero"][0, 0].tolist() == [0] * 4
+        assert np.allclose(e["kscale_raw"][0, 0], [1, -1, 0, 0]) and e["kzero"][0, 0].tolist() == [0] * 4
         kb = e["kcodes"][0, :4, 0].tolist()
         # byte of token t = code(ch0) | code(ch1) << 2 | code(ch2) << 4 | code(ch3) << 6
         exp = [t | (1 << 2) | (1 << 4) | (1 << 6) for t in range(4)]
@@ -258,11 +258,11 @@ def test_per_token_k_hand_worked(orc):
     c = orc.OracleCache(_cfg(orc, kind=orc.PSA, top_k=0, k_axis=1))
     assert c.prefill(K, K, colsum=np.zeros((1, 1, 4), np.float32)) == 0 and c.nq == 4
     e = c.export()
-    assert e["kscale32"].shape == (1, c.cap, 1)
+    assert e["kscale_raw"].shape == (1, c.cap, 1)
     s0, s1 = np.float32(np.float32(3.2) / np.float32(3.0)), np.float32(5.6) / np.float32(3.0)
-    assert np.isclose(e["kscale32"][0, 0, 0], 3.2 / 3, rtol=1e-6)
-    assert np.isclose(e["kscale32"][0, 1, 0], 5.6 / 3, rtol=1e-6)
-    assert e["kscale32"][0, 2, 0] == 2.0 and e["kscale32"][0, 3, 0] == 0.0
+    assert np.isclose(e["kscale_raw"][0, 0, 0], 3.2 / 3, rtol=1e-6)
+    assert np.isclose(e["kscale_raw"][0, 1, 0], 5.6 / 3, rtol=1e-6)
+    assert e["kscale_raw"][0, 2, 0] == 2.0 and e["kscale_raw"][0, 3, 0] == 0.0
     assert e["kzero"][0, :4, 0].tolist() == [0, 2, 0, 0]
     codes = orc.unpack(e["kcodes"][0, :4].reshape(-1), 16, 2).reshape(4, 4)
     assert codes.tolist() == [[0, 1, 2, 3], [0, 1, 2, 3], [1, 1, 1, 1], [1, 1, 1, 1]]
@@ -290,7 +290,7 @@ def test_per_token_k_bounds_and_library_sdpa(orc):
     e = c.export()
     Kh, Vh = c.view()
     nq = c.nq
-    xs = e["xs_k"][:, :nq].astype(np.float64) / np.sqrt(d)      # rotated, normalized
+    xs = e["xs_k"][:, :nq] / np.sqrt(d)      # rotated, normalized
     sal = e["salient"][:, :nq].astype(bool)
     sc = np.repeat(e["kscale"][:, :nq], G, axis=-1)             # per token, per channel
     zf = np.repeat(e["kzero"][:, :nq], G, axis=-1).astype(np.float64)
@@ -370,7 +370,7 @@ def test_prefill_equals_incremental_append(orc):
         ea, eb = a.export(), b.export()
         assert a.nq == b.nq and a.L == b.L
         for key in ea:
-            assert np.array_equal(ea[key], eb[key]), key
+            assert np.array_equal(ea[key], eb[key], equal_nan=ea[key].dtype.kind == "f"), key
 
 
 def test_region_partition_and_view_bounds(orc):
@@ -599,3 +599,167 @@ def test_prefill_with_pivot_mask(orc):
     over = mask.copy(); over[0, 50] = 1; over[0, 51] = 1
     assert orc.OracleCache(cfg).prefill_pivots(K, V, over) == 1      # EINVAL
 
+
+
+# ----------------------------------------------------------------- fp64 decisions
+def test_quantizer_fp64_decisions_spec_and_hand_worked(orc):
+    """The fp64-decision quantizer (the cache default) on the same
+    pins as the fp32 one: SPEC examples S:131-133, the on-grid and clip-0.8
+    hand-worked groups, salient skip, empty and degenerate groups."""
+    for ex in _spec()["quantize"]:
+        s, z, c, _ = orc.quantize_group64(ex["x"], ex["bits"], ex["clip"])
+        assert s == pytest.approx(ex["scale"], rel=1e-7), ex["cite"]
+        assert z == ex["zero"] and c.tolist() == ex["codes"], ex["cite"]
+    x = [-0.5, 0, 0.5, 1, 1, -0.5, 0.5, 0]
+    s, z, c, zp = orc.quantize_group64(x, 2, 1.0)
+    assert (s, z, c.tolist(), zp) == (0.5, 1, [0, 1, 2, 3, 3, 0, 2, 1], -1.0)
+    s, z, c, zp = orc.quantize_group64([-3, -1, 0.25, 2, 5], 2, 0.8)
+    # clip is the fp32 constant 0.8f widened exactly (R3)
+    c8 = float(np.float32(0.8))
+    assert s == pytest.approx((5 * c8 + 3 * c8) / 3, rel=1e-15)
+    assert zp == pytest.approx(-1.125, rel=1e-12) and z == 1 and c.tolist() == [0, 1, 1, 2, 3]
+    s2, z2, c2, _ = orc.quantize_group64([-3, -1, 100.0, 2, 5], 2, 0.8, skip=[0, 0, 1, 0, 0])
+    assert (s2, z2) == (s, z) and c2.tolist() == [0, 1, 0, 2, 3]
+    s3, z3, c3, zp3 = orc.quantize_group64([1.0, 2.0], 2, 0.8, skip=[1, 1])
+    assert (s3, z3, c3.tolist()) == (0.0, 0, [0, 0]) and math.isnan(zp3)
+    s4, z4, c4, zp4 = orc.quantize_group64([5.0] * 4, 2, 0.8)       # degenerate (S:132)
+    assert (s4, z4, c4.tolist()) == (5.0, 0, [1, 1, 1, 1]) and math.isnan(zp4)
+
+
+@pytest.mark.parametrize("bits,clip", [(2, 0.8), (2, 1.0), (4, 1.0)])
+def test_quantizer_fp64_brute_force_and_bounds(orc, bits, clip):
+    """fp64 decisions: brute-force nearest code, |x - x'| <= scale/2 for
+    in-clip elements, monotone -- on fp64 inputs."""
+    rng = np.random.default_rng(100 + bits)
+    levels = (1 << bits) - 1
+    c32 = float(np.float32(clip))
+    for _ in range(300):
+        x = rng.uniform(-1, 1, size=128) * rng.uniform(0.1, 10)
+        s, z, c, zp = orc.quantize_group64(x, bits, clip)
+        assert s == (c32 * x.max() - c32 * x.min()) / levels
+        assert z == -round(c32 * x.min() / s) and zp == c32 * x.min() / s
+        grid = s * (np.arange(levels + 1)[None, :] - z)
+        assert np.array_equal(np.abs(x[:, None] - grid).argmin(1), c)
+        xr = s * (c.astype(np.float64) - z)
+        inclip = (x >= c32 * x.min()) & (x <= c32 * x.max())
+        assert np.all(np.abs(x[inclip] - xr[inclip]) <= s / 2 * (1 + 1e-12))
+        o = np.argsort(x, kind="stable")
+        assert np.all(np.diff(c[o].astype(int)) >= 0)
+
+
+def test_fp64_and_fp32_decision_modes_agree_except_ties(orc):
+    """The two decision precisions of one cache (R6) give the same codes and zero
+    points except documented round-half ties (pre-round value within 1e-5 of a
+    half-integer in the fp64 mode), and scales within 1e-6 relative."""
+    rng = np.random.default_rng(21)
+    U, L0, d, G = 3, 300, 64, 32
+    K = _bf16_bits(rng.normal(size=(U, L0, d)) * np.where(np.arange(d) == 9, 15, 1))
+    V = _bf16_bits(rng.normal(size=(U, L0, d)))
+    types = (rng.random((U, L0)) < 0.3).astype(np.uint8)
+    cs = rng.random((U, 1, L0)).astype(np.float32)
+    half = lambda a: np.abs(np.abs(np.mod(a, 1.0)) - 0.5) <= 1e-5
+    for kind in (orc.PSA, orc.TSA):
+        ex = []
+        for d64 in (1, 0):
+            c = orc.OracleCache(_cfg(orc, U=U, d=d, G=G, R=12, capacity=L0, kind=kind, top_k=5,
+                                     dtype16=orc.BF16, decide64=d64))
+            assert c.prefill(K, V, types=types, colsum=cs) == 0
+            ex.append(c.export())
+        e64, e32 = ex
+        nq = c.nq
+        for key, pre in (("kcodes", "kpre"), ("vcodes", "vpre")):
+            a = orc.unpack(e64[key][:, :nq].reshape(-1), U * nq * d, 2)
+            b = orc.unpack(e32[key][:, :nq].reshape(-1), U * nq * d, 2)
+            tie = half(e64[pre][:, :nq].reshape(-1))
+            assert np.all((a == b) | tie), key
+        for key, zp in (("kzero", "kzpre"), ("vzero", "vzpre")):
+            dz = e64[key] != e32[key]
+            assert np.all(~dz | half(e64[zp])), key
+        for key in ("kscale_raw", "vscale_raw", "side4_scale"):
+            assert np.all(np.abs(e64[key] - e32[key]) <= 1e-6 * np.abs(e64[key]) + 1e-30), key
+        if kind == orc.TSA:
+            cnt = e64["side_count"]
+            for u in range(U):
+                a = orc.unpack(e64["side4"][u, :cnt[u]].reshape(-1), cnt[u] * 2 * d, 4)
+                b = orc.unpack(e32["side4"][u, :cnt[u]].reshape(-1), cnt[u] * 2 * d, 4)
+                tie = half(e64["side4_pre"][u, :cnt[u]].reshape(-1))
+                assert np.all((a == b) | tie)
+
+
+# ----------------------------------------------------------------- TSA 4-bit tier
+def test_tsa_4bit_tier_hand_worked(orc):
+    """TSA text tokens ("stored with 4-bit precision"; Eqs. 3-6 with
+    clip 1.0): d = G = 4, rotated targets chosen by hand, tokens 0 and 2
+    text (salient, 4-bit side rows), tokens 1 and 3 vision (2-bit block).
+      K.H_s of token 0 = [-2, 1, 4, 7]: range 9 -> scale 9/15 = 0.6, cmn/scale =
+        -10/3 -> zero 3; x/scale = [-10/3, 5/3, 20/3, 35/3] -> rne [-3, 2, 7, 12]
+        + 3 -> codes [0, 5, 10, 15]; packed low nibble first: 0x50, 0xFA.
+      K.H_s of token 2 = [-3, 0, 5, 12] (on the grid): scale 1, zero 3, codes
+        [0, 3, 8, 15] -> 0x30, 0xF8; dequantizes exactly.
+      V.H_s of tokens 0, 2 = [0, 3, 6, 9]: scale 0.6, zero 0, codes [0, 5, 10, 15].
+    Stored scale = decision scale / sqrt(d) (R5); view = stored scale (code - zero)."""
+    X = np.array([[-2, 1, 4, 7], [1, -1, 2, 0], [-3, 0, 5, 12], [0, 2, -2, 1]], float)
+    Y = np.array([[0, 3, 6, 9], [1, 0, 0, -1], [0, 3, 6, 9], [2, 1, 0, 3]], float)
+    K, V = _rows_with_rotation(X)[None], _rows_with_rotation(Y)[None]
+    types = np.array([[1, 0, 1, 0]], np.uint8)
+    for d64 in (1, 0):
+        c = orc.OracleCache(_cfg(orc, kind=orc.TSA, clip4=1.0, decide64=d64))
+        assert c.prefill(K, V, types=types) == 0 and c.nq == 4
+        e = c.export()
+        assert e["side_count"][0] == 2 and e["side_index"][0, :2].tolist() == [0, 2]
+        assert e["side4"][0, 0, 0].tolist() == [0x50, 0xFA]           # K of token 0
+        assert e["side4"][0, 1, 0].tolist() == [0x30, 0xF8]           # K of token 2
+        assert e["side4"][0, 0, 1].tolist() == [0x50, 0xFA]           # V of token 0
+        assert np.allclose(e["side4_scale"][0, 0, :, 0], [0.6 / 2, 0.6 / 2], rtol=1e-6)
+        assert e["side4_scale"][0, 1, 0, 0] == 0.5                   # 1 / sqrt(4)
+        assert e["side4_zero"][0, 0, :, 0].tolist() == [3, 0]
+        assert e["side4_zero"][0, 1, 0, 0] == 3
+        # the 2-bit region holds codes 0 and meta (0, 0) for the text tokens
+        assert e["vscale"][0, [0, 2], 0].tolist() == [0.0, 0.0]
+        codes = orc.unpack(e["kcodes"][0, :4].reshape(-1), 16, 2).reshape(4, 4)
+        assert codes[0].tolist() == [0] * 4 and codes[2].tolist() == [0] * 4
+        Kh, Vh = c.view()
+        assert np.allclose(Kh[0, 0], 0.3 * (np.array([0, 5, 10, 15]) - 3), atol=1e-6)
+        assert np.abs(Kh[0, 2] - X[2] / 2).max() <= 1e-6            # on the grid: exact
+        assert np.abs(Vh[0, 0] - Y[0] / 2).max() <= 1e-6
+        # |x - x'| <= scale / 2 on the 4-bit row (clip 1.0: every element in-clip)
+        assert np.all(np.abs(Kh[0, 0] - X[0] / 2) <= 0.15 + 1e-6)
+
+
+@pytest.mark.parametrize("d64", [1, 0])
+def test_tsa_4bit_view_bounds_and_on_grid(orc, d64):
+    """TSA layer on random outlier data: every 4-bit side element within scale/2
+    of the exact rotated value x.H (clip 1.0); side rows on a
+    power-of-two grid reconstruct exactly; 16-bit ring rows exact."""
+    rng = np.random.default_rng(22)
+    U, L0, d, G, R = 2, 160, 64, 32, 16
+    K = rng.normal(size=(U, L0, d)); K[:, :, 7] *= 20
+    V = rng.normal(size=(U, L0, d))
+    types = (rng.random((U, L0)) < 0.4).astype(np.uint8)
+    # unit 1, tokens 0..15: rows on a 4-bit grid (scale 0.25 after rotation,
+    # integer zero point, codes 0 and 15 both present in every group)
+    grid = rng.integers(0, 16, size=(16, d)).astype(float)
+    grid[:, 0], grid[:, 1] = 0, 15
+    grid[:, 32], grid[:, 33] = 0, 15
+    Xg = 0.25 * (grid - 5)
+    Kb, Vb = _f16_bits(K), _f16_bits(V)
+    Kb[1, :16] = _rows_with_rotation(Xg)
+    types[1, :16] = 1
+    c = orc.OracleCache(_cfg(orc, U=U, d=d, G=G, R=R, capacity=L0, kind=orc.TSA, clip4=1.0,
+                             decide64=d64))
+    assert c.prefill(Kb, Vb, types=types) == 0
+    e = c.export()
+    Kh, Vh = c.view()
+    H = scipy.linalg.hadamard(d) / math.sqrt(d)
+    Kf = Kb.view(np.float16).astype(np.float64) @ H
+    Vf = Vb.view(np.float16).astype(np.float64) @ H
+    nq = c.nq
+    for u in range(U):
+        n = e["side_count"][u]
+        idx = e["side_index"][u, :n]
+        assert idx.tolist() == np.flatnonzero(types[u, :nq]).tolist()
+        for kv, (Xh, Xf) in enumerate(((Kh, Kf), (Vh, Vf))):
+            s = np.repeat(e["side4_scale"][u, :n, kv], G, axis=-1)
+            assert np.all(np.abs(Xh[u, idx] - Xf[u, idx]) <= s / 2 * (1 + 1e-6) + 1e-12)
+        assert np.abs(Kh[u, nq:] - Kf[u, nq:]).max() <= 1e-12
+    assert np.abs(Kh[1, :16] - Xg / math.sqrt(d)).max() <= 1e-12
