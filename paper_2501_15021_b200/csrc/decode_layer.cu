@@ -58,8 +58,17 @@ constexpr int kRows4 = 32;         // 4-bit TSA rows per side sub-load
 #endif
 #define AKVQ_PRAGMA(x) _Pragma(#x)
 #define AKVQ_UNROLL(n) AKVQ_PRAGMA(unroll n)
-constexpr int kQMax = 32639;       // K-side fixed point: |Q| <= 127 * 257 (2 signed limbs)
-constexpr int kWMax = 65535;       // V-side fixed point: W <= 2^16 - 1 (2 limbs)
+// Page fixed points: three 8-bit limbs each, i.e. 24-bit
+// precision relative to the page's largest |q~ s^K| / largest softmax weight.
+//  K: |Q| <= kQMax < 127 * 65793, Q + kQOff in [0, 2^24), limb k = byte k of
+//     Q + kQOff, minus 128 (signed int8: byte ^ 0x80); kQMax leaves room for
+//     the 2-ulp error of __fdividef in the scale.
+//  V: 0 <= W <= 2^24 - 1, limb k = byte k (unsigned int8).
+// Each head owns 4 MMA B columns: limbs 0, 1, 2 and one unused column.
+constexpr int kQMax = 8355700;
+constexpr uint32_t kQOff = 0x808080u;
+constexpr int kWMax = 16777215;
+constexpr int kLimbCols = 4;
 #ifndef AKVQ_LY_CTAS
 #define AKVQ_LY_CTAS 4
 #endif
@@ -73,12 +82,14 @@ template <int D, int G, int NH>
 struct LySmem {
   static constexpr int NG = D / G;
   static __host__ __device__ size_t qh_off(size_t sb) { return kLyStages * sb; }
-  static constexpr size_t KL = (size_t)NH * (D / 16) * 32, VL = (size_t)NH * NG * (G / 16) * 32;
+  // limbs: K [kLimbCols NH][D/4] u32, V [NG][kLimbCols NH][G/4] u32
+  static constexpr size_t KL = (size_t)NH * kLimbCols * D, VL = (size_t)NH * NG * kLimbCols * G;
   static __host__ __device__ size_t kl_off(size_t sb) { return qh_off(sb) + NH * D * 4; }
   static __host__ __device__ size_t vl_off(size_t sb) { return kl_off(sb); }   // shared
   // page logits [NH][G] / page V sums [NH][D] (fp32, one at a time)
   static __host__ __device__ size_t lv_off(size_t sb) { return kl_off(sb) + (KL > VL ? KL : VL); }
-  static __host__ __device__ size_t ds_off(size_t sb) { return lv_off(sb) + (size_t)NH * D * 4; }
+  // [2][NH][D] f32: per-limb-pair partial sums (even / odd MMA lanes), G <= D
+  static __host__ __device__ size_t ds_off(size_t sb) { return lv_off(sb) + (size_t)2 * NH * D * 4; }
   static __host__ __device__ size_t bar_off(size_t sb) { return ds_off(sb) + kLyStages * 32; }
   static __host__ __device__ size_t warp_bytes(size_t sb) {
     return (bar_off(sb) + kLyStages * 8 + 127) / 128 * 128;
@@ -353,10 +364,19 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   const int vcq = lane % CQ, vts = lane / CQ;         // page V phase and rows
   const int vgam = (4 * vcq) / G;                     // channel group of the lane's quad
   const int mg = lane >> 2, mt = lane & 3;            // page MMA: fragment group / thread in group
-  const int mcol = min(mg, 2 * NH - 1);               // B column of the lane (padded columns repeat)
-  uint32_t *qlimb = klimb;                            // [2 NH][CQ] Q limbs (page MMA layout)
-  uint32_t *wlimb = vlimb;                            // [NG][2 NH][TQ] W limbs
-  float *lgs = reinterpret_cast<float *>(wsm + S::lv_off(SB));   // [NH][G] logits / [NH][D] V sums
+  // B column of the lane: head mg / 4, limb mg % 4 (the unused 4th column and
+  // padded heads read a valid limb; their results are never used)
+  const int mcol = [&] { const int m = min(mg, kLimbCols * NH - 1); return (m & 3) == 3 ? m - 1 : m; }();
+  // MMA result columns 2 mt, 2 mt + 1 of this lane: head mt / 2; even mt holds
+  // limbs 0 and 1, odd mt limb 2 (and the unused column)
+  const int rhead = mt >> 1;
+  const bool rodd = mt & 1;
+  static_assert(kLimbCols * NH <= 8, "one MMA n-tile: at most 2 heads of 4 limb columns");
+  uint32_t *qlimb = klimb;                            // [4 NH][CQ] Q limbs (page MMA layout)
+  uint32_t *wlimb = vlimb;                            // [NG][4 NH][TQ] W limbs
+  // page logits / V sums, split by limb pair: [2][NH][D] (row 0: limbs 0 + 256 x 1
+  // from even MMA lanes, row 1: limb 2 from odd lanes; x 65536 when combined)
+  float *lgs = reinterpret_cast<float *>(wsm + S::lv_off(SB));
 
   // per-unit segment state
   // l_run and zl are per-lane partials (each lane adds its own tokens / rows),
@@ -568,12 +588,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       const int4 *kz4 = reinterpret_cast<const int4 *>(B + c.pg_kzero);
       if constexpr (KT) {                      // per-token K variant (compile time)
         // ---- per-token K (NEXT-1): Q_c = rn(q~_c / delta) once per page,
-        // logit_t = alpha delta sum_g s_tg (sum_{c in g} Q_c code_tc - z_tg SQ_g);
-        // the inner sums by the same warp MMA as the per-channel path, folded
-        // per channel group (a 32-channel chunk lies in one group: G >= 32)
+        // logit_t = alpha delta sum_g s_tg sum_k 256^k (C_k,tg - z_tg SQ_k,g) with
+        // C_k,tg = sum_{c in g} limb_k,c code_tc (the warp MMA, folded per
+        // channel group: a 32-channel chunk lies in one group since G >= 32) and
+        // SQ_k,g = sum_{c in g} limb_k,c
         const float *ksT = reinterpret_cast<const float *>(B + c.pg_kscale);    // [G][NG]
         const int32_t *kzT = reinterpret_cast<const int32_t *>(B + c.pg_kzero);
-        float dT[NH], sqg[NH][NG];
+        float dT[NH], sqg[NH][2][NG];            // per head: delta; this lane's limb sums
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
           float qv4[4] = {0.f, 0.f, 0.f, 0.f}, am = 0.f;
@@ -585,19 +606,32 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           const float M = warp_max(am);
           const float inv = M > 0.f ? __fdividef((float)kQMax, M) : 0.f;
           dT[h] = alpha_k * M * (1.0f / (float)kQMax);
-          int Qv[4];
+          uint32_t x[4];
 #pragma unroll
-          for (int b = 0; b < 4; ++b) Qv[b] = __float2int_rn(qv4[b] * inv);
-          // SQ_g = sum of Q over channel group g (lanes g*G/4 .. (g+1)*G/4 - 1)
-          int sq = (Qv[0] + Qv[1]) + (Qv[2] + Qv[3]);
+          for (int b = 0; b < 4; ++b) x[b] = (uint32_t)__float2int_rn(qv4[b] * inv) + kQOff;
+          // SQ_k,g over channel group g (lanes g*G/4 .. (g+1)*G/4 - 1), k = 0..2
+          int sq[3];
 #pragma unroll
-          for (int o = 1; o < G / 4 && o < 32; o <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+          for (int k = 0; k < 3; ++k) {
+            sq[k] = 0;
 #pragma unroll
-          for (int gi = 0; gi < NG; ++gi) sqg[h][gi] = (float)__shfl_sync(0xffffffffu, sq, (gi * (G / 4)) & 31);
+            for (int b = 0; b < 4; ++b) sq[k] += (int)((x[b] >> (8 * k)) & 255u) - 128;
+#pragma unroll
+            for (int o = 1; o < G / 4 && o < 32; o <<= 1) sq[k] += __shfl_xor_sync(0xffffffffu, sq[k], o);
+          }
+#pragma unroll
+          for (int gi = 0; gi < NG; ++gi) {
+            const int src = (gi * (G / 4)) & 31;
+            const float s0 = (float)__shfl_sync(0xffffffffu, sq[0], src);
+            const float s1 = (float)__shfl_sync(0xffffffffu, sq[1], src);
+            const float s2 = (float)__shfl_sync(0xffffffffu, sq[2], src);
+            sqg[h][0][gi] = rodd ? s2 : s0;
+            sqg[h][1][gi] = rodd ? 0.f : s1;
+          }
           if (lane < CQ) {
-            const uint32_t x0 = Qv[0] + 128, x1 = Qv[1] + 128, x2 = Qv[2] + 128, x3 = Qv[3] + 128;
-            qlimb[(2 * h) * CQ + lane] = prmt(prmt(x0, x1, 0x0040), prmt(x2, x3, 0x0040), 0x5410) ^ 0x80808080u;
-            qlimb[(2 * h + 1) * CQ + lane] = prmt(prmt(x0, x1, 0x0051), prmt(x2, x3, 0x0051), 0x5410);
+            qlimb[(4 * h) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0040), prmt(x[2], x[3], 0x0040), 0x5410) ^ 0x80808080u;
+            qlimb[(4 * h + 1) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0051), prmt(x[2], x[3], 0x0051), 0x5410) ^ 0x80808080u;
+            qlimb[(4 * h + 2) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0062), prmt(x[2], x[3], 0x0062), 0x5410) ^ 0x80808080u;
           }
         }
         __syncwarp();
@@ -609,16 +643,19 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           bq[cc][0] = b.x;
           bq[cc][1] = b.y;
         }
-        float dsel = dT[0], ssel[NG];
+        const int hsel = min(rhead, NH - 1);
+        float dsel = dT[0], ssel[2][NG];
 #pragma unroll
-        for (int gi = 0; gi < NG; ++gi) ssel[gi] = sqg[0][gi];
+        for (int gi = 0; gi < NG; ++gi) { ssel[0][gi] = sqg[0][0][gi]; ssel[1][gi] = sqg[0][1][gi]; }
 #pragma unroll
         for (int h = 1; h < NH; ++h)
-          if (mt == h) {
+          if (hsel == h) {
             dsel = dT[h];
 #pragma unroll
-            for (int gi = 0; gi < NG; ++gi) ssel[gi] = sqg[h][gi];
+            for (int gi = 0; gi < NG; ++gi) { ssel[0][gi] = sqg[h][0][gi]; ssel[1][gi] = sqg[h][1][gi]; }
           }
+        // even lanes: limbs 0 (x 1) and 1 (x 256); odd lanes: limb 2 (x 65536)
+        const float wA = rodd ? 65536.f : 1.f, wB = rodd ? 0.f : 256.f;
         const uint32_t *kcw = reinterpret_cast<const uint32_t *>(B + c.pg_kcodes);
         AKVQ_UNROLL(AKVQ_KU)
         for (int blk = 0; blk < TQ / 8; ++blk) {
@@ -634,35 +671,38 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
               mma_u8s8(c01, fmask(w.x, 0), fmask(w.x, 1), fmask(w.y, 0), fmask(w.y, 1), bq[cc][0], bq[cc][1]);
               mma_u8s8(c23, fmask(w.x, 2), fmask(w.x, 3), fmask(w.y, 2), fmask(w.y, 3), bq[cc][0], bq[cc][1]);
             }
-            const int tot[4] = {c01[1] * 256 + c01[0], c23[1] * 256 + c23[0], c01[3] * 256 + c01[2],
-                                c23[3] * 256 + c23[2]};
-            // tot[0]: token 4tq+0 (x1), tot[2]: 4tq+1 (x4), tot[1]: 4tq+2 (x16), tot[3]: 4tq+3 (x64)
-            const float t0 = (float)tot[0], t1 = (float)tot[2] * 0.25f, t2 = (float)tot[1] * 0.0625f,
-                        t3 = (float)tot[3] * 0.015625f;
-            const float tk[4] = {t0, t1, t2, t3};
+            // token 4tq+0 (x1): c01[0..1]; 4tq+1 (x4): c01[2..3]; 4tq+2 (x16): c23[0..1]; 4tq+3 (x64): c23[2..3]
+            const int ca[4] = {c01[0], c01[2], c23[0], c23[2]}, cb[4] = {c01[1], c01[3], c23[1], c23[3]};
+            const float fk[4] = {1.f, 0.25f, 0.0625f, 0.015625f};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const int mi = (4 * tq + k) * NG + gi;
-              part[k] = fmaf(ksT[mi], tk[k] - (float)kzT[mi] * ssel[gi], part[k]);
+              const float z = (float)kzT[mi];
+              const float t = fmaf(wA, fmaf((float)ca[k], fk[k], -z * ssel[0][gi]),
+                                   wB * fmaf((float)cb[k], fk[k], -z * ssel[1][gi]));
+              part[k] = fmaf(ksT[mi], t, part[k]);
             }
           }
-          if (mt < NH) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) part[k] += __shfl_xor_sync(0xffffffffu, part[k], 1);
+          if (!rodd && rhead < NH) {
             float4 r;
             r.x = part[0] * dsel; r.y = part[1] * dsel; r.z = part[2] * dsel; r.w = part[3] * dsel;
-            reinterpret_cast<float4 *>(lgs + mt * G)[tq] = r;
+            reinterpret_cast<float4 *>(lgs + rhead * D)[tq] = r;
           }
         }
         __syncwarp();
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-          const float4 r = reinterpret_cast<const float4 *>(lgs + h * G)[ktq];
+          const float4 r = reinterpret_cast<const float4 *>(lgs + h * D)[ktq];
           lg[h][0] = (sbits & 1u) ? -INFINITY : r.x;
           lg[h][1] = (sbits & 2u) ? -INFINITY : r.y;
           lg[h][2] = (sbits & 4u) ? -INFINITY : r.z;
           lg[h][3] = (sbits & 8u) ? -INFINITY : r.w;
         }
       } else {
-      float dA[NH], bA[NH];
+      float dA[NH];
+      int bA[NH][3];
 #pragma unroll
       for (int h = 0; h < NH; ++h) {      // Q_c = rn(q~_c s^K_c / delta): lane = channel quad
         float qsb[4] = {0.f, 0.f, 0.f, 0.f}, am = 0.f;
@@ -675,34 +715,37 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           am = fmaxf(fmaxf(fabsf(qsb[0]), fabsf(qsb[1])), fmaxf(fabsf(qsb[2]), fabsf(qsb[3])));
         }
         const float M = warp_max(am);
-        // fixed-point scale (any consistent inv / delta pair works: the sum is
-        // exact for the rounded Q; |Q| <= kQMax holds within __fdividef's 2 ulp)
+        // fixed-point scale (any consistent inv / delta pair works: the sums are
+        // exact for the rounded Q; |Q| <= kQMax + 2 holds within __fdividef's error)
         const float inv = M > 0.f ? __fdividef((float)kQMax, M) : 0.f;
         const float delta = M * (1.0f / (float)kQMax);
-        int Qv[4];
+        uint32_t x[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) Qv[b] = __float2int_rn(qsb[b] * inv);
-        // zero-point bias sum_c Q_c z_c (exact in fp32 while |sum| < 2^24)
-        float bq = (float)Qv[0] * (float)zq.x;
-        bq = fmaf((float)Qv[1], (float)zq.y, bq);
-        bq = fmaf((float)Qv[2], (float)zq.z, bq);
-        bq = fmaf((float)Qv[3], (float)zq.w, bq);
-        bq = warp_sum(bq);
+        for (int b = 0; b < 4; ++b) x[b] = (uint32_t)__float2int_rn(qsb[b] * inv) + kQOff;
+        // zero-point bias per limb: B_k = sum_c limb_k,c z_c (exact in int32)
+        const int zz[4] = {zq.x, zq.y, zq.z, zq.w};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          int bk = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) bk += ((int)((x[b] >> (8 * k)) & 255u) - 128) * zz[b];
+          bA[h][k] = warp_sum_i(bk);
+        }
         dA[h] = alpha_k * delta;
-        bA[h] = alpha_k * delta * bq;
         if (lane < CQ) {
-          // signed limbs Q = 256 hi + lo, lo, hi in [-128, 127]: x = Q + 128,
-          // hi = x >> 8 (byte 1 of x), lo = (x & 255) - 128 (byte 0 of x ^ 0x80)
-          const uint32_t x0 = Qv[0] + 128, x1 = Qv[1] + 128, x2 = Qv[2] + 128, x3 = Qv[3] + 128;
-          qlimb[(2 * h) * CQ + lane] = prmt(prmt(x0, x1, 0x0040), prmt(x2, x3, 0x0040), 0x5410) ^ 0x80808080u;
-          qlimb[(2 * h + 1) * CQ + lane] = prmt(prmt(x0, x1, 0x0051), prmt(x2, x3, 0x0051), 0x5410);
+          qlimb[(4 * h) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0040), prmt(x[2], x[3], 0x0040), 0x5410) ^ 0x80808080u;
+          qlimb[(4 * h + 1) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0051), prmt(x[2], x[3], 0x0051), 0x5410) ^ 0x80808080u;
+          qlimb[(4 * h + 2) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0062), prmt(x[2], x[3], 0x0062), 0x5410) ^ 0x80808080u;
         }
       }
       __syncwarp();
       // logits by warp MMA: rows = tokens (row grp: token 4 tq + k0, grp + 8:
       // 4 tq + k1, tq = 8 blk + grp), K = 32 channels per chunk, columns = Q limbs
-      // (2 h, 2 h + 1).  The masked code word (code << 2k per byte) is the A
-      // fragment of 4 channels of one token; rows carry the 4^k factor.
+      // (4 h + k).  The masked code word (code << 2k per byte) is the A fragment
+      // of 4 channels of one token; rows carry the 4^k factor.  The accumulators
+      // start at -4^k B_limb, so each limb column ends as the exact integer
+      // 4^k (C_limb - B_limb); the limbs combine in fp32 (even lanes: limb 0 +
+      // 256 limb 1, odd lanes: limb 2, x 65536 in the reader).
       constexpr int KC = D / 32;
       uint32_t bq[KC][2];
 #pragma unroll
@@ -711,38 +754,40 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         bq[cc][0] = b.x;
         bq[cc][1] = b.y;
       }
-      float dsel = dA[0], bsel = bA[0];
+      const int hsel = min(rhead, NH - 1);
+      int ba = bA[0][0], bb = bA[0][1], b2 = bA[0][2];
 #pragma unroll
       for (int h = 1; h < NH; ++h)
-        if (mt == h) { dsel = dA[h]; bsel = bA[h]; }
+        if (hsel == h) { ba = bA[h][0]; bb = bA[h][1]; b2 = bA[h][2]; }
+      if (rodd) { ba = b2; bb = 0; }
+      const float wB = rodd ? 0.f : 256.f;
+      float *lgw = lgs + (rodd ? NH : 0) * D + hsel * D;
       const uint32_t *kcw = reinterpret_cast<const uint32_t *>(B + c.pg_kcodes);
       AKVQ_UNROLL(AKVQ_KU)
       for (int blk = 0; blk < TQ / 8; ++blk) {
         const int tq = 8 * blk + mg;
-        int c01[4] = {0, 0, 0, 0}, c23[4] = {0, 0, 0, 0};
+        int c01[4] = {-ba, -bb, -4 * ba, -4 * bb}, c23[4] = {-16 * ba, -16 * bb, -64 * ba, -64 * bb};
 #pragma unroll
         for (int cc = 0; cc < KC; ++cc) {
           const uint2 w = *reinterpret_cast<const uint2 *>(kcw + kword_idx(8 * cc + 2 * mt, tq, TQ));
           mma_u8s8(c01, fmask(w.x, 0), fmask(w.x, 1), fmask(w.y, 0), fmask(w.y, 1), bq[cc][0], bq[cc][1]);
           mma_u8s8(c23, fmask(w.x, 2), fmask(w.x, 3), fmask(w.y, 2), fmask(w.y, 3), bq[cc][0], bq[cc][1]);
         }
-        if (mt < NH) {
-          float4 r;
-          r.x = fmaf((float)(c01[1] * 256 + c01[0]), dsel, -bsel);
-          r.y = fmaf((float)(c01[3] * 256 + c01[2]), dsel * 0.25f, -bsel);
-          r.z = fmaf((float)(c23[1] * 256 + c23[0]), dsel * 0.0625f, -bsel);
-          r.w = fmaf((float)(c23[3] * 256 + c23[2]), dsel * 0.015625f, -bsel);
-          reinterpret_cast<float4 *>(lgs + mt * G)[tq] = r;
-        }
+        if (rhead < NH)
+          reinterpret_cast<float4 *>(lgw)[tq] =
+              make_float4(fmaf(wB, (float)c01[1], (float)c01[0]), fmaf(wB, (float)c01[3], (float)c01[2]),
+                          fmaf(wB, (float)c23[1], (float)c23[0]), fmaf(wB, (float)c23[3], (float)c23[2]));
       }
       __syncwarp();
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
-        const float4 r = reinterpret_cast<const float4 *>(lgs + h * G)[ktq];
-        lg[h][0] = (sbits & 1u) ? -INFINITY : r.x;
-        lg[h][1] = (sbits & 2u) ? -INFINITY : r.y;
-        lg[h][2] = (sbits & 4u) ? -INFINITY : r.z;
-        lg[h][3] = (sbits & 8u) ? -INFINITY : r.w;
+        const float4 e = reinterpret_cast<const float4 *>(lgs + h * D)[ktq];
+        const float4 o = reinterpret_cast<const float4 *>(lgs + (NH + h) * D)[ktq];
+        const float d0 = dA[h], d1 = dA[h] * 0.25f, d2 = dA[h] * 0.0625f, d3 = dA[h] * 0.015625f;
+        lg[h][0] = (sbits & 1u) ? -INFINITY : fmaf(65536.f * d0, o.x, d0 * e.x);
+        lg[h][1] = (sbits & 2u) ? -INFINITY : fmaf(65536.f * d1, o.y, d1 * e.y);
+        lg[h][2] = (sbits & 4u) ? -INFINITY : fmaf(65536.f * d2, o.z, d2 * e.z);
+        lg[h][3] = (sbits & 8u) ? -INFINITY : fmaf(65536.f * d3, o.w, d3 * e.w);
       }
       }   // per-channel K
     } else if (s.kind == 1) {
@@ -794,7 +839,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
             wmax = fmaxf(wmax, wv[k]);
           }
           wmax = warp_max(wmax);
-          // 16-bit fixed point of the page's largest weight; the zero-point
+          // 24-bit fixed point of the page's largest weight; the zero-point
           // term uses the same rounded weights (incoherent rounding error)
           const float invw = wmax > 0.f ? __fdividef((float)kWMax, wmax) : 0.f;
           uint32_t W[4];
@@ -807,10 +852,10 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           dwv[h][gi] = wmax * (1.0f / (float)kWMax);
           zl[h][gi] = fmaf(zl[h][gi], sc, kcs == 0 ? dwv[h][gi] * zs : 0.f);   // lane partial
           if (kcs == 0) {
-            const uint32_t lo = prmt(prmt(W[0], W[1], 0x0040), prmt(W[2], W[3], 0x0040), 0x5410);
-            const uint32_t hi = prmt(prmt(W[0], W[1], 0x0051), prmt(W[2], W[3], 0x0051), 0x5410);
-            wlimb[(gi * 2 * NH + 2 * h) * TQ + ktq] = lo;
-            wlimb[(gi * 2 * NH + 2 * h + 1) * TQ + ktq] = hi;
+            uint32_t *wl = wlimb + (gi * kLimbCols * NH + kLimbCols * h) * TQ + ktq;
+            wl[0] = prmt(prmt(W[0], W[1], 0x0040), prmt(W[2], W[3], 0x0040), 0x5410);
+            wl[TQ] = prmt(prmt(W[0], W[1], 0x0051), prmt(W[2], W[3], 0x0051), 0x5410);
+            wl[2 * TQ] = prmt(prmt(W[0], W[1], 0x0062), prmt(W[2], W[3], 0x0062), 0x5410);
           }
         }
       }
@@ -821,26 +866,25 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       // smem to the lane layout of o_rot (lane vcq: channels 4 vcq ..).
       constexpr int TC = G / 32;
       const uint32_t *vcw = reinterpret_cast<const uint32_t *>(vc4);
+      const float wBv = rodd ? 0.f : 256.f;
+      float *lvw = lgs + (rodd ? NH : 0) * D + min(rhead, NH - 1) * D;
       AKVQ_UNROLL(AKVQ_VU)
       for (int cb = 0; cb < D / 32; ++cb) {
         const int cq = 8 * cb + mg, gi = (32 * cb) / G;
         int c01[4] = {0, 0, 0, 0}, c23[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int cc = 0; cc < TC; ++cc) {
-          const uint2 b = *reinterpret_cast<const uint2 *>(wlimb + (gi * 2 * NH + mcol) * TQ + 8 * cc + 2 * mt);
+          const uint2 b = *reinterpret_cast<const uint2 *>(wlimb + (gi * kLimbCols * NH + mcol) * TQ + 8 * cc + 2 * mt);
           const uint2 w = *reinterpret_cast<const uint2 *>(vcw + vword_idx(cq, 8 * cc + 2 * mt, CQ));
           mma_u8u8(c01, fmask(w.x, 0), fmask(w.x, 1), fmask(w.y, 0), fmask(w.y, 1), b.x, b.y);
           mma_u8u8(c23, fmask(w.x, 2), fmask(w.x, 3), fmask(w.y, 2), fmask(w.y, 3), b.x, b.y);
         }
-        if (mt < NH) {
-          // < 2^31: G tokens x 192 x 255 x 257 per column pair
-          float4 r;
-          r.x = (float)(c01[1] * 256 + c01[0]);
-          r.y = (float)(c01[3] * 256 + c01[2]) * 0.25f;
-          r.z = (float)(c23[1] * 256 + c23[0]) * 0.0625f;
-          r.w = (float)(c23[3] * 256 + c23[2]) * 0.015625f;
-          reinterpret_cast<float4 *>(lgs + mt * D)[cq] = r;
-        }
+        // per limb column: <= G tokens x 192 x 255 < 2^31 (exact); even lanes
+        // store limb 0 + 256 limb 1, odd lanes limb 2 (x 65536 in the reader)
+        if (rhead < NH)
+          reinterpret_cast<float4 *>(lvw)[cq] =
+              make_float4(fmaf(wBv, (float)c01[1], (float)c01[0]), fmaf(wBv, (float)c01[3], (float)c01[2]),
+                          fmaf(wBv, (float)c23[1], (float)c23[0]), fmaf(wBv, (float)c23[3], (float)c23[2]));
       }
       __syncwarp();
       if (vts == 0) {
@@ -850,11 +894,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           float dw = dwv[h][0];
 #pragma unroll
           for (int gi = 1; gi < NG; ++gi) if (gi == vgam) dw = dwv[h][gi];
-          const float4 r = reinterpret_cast<const float4 *>(lgs + h * D)[vcq];
-          o_rot[h][0] = fmaf(dw, r.x, o_rot[h][0]);     // zero term: zl, subtracted at flush
-          o_rot[h][1] = fmaf(dw, r.y, o_rot[h][1]);
-          o_rot[h][2] = fmaf(dw, r.z, o_rot[h][2]);
-          o_rot[h][3] = fmaf(dw, r.w, o_rot[h][3]);
+          const float4 e = reinterpret_cast<const float4 *>(lgs + h * D)[vcq];
+          const float4 o = reinterpret_cast<const float4 *>(lgs + (NH + h) * D)[vcq];
+          // channel 4 vcq + k carried the factor 4^k; zero term: zl, subtracted at flush
+          o_rot[h][0] = fmaf(dw, fmaf(65536.f, o.x, e.x), o_rot[h][0]);
+          o_rot[h][1] = fmaf(dw * 0.25f, fmaf(65536.f, o.y, e.y), o_rot[h][1]);
+          o_rot[h][2] = fmaf(dw * 0.0625f, fmaf(65536.f, o.z, e.z), o_rot[h][2]);
+          o_rot[h][3] = fmaf(dw * 0.015625f, fmaf(65536.f, o.w, e.w), o_rot[h][3]);
         }
       }
     } else {
@@ -953,6 +999,7 @@ int layer_supported(int d, int G, int g) {
 #ifndef AKVQ_GQA_NH
 #define AKVQ_GQA_NH 2
 #endif
+static_assert(AKVQ_GQA_NH == 2, "head groups of 2 (4 limb columns per head, one MMA n-tile)");
 int layer_group_heads(int g) { return g <= 2 ? g : AKVQ_GQA_NH; }
 int layer_head_groups(int g) { return (g + layer_group_heads(g) - 1) / layer_group_heads(g); }
 int layer_warps_per_cta() { return kLyWarps; }
@@ -967,7 +1014,7 @@ static cudaError_t launch_ly_g(const DevCache &c, const LayerPlan &lp, const voi
   const int nh = layer_group_heads(c.g);      // lp.hg = ceil(g / nh) groups per kv head
   if (nh == 1) return launch_ly<D, G, DT, 1>(c, lp, q, k, v, types, part, out, flags, st);
   if (nh == 2) return launch_ly<D, G, DT, 2>(c, lp, q, k, v, types, part, out, flags, st);
-  return launch_ly<D, G, DT, 4>(c, lp, q, k, v, types, part, out, flags, st);
+  return cudaErrorInvalidValue;               // 4 limb columns per head: <= 2 heads per n-tile
 }
 
 cudaError_t launch_decode_layer(const DevCache &c, int dtype16, const LayerPlan &lp, const void *q,

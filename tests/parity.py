@@ -19,7 +19,8 @@ def record_margin(case: str, worst: float, tol: float, rep: dict | None = None, 
     m["margin"] = tol / m["worst_out_err"] if m["worst_out_err"] > 0 else None
     for k, v in (rep or {}).items():
         m[k] = m.get(k, 0) + v
-    m.update(extra)
+    for k, v in extra.items():
+        m[k] = max(m.get(k, v), v) if isinstance(v, float) else v
 
 
 def f16_bits(t: torch.Tensor) -> np.ndarray:

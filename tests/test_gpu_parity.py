@@ -50,42 +50,55 @@ def _configs(ak, orc, w, layer, units_n, kind=None, cap=None, k_axis=0, decide64
 
 
 def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every=1,
-              flags=0, report=None, options=0, fused_step=None, k_axis=0, decide64=1,
+              flags=0, report=None, options=0, fused_step=None, k_axis=0,
               xf_layer=None, xf_decode=None, case=None):
     """Prefill + `steps` decode steps on the GPU for all units; the oracle runs the
-    sampled `units` (default all).  Compares state after prefill and after every
-    flush, outputs every `check_every` steps.  decide64: the oracle's decision
-    precision (1 = fp64, the contract; 0 = fp32, R6).  xf_layer / xf_decode:
-    input transforms (stress cases) applied identically to the GPU inputs and
-    the oracle's sampled inputs.  The worst output error and the tie counts go
-    to the margins report (parity.MARGINS)."""
+    sampled `units` (default all) in BOTH decision precisions: fp64 (SURVEY 8(c),
+    the contract) and fp32 (R6, the kernel's).  The cache state is compared with
+    each after prefill and after every flush (bit-exact modulo documented ties),
+    the outputs every `check_every` steps: within OUT_TOL of the fp32-decision
+    oracle always, and of the fp64-decision oracle unless the state comparison
+    found a documented tie (one tied code on a heavily attended token moves the
+    output by up to scale * p).  xf_layer / xf_decode: input
+    transforms (stress cases) applied identically to the GPU inputs and the
+    oracle's sampled inputs.  Worst errors and tie counts go to parity.MARGINS."""
     U = w.U
     us = list(range(U)) if units is None else list(units)
     gcfg, _ = _configs(ak, orc, w, layer, U, kind, k_axis=k_axis)
-    _, ocfg = _configs(ak, orc, w, layer, len(us), kind, k_axis=k_axis, decide64=decide64)
-    rep = {} if report is None else report
+    ocfgs = [_configs(ak, orc, w, layer, len(us), kind, k_axis=k_axis, decide64=d)[1]
+             for d in (1, 0)]
+    rep64 = {} if report is None else report
+    rep32 = {}
     dev = "cuda"
     inp = sy.layer_inputs(w, layer, device=dev)
     if xf_layer:
         inp = xf_layer(inp)
     lc = ak.LayerCache(gcfg, options=options)
     lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
-    oc = orc.OracleCache(ocfg)
     inp_o = sy.layer_inputs(w, layer, units=us, device="cpu")
     if xf_layer:
         inp_o = xf_layer(inp_o)
     # the CPU-generated sampled units are the GPU's units (counter-based generator)
     assert torch.equal(inp_o["K"], inp["K"][us].cpu())
     assert torch.equal(inp_o["V"], inp["V"][us].cpu())
-    assert oc.prefill(f16_bits(inp_o["K"]), f16_bits(inp_o["V"]), inp_o["types"].numpy(),
-                      inp_o["colsum"].numpy()) == 0
+    ocs = [orc.OracleCache(c) for c in ocfgs]
+    for oc in ocs:
+        assert oc.prefill(f16_bits(inp_o["K"]), f16_bits(inp_o["V"]), inp_o["types"].numpy(),
+                          inp_o["colsum"].numpy()) == 0
+    oc = ocs[0]
     rows_k = [f16_bits(inp_o["K"])]
     rows_v = [f16_bits(inp_o["V"])]
-    gs = GpuState(lc)
-    assert (gs.L, gs.n_q) == (oc.L, oc.nq)
-    compare_state(gs, oc.export(), gcfg, rep, units=us)
-    compare_ring(gs, np.concatenate(rows_k, 1), np.concatenate(rows_v, 1), gs.ring.shape[1], us)
-    worst = 0.0
+
+    def check_state():
+        gs = GpuState(lc)
+        assert (gs.L, gs.n_q) == (oc.L, oc.nq)
+        compare_state(gs, ocs[0].export(), gcfg, rep64, units=us)
+        compare_state(gs, ocs[1].export(), gcfg, rep32, units=us)
+        compare_ring(gs, np.concatenate(rows_k, 1), np.concatenate(rows_v, 1), gs.ring.shape[1], us)
+
+    check_state()
+    worst = [0.0, 0.0]
+    name = case or _case_name()
     for step in range(steps):
         di = sy.decode_inputs(w, layer, step, device=dev)
         if xf_decode:
@@ -100,24 +113,27 @@ def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every
         do = sy.decode_inputs(w, layer, step, units=us, device="cpu")
         if xf_decode:
             do = xf_decode(do)
-        oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
+        for o in ocs:
+            o.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
         rows_k.append(f16_bits(do["k"])[:, None])
         rows_v.append(f16_bits(do["v"])[:, None])
         assert (lc.L, lc.n_q) == (oc.L, oc.nq)
         if lc.n_q != nq_before:
-            gs = GpuState(lc)
-            compare_state(gs, oc.export(), gcfg, rep, units=us)
-            compare_ring(gs, np.concatenate(rows_k, 1), np.concatenate(rows_v, 1),
-                         gs.ring.shape[1], us)
+            check_state()
         if step % check_every == 0 or step == steps - 1:
-            ref = oc.decode(f16_bits(do["q"]), out_rotated=bool(flags & ak.AKVQ_OUT_ROTATED))
             got = out[us].double().cpu().numpy()
-            err = np.abs(got - ref).max()
-            worst = max(worst, err)
-            record_margin(case or _case_name(), worst, OUT_TOL, None, decide64=decide64)
-            assert err <= OUT_TOL, f"step {step}: max-abs {err}"
-    record_margin(case or _case_name(), worst, OUT_TOL, rep)
-    return lc, oc, worst
+            errs = [float(np.abs(got - o.decode(f16_bits(do["q"]),
+                                                out_rotated=bool(flags & ak.AKVQ_OUT_ROTATED))).max())
+                    for o in ocs]
+            worst = [max(a, b) for a, b in zip(worst, errs)]
+            ties64 = rep64.get("code_ties", 0) + rep64.get("zero_ties", 0)
+            record_margin(name, worst[1], OUT_TOL, None, worst_out_err_fp64_oracle=worst[0])
+            assert errs[1] <= OUT_TOL, f"step {step}: max-abs {errs[1]} vs the fp32-decision oracle"
+            assert errs[0] <= OUT_TOL or ties64 > 0, \
+                f"step {step}: max-abs {errs[0]} vs the fp64-decision oracle with no tie"
+    record_margin(name, worst[1], OUT_TOL, {k + "_fp64": v for k, v in rep64.items()},
+                  **{k + "_fp32": v for k, v in rep32.items()})
+    return lc, oc, worst[1]
 
 
 # ----------------------------------------------------------------- tiny (BJ:7)
@@ -389,15 +405,6 @@ def test_interleaved_layers_use_prologue(ak, orc, sy):
             ref = oc.decode(f16_bits(do["q"]))
             err = np.abs(out.double().cpu().numpy() - ref).max()
             assert err <= OUT_TOL, f"layer {layer} step {step}: {err}"
-
-
-# ----------------------------------------------------------------- decision precision
-@pytest.mark.parametrize("layer", [0, 2], ids=["TSA-L0", "PSA-L2"])
-def test_llava7b_fp32_decision_oracle(ak, orc, sy, layer):
-    """The same 7B layer against the oracle's fp32-decision mode (R6, the
-    kernel's precision): codes agree bit for bit unless the GPU's fp32 butterfly
-    sum differs from the correctly rounded x.H_s right at a tie."""
-    _run_case(ak, orc, sy, sy.LLAVA7B, layer, steps=3, decide64=0)
 
 
 # ----------------------------------------------------------------- stress (fixed point)
