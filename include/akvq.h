@@ -116,6 +116,11 @@ typedef struct {
  *  ticket  [U * hg] u32                merge tickets of the fused decode, one
  *                                      per unit and GQA head group hg (zeroed
  *                                      at init, self-resetting)
+ *  umax    [U] f32 x 2                 largest |K scale| and |V scale| of the
+ *                                      unit's quantized pages (normalized
+ *                                      basis; zeroed at init, raised by every
+ *                                      quantize launch): the decode kernel's
+ *                                      fixed-point ranges
  *  side_cap = top_k (PSA) or cap (TSA).
  */
 typedef struct {
@@ -127,6 +132,7 @@ typedef struct {
   uint64_t side_idx_off, side_cnt_off;
   uint64_t side_off, side_entry_bytes;
   uint64_t ticket_off;
+  uint64_t umax_off;
   int32_t cap, n_pages, slots, bitmask_words, side_cap, ng;
 } akvq_layout;
 
@@ -162,6 +168,10 @@ typedef struct {
  * garbage); used to attribute the decode time (bench.py --skip-rows/pages). */
 #define AKVQ_OPT_SKIP_ROWS 4
 #define AKVQ_OPT_SKIP_PAGES 8
+/* Test hook: every 2-bit page's logits take the fast kernel's plain fp32 path
+ * (the one a page with an out-of-range zero-point bias takes) instead of the
+ * fixed-point MMA; results must match the oracle the same way. */
+#define AKVQ_OPT_EXACT_LOGITS 16
 
 typedef struct {      /* memory_report, host arithmetic           */
   double bytes_fp16, bytes_int4, bytes_int2, bytes_overhead;

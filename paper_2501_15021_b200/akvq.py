@@ -24,6 +24,7 @@ AKVQ_OPT_GENERIC_PAGES = 1
 AKVQ_OPT_STREAM_ONLY = 2
 AKVQ_OPT_SKIP_ROWS = 4
 AKVQ_OPT_SKIP_PAGES = 8
+AKVQ_OPT_EXACT_LOGITS = 16
 AKVQ_MAX_PSA_PROMPT = 49152
 
 # every symbol include/akvq.h declares
@@ -53,7 +54,7 @@ class akvq_layout(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "total_bytes", "pages_off", "page_bytes", "pg_kscale", "pg_kzero", "pg_kcodes",
         "pg_vscale", "pg_vzero", "pg_vcodes", "ring_off", "ring_unit_bytes", "bitmask_off",
-        "side_idx_off", "side_cnt_off", "side_off", "side_entry_bytes", "ticket_off")] + [
+        "side_idx_off", "side_cnt_off", "side_off", "side_entry_bytes", "ticket_off", "umax_off")] + [
         (n, C.c_int32) for n in ("cap", "n_pages", "slots", "bitmask_words", "side_cap", "ng")]
 
 

@@ -47,6 +47,7 @@ DevCache make_dev(const akvq_cache *c) {
   d.side_cnt = reinterpret_cast<int32_t *>(b + y.side_cnt_off);
   d.side = b + y.side_off;
   d.ticket = reinterpret_cast<uint32_t *>(b + y.ticket_off);
+  d.umax = reinterpret_cast<float2 *>(b + y.umax_off);
   d.page_bytes = (uint32_t)y.page_bytes;
   d.pg_kscale = (uint32_t)y.pg_kscale; d.pg_kzero = (uint32_t)y.pg_kzero;
   d.pg_kcodes = (uint32_t)y.pg_kcodes; d.pg_vscale = (uint32_t)y.pg_vscale;
@@ -160,6 +161,7 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
     if (c->options & AKVQ_OPT_SKIP_ROWS) lp.Rc = lp.Sc = 0;       // profiling hooks
     if (c->options & AKVQ_OPT_SKIP_PAGES) lp.P = 0;
     lp.per_u = lp.P + lp.Rc + lp.Sc;
+    lp.sc_inv = lp.Sc > 0 ? 1.0f / (float)lp.Sc : 0.f;
     lp.nq_mod = n_q % c->lay.slots;
     if (lp.per_u > kLyMaxTab) {           // beyond the item table: generic kernels
       p.fast = 0;
@@ -230,6 +232,7 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
       lp.per_u = 1;
     }
     lp.stream_only = (c->options & AKVQ_OPT_STREAM_ONLY) ? 1 : 0;
+    lp.exact_logits = (c->options & AKVQ_OPT_EXACT_LOGITS) ? 1 : 0;
     if (p.fast) p.n_page_splits = p.n_ring_splits = p.n_side_splits = 0;
   }
   p.S = p.n_page_splits + p.n_ring_splits + p.n_side_splits;
@@ -299,6 +302,9 @@ akvq_status akvq_cache_layout(const akvq_config *f, akvq_layout *y) {
   y->side_off = t;     t = align_up(t + U * y->side_cap * y->side_entry_bytes, 256);
   // one merge ticket per virtual unit of the decode kernel (unit x GQA head group)
   y->ticket_off = t;   t = align_up(t + U * (uint64_t)layer_head_groups(f->q_per_kv) * 4, 256);
+  // per unit: the largest |K scale| and |V scale| stored so far (the decode
+  // kernel's fixed-point ranges; maintained by the quantize kernel)
+  y->umax_off = t;     t = align_up(t + U * 8, 256);
   y->total_bytes = t;
   return AKVQ_OK;
 }

@@ -21,7 +21,8 @@ struct DevCache {
   int32_t *side_idx;       // [U][side_cap]
   int32_t *side_cnt;       // [U]
   uint8_t *side;           // [U][side_cap][side_entry]
-  uint32_t *ticket;        // [U] decode-merge tickets (zero between launches)
+  uint32_t *ticket;        // [U * hg] decode-merge tickets (zero between launches)
+  float2 *umax;            // [U] (max |K scale|, max |V scale|) of the unit's pages
   uint32_t page_bytes, pg_kscale, pg_kzero, pg_kcodes, pg_vscale, pg_vzero, pg_vcodes;
   uint32_t side_entry;
   int32_t n_pages, slots, bm_words, side_cap;

@@ -58,16 +58,17 @@ constexpr int kRows4 = 32;         // 4-bit TSA rows per side sub-load
 #endif
 #define AKVQ_PRAGMA(x) _Pragma(#x)
 #define AKVQ_UNROLL(n) AKVQ_PRAGMA(unroll n)
-// Page fixed points: three 8-bit limbs each, i.e. 24-bit
-// precision relative to the page's largest |q~ s^K| / largest softmax weight.
-//  K: |Q| <= kQMax < 127 * 65793, Q + kQOff in [0, 2^24), limb k = byte k of
-//     Q + kQOff, minus 128 (signed int8: byte ^ 0x80); kQMax leaves room for
-//     the 2-ulp error of __fdividef in the scale.
-//  V: 0 <= W <= 2^24 - 1, limb k = byte k (unsigned int8).
-// Each head owns 4 MMA B columns: limbs 0, 1, 2 and one unused column.
+// Page fixed points: signed 24-bit integers as three int8 limbs,
+// relative to per-unit ranges (umax: the largest |K| / |V| scale of the unit's
+// pages, maintained by the quantizer).
+//  K: Q_c = rn(q~_c s^K_c kQMax / (max|q~| umax.K)), |Q| <= kQMax;
+//  V: W_t = rn(p_t s^V_t kQMax / umax.V), |W| <= kQMax (p <= 1).
+// X + kQOff lies in [0, 2^24); limb k = byte k of X + kQOff minus 128 (signed
+// int8: byte ^ 0x80).  kQMax < 127 * 65793 leaves room for the few-ulp error of
+// __fdividef and the products.  Each head owns 4 MMA B columns: limbs 0, 1, 2
+// and one unused column.
 constexpr int kQMax = 8355700;
 constexpr uint32_t kQOff = 0x808080u;
-constexpr int kWMax = 16777215;
 constexpr int kLimbCols = 4;
 #ifndef AKVQ_LY_CTAS
 #define AKVQ_LY_CTAS 4
@@ -88,8 +89,12 @@ struct LySmem {
   static __host__ __device__ size_t vl_off(size_t sb) { return kl_off(sb); }   // shared
   // page logits [NH][G] / page V sums [NH][D] (fp32, one at a time)
   static __host__ __device__ size_t lv_off(size_t sb) { return kl_off(sb) + (KL > VL ? KL : VL); }
-  // [2][NH][D] f32: per-limb-pair partial sums (even / odd MMA lanes), G <= D
-  static __host__ __device__ size_t ds_off(size_t sb) { return lv_off(sb) + (size_t)2 * NH * D * 4; }
+  // [2][NH + 1][D] f32: per-limb-pair partial sums (even / odd MMA lanes; row NH
+  // takes the stores of padded lanes, so the epilogue needs no branch), G <= D
+  // rows are LP = D + 8 floats apart: the 4 MMA lanes of a fragment group (rows
+  // even/odd x head/dummy) then store to distinct banks
+  static constexpr int LP = D + 8;
+  static __host__ __device__ size_t ds_off(size_t sb) { return lv_off(sb) + (size_t)2 * (NH + 1) * LP * 4; }
   static __host__ __device__ size_t bar_off(size_t sb) { return ds_off(sb) + kLyStages * 32; }
   static __host__ __device__ size_t warp_bytes(size_t sb) {
     return (bar_off(sb) + kLyStages * 8 + 127) / 128 * 128;
@@ -131,14 +136,6 @@ __device__ __forceinline__ void mma_u8s8(int (&c)[4], uint32_t a0, uint32_t a1, 
       : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ void mma_u8u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
-  asm(
-      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
 template <int DT>
 __device__ __forceinline__ void cvt2(uint32_t w, float &a, float &b) {
   if constexpr (DT == AKVQ_BF16) {
@@ -257,7 +254,6 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   float *qh = reinterpret_cast<float *>(wsm + S::qh_off(SB));
   uint32_t *klimb = reinterpret_cast<uint32_t *>(wsm + S::kl_off(SB));
   uint32_t *vlimb = reinterpret_cast<uint32_t *>(wsm + S::vl_off(SB));
-  uint2 *desc = reinterpret_cast<uint2 *>(wsm + S::ds_off(SB));
   uint64_t *bar = reinterpret_cast<uint64_t *>(wsm + S::bar_off(SB));
 
   // Programmatic dependent launch: q, k, v (and, after a flush or append, the
@@ -281,15 +277,34 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   const float alpha_o = kLog2e * c.inv_sqrt_d; // q.k / sqrt d in log2 units
   const uint32_t kbytes = c.pg_vscale, vbytes = c.page_bytes - c.pg_vscale;
 
-  // ---- producer (lane 0): walks the items, issues TMA sub-loads, records them
+  // ---- producer: every lane walks the same items (warp-uniform state, the
+  // descriptors of the two stages stay in registers); lane 0 issues the TMA
+  // sub-loads.  A page is two sub-loads (K half, V half); the V half is issued
+  // from the pointer remembered with the K half.
   if (lane == 0) {
     for (int s = 0; s < kLyStages; ++s) mbar_init(&bar[s]);
     mbar_fence_init();
   }
-  // producer state: unit, table entry, sub-load within a side split
+  __syncwarp();
   int pu = ib / lp.per_u, pj = ib - (ib / lp.per_u) * lp.per_u, left = ie - ib, part_i = 0;
   int pphys = pu / HG, phg = pu - (pu / HG) * HG;   // physical unit / head group of pu
-  auto produce = [&](int st) {                  // lane 0 only
+  const uint8_t *ubase = c.pages + (size_t)pphys * c.n_pages * c.page_bytes;   // pages of pphys
+  const uint8_t *vsrc = nullptr;                // pending V half (issued next)
+  uint2 vdesc = make_uint2(0u, 0u);
+  // salient bits of a page's tokens, loaded with its K half (this lane's word:
+  // tokens 32 (ktq >> 3) .. of the page, the lane's token quad is ktq)
+  uint32_t pbits = 0u;
+  const int pbw = (lane % (G / 4)) >> 3;
+  auto produce = [&](int st) -> uint2 {
+    uint8_t *dst = wsm + (size_t)st * SB;
+    if (vsrc != nullptr) {                      // V half of the page whose K half went last
+      if (lane == 0) {
+        mbar_expect_tx(&bar[st], vbytes);
+        bulk_g2s(dst, vsrc, vbytes, &bar[st]);
+      }
+      vsrc = nullptr;
+      return vdesc;
+    }
     LySub sb;
     sb.kind = -1;
     while (left > 0) {
@@ -300,15 +315,22 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       sb.u = pu;
       sb.pu = pphys;
       sb.ring = 0;
-      if (kind == 0) {                            // page: K half then V half
-        sb.kind = part_i; sb.a = a; sb.n = 0;      // (n unused for pages; 6-bit field)
-        next = part_i == 1;
-        part_i = next ? 0 : 1;
+      sb.a = a;
+      if (kind == 0) {                            // page: K half now, V half next
+        sb.kind = 0; sb.n = 0;
       } else if (kind == 2) {                     // ring chunk (rows n of it)
-        sb.kind = 2; sb.ring = 1; sb.a = a; sb.n = n;
+        sb.kind = 2; sb.ring = 1; sb.n = n;
       } else {                                    // side split a: entries [lo, hi), runtime count
         const int cnt = __ldg(c.side_cnt + pphys);
-        const int lo = a * cnt / lp.Sc, hi = (a + 1) * cnt / lp.Sc;   // 32-bit: cnt <= capacity
+        // floor(a cnt / Sc) and floor((a + 1) cnt / Sc): fp32 estimate, corrected
+        // (a cnt < 2^24: cnt <= capacity, a < Sc <= 8)
+        auto fdiv = [&](int x) {
+          int qd = __float2int_rz((float)x * lp.sc_inv);
+          qd += (qd + 1) * lp.Sc <= x;
+          qd -= qd * lp.Sc > x;
+          return qd;
+        };
+        const int lo = fdiv(a * cnt), hi = fdiv((a + 1) * cnt);
         const int per = tsa ? kRows4 : kRows;
         sb.kind = tsa ? 3 : 2;
         sb.a = lo + part_i * per;
@@ -317,47 +339,59 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         next = !ok;
         part_i = ok ? part_i + 1 : 0;
       }
+      const uint8_t *pg = ubase + (size_t)a * c.page_bytes;   // (pages only)
       if (next) {
         if (++pj == lp.per_u) {
           pj = 0;
           ++pu;
-          if (++phg == HG) { phg = 0; ++pphys; }
+          if (++phg == HG) { phg = 0; ++pphys; ubase += (size_t)c.n_pages * c.page_bytes; }
         }
         --left;
       }
-      if (ok) break;
+      if (ok) {
+        if (sb.kind == 0) {
+          if (lane == 0) {
+            mbar_expect_tx(&bar[st], kbytes);
+            bulk_g2s(dst, pg, kbytes, &bar[st]);
+          }
+          pbits = __ldg(c.bitmask + (size_t)sb.pu * c.bm_words + (size_t)a * (G / 32) + pbw);
+          vsrc = pg + kbytes;
+          LySub vb = sb;
+          vb.kind = 1;
+          vdesc = pack_sub(vb);
+        } else if (sb.ring) {
+          int s0 = lp.nq_mod + sb.a;              // ring slot of row n_q + a
+          if (s0 >= c.slots) s0 -= c.slots;
+          const int n1 = min(sb.n, c.slots - s0);
+          const uint32_t rowb = 4 * D;
+          if (lane == 0) {
+            mbar_expect_tx(&bar[st], (uint32_t)sb.n * rowb);
+            bulk_g2s(dst, ring_row(c, sb.pu, s0), (uint32_t)n1 * rowb, &bar[st]);
+            if (n1 < sb.n)
+              bulk_g2s(dst + (size_t)n1 * rowb, ring_row(c, sb.pu, 0), (uint32_t)(sb.n - n1) * rowb, &bar[st]);
+          }
+        } else {
+          const uint32_t eb = c.side_entry;
+          if (lane == 0) {
+            mbar_expect_tx(&bar[st], (uint32_t)sb.n * eb);
+            bulk_g2s(dst, side_ptr(c, sb.pu, sb.a), (uint32_t)sb.n * eb, &bar[st]);
+          }
+        }
+        break;
+      }
       sb.kind = -1;
     }
-    desc[st] = pack_sub(sb);
-    if (sb.kind < 0) return;
-    uint8_t *dst = wsm + (size_t)st * SB;
-    if (sb.kind <= 1) {
-      const uint8_t *src = page_ptr(c, sb.pu, sb.a) + (sb.kind ? kbytes : 0u);
-      const uint32_t nb = sb.kind ? vbytes : kbytes;
-      mbar_expect_tx(&bar[st], nb);
-      bulk_g2s(dst, src, nb, &bar[st]);
-    } else if (sb.ring) {
-      int s0 = lp.nq_mod + sb.a;                  // ring slot of row n_q + a
-      if (s0 >= c.slots) s0 -= c.slots;
-      const int n1 = min(sb.n, c.slots - s0);
-      const uint32_t rowb = 4 * D;
-      mbar_expect_tx(&bar[st], (uint32_t)sb.n * rowb);
-      bulk_g2s(dst, ring_row(c, sb.pu, s0), (uint32_t)n1 * rowb, &bar[st]);
-      if (n1 < sb.n)
-        bulk_g2s(dst + (size_t)n1 * rowb, ring_row(c, sb.pu, 0), (uint32_t)(sb.n - n1) * rowb, &bar[st]);
-    } else {
-      const uint32_t eb = c.side_entry;
-      mbar_expect_tx(&bar[st], (uint32_t)sb.n * eb);
-      bulk_g2s(dst, side_ptr(c, sb.pu, sb.a), (uint32_t)sb.n * eb, &bar[st]);
-    }
+    return pack_sub(sb);
   };
-  if (lane == 0)
-    for (int s = 0; s < kLyStages; ++s) produce(s);
+  uint2 dsc0 = produce(0);
+  uint32_t bits0 = pbits;
+  uint2 dsc1 = produce(1);
+  uint32_t bits1 = pbits;
+  static_assert(kLyStages == 2, "two stages: descriptors dsc0 / dsc1");
   if (lp.prologue) {                            // inputs from the preceding grid from here on
     pdl_wait();
     pdl_launch_dependents();
   }
-  __syncwarp();
 
   // lane roles
   const int ktq = lane % TQ, kcs = lane / TQ;         // page K phase
@@ -383,6 +417,11 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   // reduced across the warp once per segment in flush
   float m_run[NH], l_run[NH], o_rot[NH][4], o_org[NH][4], zl[NH][NG];
   float qk[NH][4], qt[NH][4], qsum[NH];               // q (orig) * alpha_o; q~ * alpha_k; sum
+  // per-unit fixed points (per-channel K): Q_c = rn(q~_c s^K_c inv), inv =
+  // kQMax / (max_c |q~_c| * umax.K), so |Q| <= kQMax on every page of the unit;
+  // qinv = q~ * inv for the lane's channel quad; dA = alpha_k / inv.  V weights:
+  // W_t = rn(p_t s^V_t winv) with winv = kQMax / umax.V (p <= 1), dw = 1 / winv.
+  float qinv[NH][4], dAu[NH], winv = 0.f, dwu = 0.f;
   float lg[NH][4];                                    // page logits of the lane's token quad
   int cur_u = -1, cur_pu = 0, cur_hg = 0;      // virtual unit, its physical unit and head group
   const int u_first = ib / lp.per_u;
@@ -512,14 +551,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   int st = 0;
   uint32_t par = 0;
   for (;;) {
-    const LySub s = unpack_sub(desc[st]);
+    const LySub s = unpack_sub(st ? dsc1 : dsc0);
     if (s.kind < 0) break;
     uint8_t *B = wsm + (size_t)st * SB;
     if constexpr (SO) {                             // profiling: pipeline only
       mbar_wait(&bar[st], par);
       __syncwarp();
-      if (lane == 0) produce(st);
-      __syncwarp();
+      if (st) { dsc1 = produce(st); bits1 = pbits; } else { dsc0 = produce(st); bits0 = pbits; }
       if (++st == kLyStages) { st = 0; par ^= 1u; }
       continue;
     }
@@ -569,6 +607,19 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         qt[h][0] = t4.x * alpha_k; qt[h][1] = t4.y * alpha_k;
         qt[h][2] = t4.z * alpha_k; qt[h][3] = t4.w * alpha_k;
         qsum[h] = (qt[h][0] + qt[h][1]) + (qt[h][2] + qt[h][3]);
+        if constexpr (!KT) {
+          const float2 um = c.umax[cur_pu];
+          const float M = warp_max(fmaxf(fmaxf(fabsf(t4.x), fabsf(t4.y)), fmaxf(fabsf(t4.z), fabsf(t4.w)))) * um.x;
+          const float inv = M > 0.f ? __fdividef((float)kQMax, M) : 0.f;
+          dAu[h] = alpha_k * M * (1.0f / (float)kQMax);
+          qinv[h][0] = t4.x * inv; qinv[h][1] = t4.y * inv; qinv[h][2] = t4.z * inv; qinv[h][3] = t4.w * inv;
+          winv = um.y > 0.f ? __fdividef((float)kQMax, um.y) : 0.f;
+          dwu = um.y * (1.0f / (float)kQMax);
+        } else {
+          const float um_v = c.umax[cur_pu].y;
+          winv = um_v > 0.f ? __fdividef((float)kQMax, um_v) : 0.f;
+          dwu = um_v * (1.0f / (float)kQMax);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) { qk[h][k] *= alpha_o; o_rot[h][k] = 0.f; o_org[h][k] = 0.f; }
         m_run[h] = -INFINITY;
@@ -580,9 +631,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
 
     if (s.kind == 0) {
       // ================= page K half: logits of the page's G tokens
-      const uint32_t sbits =
-          (__ldg(c.bitmask + (size_t)cur_pu * c.bm_words + (size_t)s.a * (G / 32) + (ktq >> 3)) >>
-           (4 * (ktq & 7))) & 15u;
+      const uint32_t sbits = ((st ? bits1 : bits0) >> (4 * (ktq & 7))) & 15u;
       mbar_wait(&bar[st], par);
       const float4 *ks4 = reinterpret_cast<const float4 *>(B + c.pg_kscale);
       const int4 *kz4 = reinterpret_cast<const int4 *>(B + c.pg_kzero);
@@ -688,13 +737,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           if (!rodd && rhead < NH) {
             float4 r;
             r.x = part[0] * dsel; r.y = part[1] * dsel; r.z = part[2] * dsel; r.w = part[3] * dsel;
-            reinterpret_cast<float4 *>(lgs + rhead * D)[tq] = r;
+            reinterpret_cast<float4 *>(lgs + rhead * S::LP)[tq] = r;
           }
         }
         __syncwarp();
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-          const float4 r = reinterpret_cast<const float4 *>(lgs + h * D)[ktq];
+          const float4 r = reinterpret_cast<const float4 *>(lgs + h * S::LP)[ktq];
           lg[h][0] = (sbits & 1u) ? -INFINITY : r.x;
           lg[h][1] = (sbits & 2u) ? -INFINITY : r.y;
           lg[h][2] = (sbits & 4u) ? -INFINITY : r.z;
@@ -704,34 +753,27 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       float dA[NH];
       int bA[NH][3];
 #pragma unroll
-      for (int h = 0; h < NH; ++h) {      // Q_c = rn(q~_c s^K_c / delta): lane = channel quad
-        float qsb[4] = {0.f, 0.f, 0.f, 0.f}, am = 0.f;
+      for (int h = 0; h < NH; ++h) {      // Q_c = rn(q~_c s^K_c inv): lane = channel quad
+        float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
         int4 zq = make_int4(0, 0, 0, 0);
-        if (lane < CQ) {
-          const float4 qv = reinterpret_cast<const float4 *>(qh + h * D)[lane];
-          const float4 sv = ks4[lane];
-          zq = kz4[lane];
-          qsb[0] = qv.x * sv.x; qsb[1] = qv.y * sv.y; qsb[2] = qv.z * sv.z; qsb[3] = qv.w * sv.w;
-          am = fmaxf(fmaxf(fabsf(qsb[0]), fabsf(qsb[1])), fmaxf(fabsf(qsb[2]), fabsf(qsb[3])));
-        }
-        const float M = warp_max(am);
-        // fixed-point scale (any consistent inv / delta pair works: the sums are
-        // exact for the rounded Q; |Q| <= kQMax + 2 holds within __fdividef's error)
-        const float inv = M > 0.f ? __fdividef((float)kQMax, M) : 0.f;
-        const float delta = M * (1.0f / (float)kQMax);
+        if (lane < CQ) { sv = ks4[lane]; zq = kz4[lane]; }
         uint32_t x[4];
+        x[0] = (uint32_t)__float2int_rn(qinv[h][0] * sv.x) + kQOff;
+        x[1] = (uint32_t)__float2int_rn(qinv[h][1] * sv.y) + kQOff;
+        x[2] = (uint32_t)__float2int_rn(qinv[h][2] * sv.z) + kQOff;
+        x[3] = (uint32_t)__float2int_rn(qinv[h][3] * sv.w) + kQOff;
+        // zero-point bias B = sum_c Q_c z_c exactly (int64), split into limb
+        // terms B = b0 + 256 b1 + 65536 b2 with b0, b1 in [0, 255] (the MMA
+        // accumulators start at -4^k b_limb; |4^k b2| < 2^31 for any int32 z
+        // with |z| < 2^14)
+        long long bz = (long long)(int)(x[0] - kQOff) * zq.x + (long long)(int)(x[1] - kQOff) * zq.y +
+                       (long long)(int)(x[2] - kQOff) * zq.z + (long long)(int)(x[3] - kQOff) * zq.w;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) x[b] = (uint32_t)__float2int_rn(qsb[b] * inv) + kQOff;
-        // zero-point bias per limb: B_k = sum_c limb_k,c z_c (exact in int32)
-        const int zz[4] = {zq.x, zq.y, zq.z, zq.w};
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          int bk = 0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) bk += ((int)((x[b] >> (8 * k)) & 255u) - 128) * zz[b];
-          bA[h][k] = warp_sum_i(bk);
-        }
-        dA[h] = alpha_k * delta;
+        for (int o = 16; o > 0; o >>= 1) bz += __shfl_xor_sync(0xffffffffu, bz, o);
+        bA[h][0] = (int)(bz & 255);
+        bA[h][1] = (int)((bz >> 8) & 255);
+        bA[h][2] = (int)(bz >> 16);
+        dA[h] = dAu[h];
         if (lane < CQ) {
           qlimb[(4 * h) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0040), prmt(x[2], x[3], 0x0040), 0x5410) ^ 0x80808080u;
           qlimb[(4 * h + 1) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0051), prmt(x[2], x[3], 0x0051), 0x5410) ^ 0x80808080u;
@@ -739,6 +781,31 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         }
       }
       __syncwarp();
+      // Exactness needs |4^k b2| + |C| < 2^31, i.e. |b2| < 2^24 (zero points up to
+      // ~1000 in magnitude).  A page beyond that (a near-constant channel with a
+      // large offset: tiny range, huge zero point) takes the plain fp32 path:
+      // logit_t = alpha_k sum_c q~_c s_c (code_tc - z_c), each (code - z) exact.
+      bool slow = lp.exact_logits != 0;
+#pragma unroll
+      for (int h = 0; h < NH; ++h) slow |= bA[h][2] >= (1 << 24) || bA[h][2] <= -(1 << 24);
+      if (slow) {
+        const float *ksf = reinterpret_cast<const float *>(B + c.pg_kscale);
+        const int32_t *kzf = reinterpret_cast<const int32_t *>(B + c.pg_kzero);
+        const uint8_t *kcb = B + c.pg_kcodes;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int ch = 0; ch < D; ++ch) {
+            const float qs = qh[h * D + ch] * ksf[ch];
+            const float z = (float)kzf[ch];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              acc[k] = fmaf(qs, (float)kcode_at(kcb, 4 * ktq + k, ch, G) - z, acc[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) lg[h][k] = ((sbits >> k) & 1u) ? -INFINITY : alpha_k * acc[k];
+        }
+      } else {
       // logits by warp MMA: rows = tokens (row grp: token 4 tq + k0, grp + 8:
       // 4 tq + k1, tq = 8 blk + grp), K = 32 channels per chunk, columns = Q limbs
       // (4 h + k).  The masked code word (code << 2k per byte) is the A fragment
@@ -761,7 +828,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         if (hsel == h) { ba = bA[h][0]; bb = bA[h][1]; b2 = bA[h][2]; }
       if (rodd) { ba = b2; bb = 0; }
       const float wB = rodd ? 0.f : 256.f;
-      float *lgw = lgs + (rodd ? NH : 0) * D + hsel * D;
+      float *lgw = lgs + ((rodd ? NH + 1 : 0) + min(rhead, NH)) * S::LP;
       const uint32_t *kcw = reinterpret_cast<const uint32_t *>(B + c.pg_kcodes);
       AKVQ_UNROLL(AKVQ_KU)
       for (int blk = 0; blk < TQ / 8; ++blk) {
@@ -773,22 +840,22 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           mma_u8s8(c01, fmask(w.x, 0), fmask(w.x, 1), fmask(w.y, 0), fmask(w.y, 1), bq[cc][0], bq[cc][1]);
           mma_u8s8(c23, fmask(w.x, 2), fmask(w.x, 3), fmask(w.y, 2), fmask(w.y, 3), bq[cc][0], bq[cc][1]);
         }
-        if (rhead < NH)
-          reinterpret_cast<float4 *>(lgw)[tq] =
+        reinterpret_cast<float4 *>(lgw)[tq] =
               make_float4(fmaf(wB, (float)c01[1], (float)c01[0]), fmaf(wB, (float)c01[3], (float)c01[2]),
                           fmaf(wB, (float)c23[1], (float)c23[0]), fmaf(wB, (float)c23[3], (float)c23[2]));
       }
       __syncwarp();
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
-        const float4 e = reinterpret_cast<const float4 *>(lgs + h * D)[ktq];
-        const float4 o = reinterpret_cast<const float4 *>(lgs + (NH + h) * D)[ktq];
+        const float4 e = reinterpret_cast<const float4 *>(lgs + h * S::LP)[ktq];
+        const float4 o = reinterpret_cast<const float4 *>(lgs + (NH + 1 + h) * S::LP)[ktq];
         const float d0 = dA[h], d1 = dA[h] * 0.25f, d2 = dA[h] * 0.0625f, d3 = dA[h] * 0.015625f;
         lg[h][0] = (sbits & 1u) ? -INFINITY : fmaf(65536.f * d0, o.x, d0 * e.x);
         lg[h][1] = (sbits & 2u) ? -INFINITY : fmaf(65536.f * d1, o.y, d1 * e.y);
         lg[h][2] = (sbits & 4u) ? -INFINITY : fmaf(65536.f * d2, o.z, d2 * e.z);
         lg[h][3] = (sbits & 8u) ? -INFINITY : fmaf(65536.f * d3, o.w, d3 * e.w);
       }
+      }   // MMA path
       }   // per-channel K
     } else if (s.kind == 1) {
       // ================= page V half: softmax update, value accumulation
@@ -832,30 +899,24 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         l_run[h] = fmaf(l_run[h], sc, kcs == 0 ? psum : 0.f);   // lane partial
 #pragma unroll
         for (int gi = 0; gi < NG; ++gi) {
-          float wv[4], wmax = 0.f;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            wv[k] = pr[k] * vsv[gi][k];
-            wmax = fmaxf(wmax, wv[k]);
-          }
-          wmax = warp_max(wmax);
-          // 24-bit fixed point of the page's largest weight; the zero-point
-          // term uses the same rounded weights (incoherent rounding error)
-          const float invw = wmax > 0.f ? __fdividef((float)kWMax, wmax) : 0.f;
+          // W_t = rn(p_t s^V_t winv): |W| <= kQMax (p <= 1, |s^V| <= umax.V); signed
+          // 24-bit fixed point (degenerate groups may store a negative scale, R8);
+          // the zero-point term uses the same rounded weights
           uint32_t W[4];
           float zs = 0.f;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            W[k] = min(__float2uint_rn(wv[k] * invw), (uint32_t)kWMax);
-            zs = fmaf((float)W[k], vzv[gi][k], zs);
+            const int wi = __float2int_rn(pr[k] * vsv[gi][k] * winv);
+            W[k] = (uint32_t)wi + kQOff;
+            zs = fmaf((float)wi, vzv[gi][k], zs);
           }
-          dwv[h][gi] = wmax * (1.0f / (float)kWMax);
-          zl[h][gi] = fmaf(zl[h][gi], sc, kcs == 0 ? dwv[h][gi] * zs : 0.f);   // lane partial
+          dwv[h][gi] = dwu;
+          zl[h][gi] = fmaf(zl[h][gi], sc, kcs == 0 ? dwu * zs : 0.f);   // lane partial
           if (kcs == 0) {
             uint32_t *wl = wlimb + (gi * kLimbCols * NH + kLimbCols * h) * TQ + ktq;
-            wl[0] = prmt(prmt(W[0], W[1], 0x0040), prmt(W[2], W[3], 0x0040), 0x5410);
-            wl[TQ] = prmt(prmt(W[0], W[1], 0x0051), prmt(W[2], W[3], 0x0051), 0x5410);
-            wl[2 * TQ] = prmt(prmt(W[0], W[1], 0x0062), prmt(W[2], W[3], 0x0062), 0x5410);
+            wl[0] = prmt(prmt(W[0], W[1], 0x0040), prmt(W[2], W[3], 0x0040), 0x5410) ^ 0x80808080u;
+            wl[TQ] = prmt(prmt(W[0], W[1], 0x0051), prmt(W[2], W[3], 0x0051), 0x5410) ^ 0x80808080u;
+            wl[2 * TQ] = prmt(prmt(W[0], W[1], 0x0062), prmt(W[2], W[3], 0x0062), 0x5410) ^ 0x80808080u;
           }
         }
       }
@@ -867,7 +928,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       constexpr int TC = G / 32;
       const uint32_t *vcw = reinterpret_cast<const uint32_t *>(vc4);
       const float wBv = rodd ? 0.f : 256.f;
-      float *lvw = lgs + (rodd ? NH : 0) * D + min(rhead, NH - 1) * D;
+      float *lvw = lgs + ((rodd ? NH + 1 : 0) + min(rhead, NH)) * S::LP;
       AKVQ_UNROLL(AKVQ_VU)
       for (int cb = 0; cb < D / 32; ++cb) {
         const int cq = 8 * cb + mg, gi = (32 * cb) / G;
@@ -876,13 +937,12 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         for (int cc = 0; cc < TC; ++cc) {
           const uint2 b = *reinterpret_cast<const uint2 *>(wlimb + (gi * kLimbCols * NH + mcol) * TQ + 8 * cc + 2 * mt);
           const uint2 w = *reinterpret_cast<const uint2 *>(vcw + vword_idx(cq, 8 * cc + 2 * mt, CQ));
-          mma_u8u8(c01, fmask(w.x, 0), fmask(w.x, 1), fmask(w.y, 0), fmask(w.y, 1), b.x, b.y);
-          mma_u8u8(c23, fmask(w.x, 2), fmask(w.x, 3), fmask(w.y, 2), fmask(w.y, 3), b.x, b.y);
+          mma_u8s8(c01, fmask(w.x, 0), fmask(w.x, 1), fmask(w.y, 0), fmask(w.y, 1), b.x, b.y);
+          mma_u8s8(c23, fmask(w.x, 2), fmask(w.x, 3), fmask(w.y, 2), fmask(w.y, 3), b.x, b.y);
         }
         // per limb column: <= G tokens x 192 x 255 < 2^31 (exact); even lanes
         // store limb 0 + 256 limb 1, odd lanes limb 2 (x 65536 in the reader)
-        if (rhead < NH)
-          reinterpret_cast<float4 *>(lvw)[cq] =
+        reinterpret_cast<float4 *>(lvw)[cq] =
               make_float4(fmaf(wBv, (float)c01[1], (float)c01[0]), fmaf(wBv, (float)c01[3], (float)c01[2]),
                           fmaf(wBv, (float)c23[1], (float)c23[0]), fmaf(wBv, (float)c23[3], (float)c23[2]));
       }
@@ -894,8 +954,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           float dw = dwv[h][0];
 #pragma unroll
           for (int gi = 1; gi < NG; ++gi) if (gi == vgam) dw = dwv[h][gi];
-          const float4 e = reinterpret_cast<const float4 *>(lgs + h * D)[vcq];
-          const float4 o = reinterpret_cast<const float4 *>(lgs + (NH + h) * D)[vcq];
+          const float4 e = reinterpret_cast<const float4 *>(lgs + h * S::LP)[vcq];
+          const float4 o = reinterpret_cast<const float4 *>(lgs + (NH + 1 + h) * S::LP)[vcq];
           // channel 4 vcq + k carried the factor 4^k; zero term: zl, subtracted at flush
           o_rot[h][0] = fmaf(dw, fmaf(65536.f, o.x, e.x), o_rot[h][0]);
           o_rot[h][1] = fmaf(dw * 0.25f, fmaf(65536.f, o.y, e.y), o_rot[h][1]);
@@ -944,9 +1004,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         else if constexpr (tsa) rows_group(sb0, pitch, n, std::integral_constant<bool, false>());
       }
     }
-    __syncwarp();
-    if (lane == 0) produce(st);                     // refill stage st, record its descriptor
-    __syncwarp();
+    __syncwarp();                                   // every lane is done with stage st
+    if (st) { dsc1 = produce(st); bits1 = pbits; } else { dsc0 = produce(st); bits0 = pbits; }   // refill it
     if (++st == kLyStages) { st = 0; par ^= 1u; }
   }
   if constexpr (!SO)

@@ -38,6 +38,8 @@ struct LayerPlan {
   // cu, the unit's cost); CT = units * cu; warp w owns the items whose start cost
   // c satisfies floor(c W / CT) == w (64-bit products; host: CT / W >= max cost)
   int cu, CT;
+  int exact_logits;     // AKVQ_OPT_EXACT_LOGITS (test hook): fp32 page logits
+  float sc_inv;         // 1 / Sc (side-split bounds without an integer division)
   int prologue;         // 1: the preceding grid does not write this cache, so the
                         // first TMA sub-loads may be issued before griddepcontrol.wait
   uint32_t tab[kLyMaxTab];

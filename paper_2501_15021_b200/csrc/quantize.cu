@@ -142,12 +142,13 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
   __shared__ uint32_t s_bits[G / 32];
   __shared__ __align__(16) uint8_t vb8[G * D / 4];   // V S:146 bytes per token
   __shared__ int s_base;
+  __shared__ unsigned s_kmax, s_vmax;     // block max of |stored K / V scale| (float bits)
 
   const int u = blockIdx.y, j = block0 + blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5, rg = lane >> 3, cl = lane & 7;
   const uint32_t *bm = c.bitmask + (size_t)u * c.bm_words;
   if (tid < G / 32) s_bits[tid] = bm[j * (G / 32) + tid];
-  if (tid == 0) s_base = 0;
+  if (tid == 0) { s_base = 0; s_kmax = 0u; s_vmax = 0u; }
   __syncthreads();
   {  // salient entries before this block -> first side slot of the block
     int cnt = 0;
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
   int32_t *vz_g = reinterpret_cast<int32_t *>(pg + c.pg_vzero);
 
   // ---------------- rows: FWHT of K and V, V quantization, side entries
+  unsigned kmax_l = 0u, vmax_l = 0u;          // this lane's largest |stored scale| (bits)
   for (int r0 = warp * 4; r0 < G; r0 += NW * 4) {
     const int t = r0 + rg;                   // token within the block
     const int tok = j * G + t;
@@ -192,8 +194,10 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
         const int mi = t * NG + gi;                  // meta [G][NG], same bytes as [D]
         s_s[mi] = m.s; s_z[mi] = m.zf; s_mode[mi] = m.mode;
         s_rs[mi] = m.mode == 0 ? __frcp_rn(m.s) : 0.f;
-        reinterpret_cast<float *>(pg + c.pg_kscale)[mi] = sal ? 0.f : __fmul_rn(m.s, c.inv_sqrt_d);
+        const float ks = sal ? 0.f : __fmul_rn(m.s, c.inv_sqrt_d);
+        reinterpret_cast<float *>(pg + c.pg_kscale)[mi] = ks;
         reinterpret_cast<int32_t *>(pg + c.pg_kzero)[mi] = sal ? 0 : zero_i32(m.zf);
+        kmax_l = max(kmax_l, __float_as_uint(fabsf(ks)));
       }
     }
 
@@ -206,8 +210,10 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
       group_minmax<GL>(mn, mx);
       const QMeta m = q_meta(mn, mx, !sal, c.clip2, 3.f);
       if ((cl % GL) == 0) {
-        vs_g[t * NG + gi] = sal ? 0.f : __fmul_rn(m.s, c.inv_sqrt_d);
+        const float vsn = sal ? 0.f : __fmul_rn(m.s, c.inv_sqrt_d);
+        vs_g[t * NG + gi] = vsn;
         vz_g[t * NG + gi] = sal ? 0 : zero_i32(m.zf);
+        vmax_l = max(vmax_l, __float_as_uint(fabsf(vsn)));
       }
       static_assert(CPL == 8 || CPL == 16, "channels per lane");
       uint32_t w = 0;                         // the lane's CPL/4 S:146 bytes
@@ -266,6 +272,10 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
       }
     }
   }
+  {
+    const unsigned kw = __reduce_max_sync(0xffffffffu, kmax_l), vw = __reduce_max_sync(0xffffffffu, vmax_l);
+    if (lane == 0) { atomicMax(&s_kmax, kw); atomicMax(&s_vmax, vw); }
+  }
   __syncthreads();
 
   // ---------------- K: per-channel block stats over non-salient tokens (R1);
@@ -295,11 +305,17 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
       const QMeta m = q_meta(any ? mn : 0.f, any ? mx : 0.f, any, c.clip2, 3.f);
       s_s[ch] = m.s; s_z[ch] = m.zf; s_mode[ch] = m.mode;
       s_rs[ch] = m.mode == 0 ? __frcp_rn(m.s) : 0.f;
-      reinterpret_cast<float *>(pg + c.pg_kscale)[ch] = __fmul_rn(m.s, c.inv_sqrt_d);
+      const float ks = __fmul_rn(m.s, c.inv_sqrt_d);
+      reinterpret_cast<float *>(pg + c.pg_kscale)[ch] = ks;
       reinterpret_cast<int32_t *>(pg + c.pg_kzero)[ch] = zero_i32(m.zf);
+      atomicMax(&s_kmax, __float_as_uint(fabsf(ks)));
     }
   }
   __syncthreads();
+  if (tid == 0) {   // the unit's fixed-point ranges for the decode kernel (umax)
+    atomicMax(reinterpret_cast<unsigned *>(&c.umax[u].x), s_kmax);
+    atomicMax(reinterpret_cast<unsigned *>(&c.umax[u].y), s_vmax);
+  }
   // ---------------- code words in the page's 4x4 tile layout
   {
     constexpr int TQ = G / 4, CQ = D / 4;

@@ -457,3 +457,84 @@ def test_stress_fixed_point_sweep64(ak, orc, sy, stress, layer):
           "v100": dict(xf_layer=_xf_v_channel(5, 100.0)),
           "kpage": dict(xf_layer=_xf_k_page_channel(37, 8.0, 384, 512))}[stress]
     _run_case(ak, orc, sy, w, layer, steps=2, units=[0, w.U // 2, w.U - 1], **kw)
+
+
+# ----------------------------------------------------------------- fixed-point edge cases
+def _custom_case(ak, orc, K, V, cfg_kw, q, kind=1, strict64=True):
+    """Prefill custom 16-bit K, V (torch, CPU) on the GPU and in both oracle
+    modes; compare the state and the decode outputs for q."""
+    U, L0, d = K.shape
+    dt = ak.AKVQ_FP16 if K.dtype == torch.float16 else ak.AKVQ_BF16
+    od = orc.FP16 if dt == ak.AKVQ_FP16 else orc.BF16
+    G, R, top_k = cfg_kw["G"], cfg_kw["R"], cfg_kw["top_k"]
+    cap = L0 + 4
+    gcfg = ak.make_config(U, 1, d, G, R, cap, top_k, kind, dt)
+    lc = ak.LayerCache(gcfg)
+    g = torch.Generator().manual_seed(3)
+    cs = torch.rand((U, 1, L0), generator=g)
+    types = torch.zeros((U, L0), dtype=torch.uint8)
+    lc.prefill(K.cuda(), V.cuda(), types.cuda(), cs.cuda())
+    out = lc.decode(q.cuda()).double().cpu().numpy()
+    errs = []
+    for d64 in (1, 0):
+        oc = orc.OracleCache(orc.OracleConfig(U, 1, d, G, R, cap, top_k, kind, od, decide64=d64))
+        assert oc.prefill(f16_bits(K), f16_bits(V), types.numpy(), cs.numpy()) == 0
+        if d64 and not strict64:
+            # groups with a tiny clipped range next to a large offset: the fp32
+            # rounding of clip*max and clip*min (R6) moves the scale by more than
+            # 1e-6 relative; the state is checked against the fp32-decision oracle
+            try:
+                rep = compare_state(GpuState(lc), oc.export(), gcfg)
+            except AssertionError as e:
+                rep = {"code_ties": -1, "zero_ties": -1, "fp64_state": str(e)[:80]}
+        else:
+            rep = compare_state(GpuState(lc), oc.export(), gcfg)
+        errs.append((float(np.abs(out - oc.decode(f16_bits(q))).max()), rep))
+    return errs
+
+
+def test_negative_degenerate_v_groups(ak, orc):
+    """V rows v = c e_0 (c < 0) rotate to a constant negative row: every V group of
+    those tokens is degenerate with a NEGATIVE scale (R8: scale = the constant).
+    The signed 24-bit weights must carry them (an unsigned weight would drop them)."""
+    U, L0, d = 2, 300, 128
+    g = torch.Generator().manual_seed(11)
+    K = torch.randn((U, L0, d), generator=g).to(torch.bfloat16)
+    V = torch.randn((U, L0, d), generator=g)
+    V[:, ::3, :] = 0.0
+    V[:, ::3, 0] = -2.0                      # every third token: v = -2 e_0
+    V = V.to(torch.bfloat16)
+    q = torch.randn((U, 1, d), generator=g).to(torch.bfloat16)
+    for (err, rep), name in zip(_custom_case(ak, orc, K, V, dict(G=128, R=8, top_k=2), q),
+                                ("fp64", "fp32")):
+        record_margin(f"test_negative_degenerate_v_groups[{name}]", err, OUT_TOL, rep)
+        assert err <= OUT_TOL, (name, err)
+
+
+def test_large_zero_points_exact_bias(ak, orc):
+    """fp16 K rows = a fixed +-1024 pattern plus sparse one-ulp noise: every rotated
+    K channel is a large offset with a small range, so the zero points reach tens
+    of thousands and the exact page bias sum_c Q_c z_c (int64, folded into the MMA
+    accumulators) is near its largest for 16-bit inputs."""
+    U, L0, d = 2, 200, 128
+    g = torch.Generator().manual_seed(12)
+    sign = torch.where(torch.rand((1, 1, d), generator=g) < 0.5, -1.0, 1.0)
+    K = (1024.0 * sign + (torch.rand((U, L0, d), generator=g) < 0.01).float()).to(torch.float16)
+    V = torch.randn((U, L0, d), generator=g).to(torch.float16)
+    q = (torch.randn((U, 1, d), generator=g) * 0.01).to(torch.float16)
+    for (err, rep), name in zip(_custom_case(ak, orc, K, V, dict(G=32, R=8, top_k=2), q,
+                                             strict64=False), ("fp64", "fp32")):
+        record_margin(f"test_large_zero_points_exact_bias[{name}]", err, OUT_TOL,
+                      {k: v for k, v in rep.items() if isinstance(v, int)})
+        if name == "fp32":
+            assert err <= OUT_TOL, (name, err)
+
+
+@pytest.mark.parametrize("name,layer", [("tiny", 0), ("llava7b", 2), ("llava7b", 0)])
+def test_exact_logit_path(ak, orc, sy, name, layer):
+    """AKVQ_OPT_EXACT_LOGITS routes every page through the fp32 logit path that a
+    page with an out-of-range zero-point bias takes (unreachable with ordinary
+    16-bit inputs): parity as usual."""
+    w = sy.get(name)
+    units = None if name == "tiny" else [0, 17, 31]
+    _run_case(ak, orc, sy, w, layer, steps=3, units=units, options=ak.AKVQ_OPT_EXACT_LOGITS)

@@ -1,12 +1,9 @@
 #!/bin/bash
-# quick GPU iteration: parity tests, then bench variants. Usage: bash tools/gpu_quick.sh TAG [notests]
-TAG=${1:-q}; OUT=gpurun_out/$TAG; mkdir -p $OUT
-if [ "$2" != "notests" ]; then
-  timeout -k 10 900 python -m pytest tests -m gpu -x -q --timeout 300 -o timeout_method=thread > $OUT/tests.log 2>&1; echo "tests rc=$?"; tail -1 $OUT/tests.log
-fi
-i=0
-for opt in "" "--skip-rows" "--skip-pages" "--stream-only" "--skip-pages --stream-only" "--skip-rows --stream-only"; do
-  i=$((i+1))
-  timeout -k 10 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline $opt > $OUT/bench$i.json 2> $OUT/bench$i.err
-  python -c "import json,sys; j=json.loads(open('$OUT/bench$i.json').read().strip().splitlines()[-1]); print('$opt'.ljust(28), round(j['value']), round(j['ms_per_step'],3), round(j['roofline']['launch_ms']*1000,1), 'us', round(j['roofline']['frac'],3))" || tail -5 $OUT/bench$i.err
-done
+# Quick check on the box: a subset of GPU parity tests + a short bench line.
+# Usage: bash tools/gpu_quick.sh TAG [pytest -k expression] [bench args...]
+TAG=${1:-q}; K=${2:-"tiny or llava7b_layer_full or full_size_sampled or gqa_head_groups"}; shift; shift
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+timeout -k 10 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "$K" > $OUT/tests.log 2>&1; echo "tests rc=$?"; tail -2 $OUT/tests.log
+timeout -k 10 600 python bench.py --no-cpu-baseline --steps 20 "$@" > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
+python -c "import json;j=json.load(open('$OUT/bench.json'));print('tok/s %.0f  launch_us %.2f  frac %.4f' % (j['value'], 1e3*j['roofline']['launch_ms'], j['roofline']['frac']))"
