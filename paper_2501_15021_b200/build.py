@@ -20,7 +20,7 @@ OUT = os.path.join(PKG, "libakvq.so")
 BUILD = os.path.join(PKG, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["api.cu", "quantize.cu", "decode.cu", "decode_layer.cu", "pivots.cu"]
+SOURCES = ["api.cu", "quantize.cu", "decode.cu", "decode_layer.cu", "decode_gqa.cu", "pivots.cu"]
 HEADERS = ["common.cuh", "kernels.h", "decode_common.cuh"]
 
 FLAGS = [

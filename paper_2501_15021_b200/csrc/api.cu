@@ -157,6 +157,12 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
     } else {
       lp.Sc = n_q > 0 ? (n_q + 255) / 256 : 0;                              // text rows <= n_q
       if (lp.Sc > 8) lp.Sc = 8;
+      // the GQA kernel takes its rows one at a time for all heads (~ a page's work
+      // per dozen rows): many small splits keep the long text tiers balanced
+      if (layer_uses_gqa(f.q_per_kv)) {
+        lp.Sc = n_q > 0 ? (n_q + 63) / 64 : 0;
+        if (lp.Sc > 512) lp.Sc = 512;
+      }
     }
     if (c->options & AKVQ_OPT_SKIP_ROWS) lp.Rc = lp.Sc = 0;       // profiling hooks
     if (c->options & AKVQ_OPT_SKIP_PAGES) lp.P = 0;
@@ -192,7 +198,8 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
 #ifndef AKVQ_CROWS
 #define AKVQ_CROWS 2
 #endif
-    const int c_page = AKVQ_CPAGE, c_rows = AKVQ_CROWS, c_side = f.kind == AKVQ_TSA ? 6 : 2;
+    const int c_page = AKVQ_CPAGE, c_rows = AKVQ_CROWS,
+              c_side = f.kind == AKVQ_TSA ? (layer_uses_gqa(f.q_per_kv) ? 3 : 6) : 2;
     lp.cu = lp.P * c_page + lp.Rc * c_rows + lp.Sc * c_side;   // <= 2048 * 7 < 2^16
     if (build_tab && lp.per_u <= kLyMaxTab) {
       int acc = 0;
@@ -207,8 +214,10 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
     if (p.fast && lp.per_u > 0) {
       const long long T = (long long)f.n_units * lp.hg * lp.per_u;
       const long long CT = (long long)f.n_units * lp.hg * lp.cu;
-      const int ctas = pg_ctas_override() > 0 ? pg_ctas_override() : layer_ctas_per_sm(layer_group_heads(f.q_per_kv));
-      const long long wmax = (long long)sms * ctas * layer_warps_per_cta();
+      const bool gq = layer_uses_gqa(f.q_per_kv);
+      const int ctas = pg_ctas_override() > 0 ? pg_ctas_override()
+                       : (gq ? gqa_ctas_per_sm() : layer_ctas_per_sm(layer_group_heads(f.q_per_kv)));
+      const long long wmax = (long long)sms * ctas * (gq ? gqa_warps_per_cta() : layer_warps_per_cta());
       if (CT >= (1LL << 31) || T >= (1LL << 31)) {   // beyond the plan's 32-bit counters
         p.fast = 0;
         lp.per_u = 1;
@@ -241,9 +250,10 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
 
 size_t ws_bytes_for(const akvq_cache *c, const DecodePlan &p) {
   const size_t g = c->cfg.q_per_kv, d = c->cfg.head_dim;
-  if (p.fast) {   // NH heads per record: g for g <= 2, 4 for head groups
+  if (p.fast) {   // NH heads per record: [o_org][o_rot][m][l] (g <= 2) or [o_rot][m][l] (GQA)
     const size_t nh = (size_t)layer_group_heads((int)g);
-    return (size_t)p.lp.W * p.lp.maxseg * nh * (2 * d + 4) * sizeof(float);
+    const size_t rec = layer_uses_gqa((int)g) ? gqa_record_floats((int)d) : 2 * d + 4;
+    return (size_t)p.lp.W * p.lp.maxseg * nh * rec * sizeof(float);
   }
   return (size_t)c->cfg.n_units * p.S * g * (d + 2) * sizeof(float);
 }
@@ -258,8 +268,10 @@ akvq_status launch_fast(const akvq_cache *c, DecodePlan &p, const void *q, const
   // prologue prefetch: only if the preceding kernel of this stream does not
   // write this cache (the new row of a fused step is patched in after the wait)
   p.lp.prologue = prefetch_safe(c, s) && !(c->options & AKVQ_OPT_STREAM_ONLY) ? 1 : 0;
-  const cudaError_t e = launch_decode_layer(d, c->cfg.dtype16, p.lp, q, k, v, types,
-                                            static_cast<float *>(ws), out, flags, s);
+  const cudaError_t e =
+      layer_uses_gqa(c->cfg.q_per_kv)
+          ? launch_decode_gqa(d, c->cfg.dtype16, p.lp, q, k, v, types, static_cast<float *>(ws), out, flags, s)
+          : launch_decode_layer(d, c->cfg.dtype16, p.lp, q, k, v, types, static_cast<float *>(ws), out, flags, s);
   // the fused step appends (writes the ring); a plain decode writes only its
   // self-resetting tickets, which no prologue reads
   note_launch(const_cast<akvq_cache *>(c), s, k != nullptr);

@@ -43,32 +43,6 @@
 namespace akvq {
 
 constexpr int kLyWarps = 4;        // warps per CTA
-#ifndef AKVQ_LY_STAGES
-#define AKVQ_LY_STAGES 2
-#endif
-constexpr int kLyStages = AKVQ_LY_STAGES;   // TMA stages per warp
-constexpr int kRows = 8;           // 16-bit rows per ring chunk / side sub-load
-constexpr int kRows4 = 32;         // 4-bit TSA rows per side sub-load
-// unroll factors of the page MMA loops (K: token blocks, V: channel blocks)
-#ifndef AKVQ_KU
-#define AKVQ_KU 4
-#endif
-#ifndef AKVQ_VU
-#define AKVQ_VU 4
-#endif
-#define AKVQ_PRAGMA(x) _Pragma(#x)
-#define AKVQ_UNROLL(n) AKVQ_PRAGMA(unroll n)
-// Page fixed points: signed 24-bit integers as three int8 limbs,
-// relative to per-unit ranges (umax: the largest |K| / |V| scale of the unit's
-// pages, maintained by the quantizer).
-//  K: Q_c = rn(q~_c s^K_c kQMax / (max|q~| umax.K)), |Q| <= kQMax;
-//  V: W_t = rn(p_t s^V_t kQMax / umax.V), |W| <= kQMax (p <= 1).
-// X + kQOff lies in [0, 2^24); limb k = byte k of X + kQOff minus 128 (signed
-// int8: byte ^ 0x80).  kQMax < 127 * 65793 leaves room for the few-ulp error of
-// __fdividef and the products.  Each head owns 4 MMA B columns: limbs 0, 1, 2
-// and one unused column.
-constexpr int kQMax = 8355700;
-constexpr uint32_t kQOff = 0x808080u;
 constexpr int kLimbCols = 4;
 #ifndef AKVQ_LY_CTAS
 #define AKVQ_LY_CTAS 4
@@ -100,134 +74,6 @@ struct LySmem {
     return (bar_off(sb) + kLyStages * 8 + 127) / 128 * 128;
   }
 };
-
-// stage bytes: max(page K half, page V half, kRows 16-bit rows, kRows4 side4 rows)
-__host__ __device__ inline size_t ly_stage_bytes(const DevCache &c) {
-  size_t a = c.pg_vscale, b = c.page_bytes - c.pg_vscale;
-  size_t m = a > b ? a : b;
-  const size_t r16 = (size_t)kRows * 4 * c.d;
-  if (r16 > m) m = r16;
-  if (c.kind == AKVQ_TSA) {
-    const size_t r4 = (size_t)kRows4 * c.side_entry;
-    if (r4 > m) m = r4;
-  }
-  return (m + 127) / 128 * 128;
-}
-
-// 2^x with the SFU's approximate ex2 (rel. error ~2^-22, flushes subnormal
-// results to 0): softmax weights below 2^-126 of the running max are 0 anyway.
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-__device__ __forceinline__ uint32_t fmask(uint32_t w, int s) { return w & (0x03030303u << (2 * s)); }
-
-// Legacy warp MMA m16n8k32 (IMMA, int32 accumulate): A 16x32 u8 row-major, B
-// 32x8 s8 / u8 column-major.  Fragments (lane = 4 * grp + tig): a0 / a1 hold
-// rows grp / grp + 8, columns 4 tig .. 4 tig + 3; a2 / a3 the same rows,
-// columns 16 + 4 tig ..; b0 / b1 rows 4 tig .. / 16 + 4 tig .. of column grp;
-// c0, c1 row grp, columns 2 tig, 2 tig + 1; c2, c3 row grp + 8.
-__device__ __forceinline__ void mma_u8s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
-  asm(
-      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-template <int DT>
-__device__ __forceinline__ void cvt2(uint32_t w, float &a, float &b) {
-  if constexpr (DT == AKVQ_BF16) {
-    a = __uint_as_float(w << 16);
-    b = __uint_as_float(w & 0xffff0000u);
-  } else {
-    const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w));
-    a = f.x;
-    b = f.y;
-  }
-}
-
-// Sum v[NV] over the CQ lanes of a row group (lane bits below CQ): a reduce-
-// scatter halves the values per step, then a butterfly finishes.  On return
-// `mine` is the slot whose total this lane holds.
-template <int NV, int CQ>
-__device__ __forceinline__ float rs_reduce(float (&v)[NV], int cq, int &mine) {
-  constexpr int L2 = NV == 8 ? 3 : (NV == 4 ? 2 : (NV == 2 ? 1 : 0));
-  static_assert((1 << L2) == NV && (CQ >> L2) >= 1, "reduce shape");
-  mine = 0;
-#pragma unroll
-  for (int step = 0; step < L2; ++step) {
-    const int n = NV >> step, off = CQ >> (step + 1);
-    const bool up = cq & off;
-#pragma unroll
-    for (int i = 0; i < n / 2; ++i) {
-      const float send = up ? v[i] : v[i + n / 2];
-      const float keep = up ? v[i + n / 2] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-    if (up) mine += n / 2;
-  }
-  float t = v[0];
-#pragma unroll
-  for (int off = CQ >> (L2 + 1); off >= 1; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-  return t;
-}
-
-// One sub-load of the pipeline: an item split into stage-sized pieces.  The
-// producer lane records it in the warp's descriptor ring (one per stage).
-struct LySub {
-  int u, kind;   // u: (virtual) unit; kind: 0 page K half, 1 page V half, 2 16-bit rows, 3 4-bit rows, -1 none
-  int pu;        // physical unit (u / head groups), producer side only
-  int a, n;      // page index | first row (ring offset from n_q / side entry) and row count
-  int ring;      // 1 if ring rows
-};
-// descriptor as it travels from the producer lane to the warp: two words
-//   x = u, y = (kind + 1) | ring << 3 | n << 4 (n < 64) | a << 10
-__device__ __forceinline__ uint2 pack_sub(const LySub &s) {
-  return make_uint2((uint32_t)s.u, (uint32_t)(s.kind + 1) | ((uint32_t)s.ring << 3) |
-                                       ((uint32_t)s.n << 4) | ((uint32_t)s.a << 10));
-}
-__device__ __forceinline__ LySub unpack_sub(uint2 w) {
-  LySub s;
-  s.u = (int)w.x;
-  s.kind = (int)(w.y & 7u) - 1;
-  s.ring = (int)((w.y >> 3) & 1u);
-  s.n = (int)((w.y >> 4) & 63u);
-  s.a = (int)(w.y >> 10);
-  return s;
-}
-
-__device__ __forceinline__ uint2 lds64(uint32_t a) {
-  uint2 v;
-  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint32_t lds16(uint32_t a) {
-  unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ float lds_f32(uint32_t a) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ int lds_s32(uint32_t a) {
-  int v;
-  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-
-// lane bits that encode slot m of rs_reduce<NV, CQ> (see there)
-template <int NV, int CQ>
-__device__ __forceinline__ constexpr int rs_enc(int m) {
-  constexpr int L2 = NV == 8 ? 3 : (NV == 4 ? 2 : (NV == 2 ? 1 : 0));
-  int e = 0;
-  for (int j = 0; j < L2; ++j)
-    if ((m >> (L2 - 1 - j)) & 1) e |= CQ >> (j + 1);
-  return e;
-}
 
 template <int D, int G, int DT, int NH, bool TSA, int KM>
 __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
@@ -1052,17 +898,14 @@ static cudaError_t launch_ly(const DevCache &c, const LayerPlan &lp, const void 
 int layer_supported(int d, int G, int g) {
   return (d == 128 || d == 64) && G >= 32 && G <= d && g >= 1 && g <= 16;
 }
-// heads per group: g itself for g <= 2, else AKVQ_GQA_NH (2, measured best for the
-// Qwen g = 7 config: 245 vs 272 us per layer; 4: fewer cache passes,
-// 2 CTAs/SM; 2: more passes, 3 CTAs/SM)
-#ifndef AKVQ_GQA_NH
-#define AKVQ_GQA_NH 2
-#endif
-static_assert(AKVQ_GQA_NH == 2, "head groups of 2 (4 limb columns per head, one MMA n-tile)");
-int layer_group_heads(int g) { return g <= 2 ? g : AKVQ_GQA_NH; }
+// query heads per pass over a unit's cache: g itself for g <= 2 (k_decode_layer),
+// else the single-pass GQA kernel's group of 4 or 8 (k_decode_gqa; g > 8 runs
+// ceil(g / 8) groups)
+int layer_uses_gqa(int g) { return g >= 3; }
+int layer_group_heads(int g) { return g <= 2 ? g : gqa_heads(g); }
 int layer_head_groups(int g) { return (g + layer_group_heads(g) - 1) / layer_group_heads(g); }
 int layer_warps_per_cta() { return kLyWarps; }
-int layer_ctas_per_sm(int g) { return ly_ctas_per_sm(g); }
+int layer_ctas_per_sm(int nh) { return ly_ctas_per_sm(nh); }
 int layer_rows_per_chunk() { return kRows; }
 int layer_rows4_per_sub() { return kRows4; }
 

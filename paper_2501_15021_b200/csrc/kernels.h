@@ -71,6 +71,14 @@ cudaError_t launch_decode(const DevCache &c, int dtype16, const DecodePlan &p, c
 cudaError_t launch_decode_layer(const DevCache &c, int dtype16, const LayerPlan &lp, const void *q,
                                 const void *k, const void *v, const uint8_t *types, float *part,
                                 float *out, uint32_t flags, cudaStream_t st);
+cudaError_t launch_decode_gqa(const DevCache &c, int dtype16, const LayerPlan &lp, const void *q,
+                              const void *k, const void *v, const uint8_t *types, float *part,
+                              float *out, uint32_t flags, cudaStream_t st);
+int gqa_heads(int g);
+int gqa_warps_per_cta();
+int gqa_ctas_per_sm();
+size_t gqa_record_floats(int d);
+int layer_uses_gqa(int g);
 int layer_supported(int d, int G, int g);
 int layer_head_groups(int g);
 int layer_group_heads(int g);
