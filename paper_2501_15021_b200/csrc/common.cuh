@@ -170,6 +170,7 @@ __device__ __forceinline__ uint32_t q_code_fast(float x, const QMeta &m, float r
 
 __device__ __forceinline__ int32_t zero_i32(float zf) { return __float2int_rz(zf); }
 
+
 // N codes of one group (same meta) packed at 2 * i bits, i < N: branch-free
 // except once per group.  Equal, bit for bit, to q_code on each element: the
 // product x * rs lies within 2 ulp of the IEEE quotient x / s, so both round to

@@ -179,10 +179,14 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
     for (int i = 0; i < CPL / 8; ++i) { cvt8<DT>(kraw[i], k + 8 * i); cvt8<DT>(vraw[i], v + 8 * i); }
     fwht_lanes8<CPL>(k, cl);
     fwht_lanes8<CPL>(v, cl);
+    // staged K rows; a salient row is staged as NaN, which fminf / fmaxf skip in
+    // the per-channel statistics (its codes are masked to 0 when packed)
+    const float kst = sal && !KT ? __int_as_float(0x7fc00000) : 0.f;
 #pragma unroll
     for (int i = 0; i < CPL / 4; ++i)
       *reinterpret_cast<float4 *>(xs + t * P + xs_col(cl * CPL + 4 * i)) =
-          make_float4(k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]);
+          sal && !KT ? make_float4(kst, kst, kst, kst)
+                     : make_float4(k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]);
     if constexpr (KT) {                   // K per token over G-channel groups (NEXT-1)
       const int gi = (cl * CPL) / G;
       float mn = k[0], mx = k[0];
@@ -224,7 +228,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
     }
     // TSA 4-bit side stats (group reductions need every lane: computed for all rows)
     QMeta mk4, mv4;
-    if (tsa) {
+    if (tsa && __any_sync(0xffffffffu, sal)) {
       float mnk = k[0], mxk = k[0], mnv = v[0], mxv = v[0];
 #pragma unroll
       for (int i = 1; i < CPL; ++i) {
@@ -288,8 +292,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
     const int ch = tid % D, part = tid / D;
     float mn = INFINITY, mx = -INFINITY;
     for (int i = part * (G / NS); i < (part + 1) * (G / NS); ++i) {
-      if ((s_bits[i >> 5] >> (i & 31)) & 1u) continue;
-      const float x = xs[i * P + xs_col(ch)];
+      const float x = xs[i * P + xs_col(ch)];     // NaN for salient rows: skipped
       mn = fminf(mn, x);
       mx = fmaxf(mx, x);
     }
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
         const int ch = 4 * cq + b;
         const float xv[4] = {xq[0][b], xq[1][b], xq[2][b], xq[3][b]};
         uint32_t c4;
-        if constexpr (!KT) {                         // one channel's meta for the 4 tokens
+        if constexpr (!KT) {                         // one channel's thresholds for the 4 tokens
           QMeta m; m.s = s_s[ch]; m.zf = s_z[ch]; m.mode = s_mode[ch];
           c4 = q_codes2<4>(xv, m, s_rs[ch]);
         } else {                                     // per-token meta
