@@ -191,6 +191,19 @@ def oracle_baseline(w, seconds=10.0, max_steps=250):
             "sample": smp.describe()}
 
 
+def workload_config(args, w, w1, world, n_layers):
+    """The `config` object of both arms' JSON lines (the workload, no model keys)."""
+    return {"workload": w1.name, "source": "BJ:9 batch sweep at LLaVA-1.5-7B shape"
+            if w1.name.startswith("sweep") else f"synth.{w1.name}",
+            "layers": n_layers, "global_batch": w.batch,
+            "per_gpu_batch": w.batch // world if args.scaling == "weak" else None,
+            "heads": w.hq, "kv_heads": w.hkv, "head_dim": w.d, "prompt_tokens": w.L0,
+            "group": w.G, "residual": w.R, "top_k": w.top_k,
+            "tsa_layers": list(w.tsa_layers), "kv_bits": 2,
+            "k_axis": "per-" + args.k_axis, "pivots": args.pivots,
+            "parallelism": f"units (batch x kv-head) sharded over {world} GPU(s)"}
+
+
 def run_reference(args, w, rank):
     """--impl reference: the oracle as the reference arm, rank 0 only."""
     if rank != 0:
@@ -207,15 +220,55 @@ def run_reference(args, w, rank):
             "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
             "ms_per_step": 1000.0 * w.batch / val, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name},
+            "config": dict(workload_config(args, w, w, max(1, args.gpus), w.n_layers),
+                           l2="n/a (CPU oracle)"),
+            "extrapolated": True,
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": smp.cores,
-                             "kind": "oracle", "sample": smp.describe()},
+                             "kind": "oracle", "sample": smp.describe(), "extrapolated": True},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------- GPU leg
+def emulate_rank_shape(ak, synth, wr, n_layers, dt, args, dev, steps=10, warmup=3):
+    """Decode-step time of one rank's share of a strong-scaled batch, on this GPU:
+    prefill every layer for the smaller batch, then time `steps` fused steps."""
+    cap = wr.L0 + warmup + steps + 2
+    caches = []
+    for layer in range(n_layers):
+        cfg = ak.make_config(wr.U, wr.g, wr.d, wr.G, wr.R, cap, wr.top_k, wr.kind(layer), dt,
+                             wr.clip2, wr.clip4, 1 if args.k_axis == "token" else 0)
+        lc = ak.LayerCache(cfg, device=dev)
+        inp = synth.layer_inputs(wr, layer, device=dev)
+        lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
+        del inp
+        caches.append(lc)
+    ins = []
+    for s in range(warmup + steps):
+        per = [synth.decode_inputs(wr, layer, s, device=dev) for layer in range(n_layers)]
+        ins.append(per)
+    outs = [torch.empty((wr.U, wr.g, wr.d), dtype=torch.float32, device=dev) for _ in range(n_layers)]
+    for s in range(warmup):
+        for layer, lc in enumerate(caches):
+            di = ins[s][layer]
+            lc.step(di["k"], di["v"], di["q"], di["types"], out=outs[layer])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for s in range(warmup, warmup + steps):
+        for layer, lc in enumerate(caches):
+            di = ins[s][layer]
+            lc.step(di["k"], di["v"], di["q"], di["types"], out=outs[layer])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del caches
+    torch.cuda.empty_cache()
+    return {"workload": wr.name, "ms_per_step": ms, "tokens_per_s": wr.batch / (ms * 1e-3),
+            "ms_per_layer": ms / n_layers}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -234,6 +287,8 @@ def main():
     ap.add_argument("--k-axis", default="channel", choices=["channel", "token"],
                     help="K quantization axis: per channel (R1, graded) or per token (P:246)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-strong-emulation", action="store_true",
+                    help="skip the 1-GPU emulation of the strong-scaling per-rank shapes")
     ap.add_argument("--stream-only", action="store_true",
                     help="profiling: kernels stream their bytes but skip the math (invalid outputs)")
     ap.add_argument("--skip-rows", action="store_true", help="profiling: no row kernel (invalid)")
@@ -268,7 +323,9 @@ def main():
     units = list(range(lo, hi))
     dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
     need_steps = args.warmup + 2 * args.steps
-    cap = w.L0 + max(w.decode_steps, need_steps)
+    nq0 = (w.L0 - w.R) // w.G * w.G if w.L0 > w.R else 0
+    first_flush = w.R + nq0 + w.G - w.L0              # decode steps until the first flush
+    cap = w.L0 + max(w.decode_steps, need_steps, first_flush + 2)
     stream = torch.cuda.current_stream()
 
     # ---------------- prefill every layer (timed separately)
@@ -423,13 +480,16 @@ def main():
             bytes_layers.append(Ul * decode_bytes_per_unit(w, kind, L, nq, side))
     dec_bytes = sum(bytes_layers) / len(bytes_layers)
     peaks = _peaks()
-    traffic = None          # dram bytes of one launch from a committed ncu --set full capture
+    traffic, traffic_commit = None, None   # dram bytes of one launch, committed ncu capture
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         with open(tf) as fh:
             tj = json.load(fh).get("k_decode_layer", {})
-        if tj.get("workload") == w.name and world == 1 and args.k_axis == "channel":
-            traffic = tj.get("traffic_bytes")
+        # only for the exact configuration the capture was taken on
+        if (tj.get("workload") == w.name and world == 1 and args.k_axis == "channel"
+                and args.pivots == "colsum" and not (args.stream_only or args.skip_rows
+                                                     or args.skip_pages)):
+            traffic, traffic_commit = tj.get("traffic_bytes"), tj.get("commit")
     achieved = dec_bytes / (dec_ms * 1e-3) / 1e9
     tokens_per_s = w.batch / (ms * 1e-3)
 
@@ -509,9 +569,58 @@ def main():
         e2e_ms = float(t[0])
         dist.barrier()
 
+    # ---------------- flush cost: a step that quantizes a G-block (every G steps)
+    # is timed on its own (the timed region above may hold none) and amortized
+    def sync_inputs(step):
+        q, k, v, ty = step_inputs(step, dev)
+        return q, k, v, ty
+
+    flush = None
+    st = args.warmup + 2 * args.steps
+    while caches[0].L - w.R - caches[0].n_q < w.G - 1 and caches[0].L < cap - 1:
+        one_step(*sync_inputs(st)); st += 1             # plain steps up to the boundary
+    drain()
+    if caches[0].L - w.R - caches[0].n_q == w.G - 1 and caches[0].L < cap:
+        fin = sync_inputs(st)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        l0 = launches[0]
+        one_step(*fin)
+        drain()
+        f1.record()
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1)
+        if dist:
+            t = torch.tensor([fms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            fms = float(t[0])
+        amort = ((w.G - 1) * ms + fms) / w.G
+        flush = {"ms_flush_step": fms, "ms_plain_step": ms, "flush_every_steps": w.G,
+                 "launches_flush_step": launches[0] - l0,
+                 "amortized_ms_per_step": amort, "amortized_tokens_per_s": w.batch / (amort * 1e-3)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_baseline(w)
+
+    # ---------------- 1-GPU emulation of the per-rank shapes of strong scaling
+    # (the BJ:9 global batch split over 2 / 4 / 8 GPUs = batch 32 / 16 / 8 per rank)
+    emul = None
+    if world == 1 and w1.name.startswith("sweep@b") and not args.no_strong_emulation:
+        del caches
+        inputs.clear()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        emul = {}
+        for nshard in (2, 4, 8):
+            if w1.batch % nshard:
+                continue
+            emul[f"n{nshard}"] = emulate_rank_shape(ak, synth, w1.with_batch(w1.batch // nshard),
+                                                    n_layers, dt, args, dev)
+            emul[f"n{nshard}"]["projected_speedup_vs_1"] = ms / emul[f"n{nshard}"]["ms_per_step"]
 
     if rank == 0:
         line = {
@@ -519,30 +628,31 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "u8-imma+f32", "data": "synthetic",
-            "config": {"workload": w1.name, "source": "BJ:9 batch sweep at LLaVA-1.5-7B shape",
-                       "layers": n_layers, "global_batch": w.batch,
-                       "per_gpu_batch": w.batch // world if args.scaling == "weak" else None,
-                       "heads": w.hq,
-                       "kv_heads": w.hkv, "head_dim": w.d, "prompt_tokens": w.L0,
-                       "group": w.G, "residual": w.R, "top_k": w.top_k,
-                       "tsa_layers": list(w.tsa_layers), "kv_bits": 2,
-                       "k_axis": "per-" + args.k_axis, "pivots": args.pivots,
-                       "parallelism": f"units (batch x kv-head) sharded over {world} GPU(s)",
-                       "l2": "no flush: per-step working set "
-                             f"{sum(bytes_layers[:n_layers]) / 1e9:.2f} GB/rank >> 126 MB L2"},
+            "config": dict(workload_config(args, w, w1, world, n_layers),
+                           l2="no flush: per-step working set "
+                              f"{sum(bytes_layers[:n_layers]) / 1e9:.2f} GB/rank >> 126 MB L2"),
             "attention_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                         "traffic": traffic, "kernel": "k_decode_layer (append + all tiers + merge, one launch per layer)",
+                         "frac_nominal": achieved / 8000.0, "peak_nominal": 8000.0,
+                         "traffic": traffic, "traffic_commit": traffic_commit,
+                         "kernel": "k_decode_layer (append + all tiers + merge, one launch per layer)",
                          "bytes_per_launch": dec_bytes, "launch_ms": dec_ms,
                          "peak_src": peaks["src"]},
             "prefill": {"ms_all_layers": pre_ms, "quantize_gbs": pre_bytes / (pre_ms * 1e-3) / 1e9,
                         "frac": pre_bytes / (pre_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
             "e2e": {"value": w.batch / (e2e_ms * 1e-3), "unit": "tokens/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                    "note": "pinned host inputs of step s+1 are copied while step s computes "
+                            "(legitimate here: synthetic queries do not depend on outputs); "
+                            "outputs of every step copied back"},
             "gpu_launches": n_launch,
             "clocks": clocks,
         }
+        if flush:
+            line["flush"] = flush
+        if emul:
+            line["strong_scaling_emulation"] = emul
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
