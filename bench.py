@@ -233,13 +233,16 @@ def run_reference(args, w, rank):
 # ----------------------------------------------------------------- GPU leg
 def emulate_rank_shape(ak, synth, wr, n_layers, dt, args, dev, steps=10, warmup=3):
     """Decode-step time of one rank's share of a strong-scaled batch, on this GPU:
-    prefill every layer for the smaller batch, then time `steps` fused steps."""
-    cap = wr.L0 + warmup + steps + 2
+    prefill every layer for the smaller batch, then time `steps` fused steps
+    issued through the C ABI, and `steps` replays of the same step captured once
+    in a CUDA graph (AKVQ_OPT_DEVICE_L caches, inputs copied into the captured
+    buffers outside the timed replays)."""
+    cap = wr.L0 + warmup + 2 * steps + 4
     caches = []
     for layer in range(n_layers):
         cfg = ak.make_config(wr.U, wr.g, wr.d, wr.G, wr.R, cap, wr.top_k, wr.kind(layer), dt,
                              wr.clip2, wr.clip4, 1 if args.k_axis == "token" else 0)
-        lc = ak.LayerCache(cfg, device=dev)
+        lc = ak.LayerCache(cfg, device=dev, options=ak.AKVQ_OPT_DEVICE_L)
         inp = synth.layer_inputs(wr, layer, device=dev)
         lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
         del inp
@@ -263,10 +266,34 @@ def emulate_rank_shape(ak, synth, wr, n_layers, dt, args, dev, steps=10, warmup=
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    # one step captured in a CUDA graph, replayed (no block flush inside the window)
+    gms = None
+    if all(lc.L - wr.R - lc.n_q + steps + 1 < wr.G for lc in caches):
+        bufs = [{k_: v_.clone() for k_, v_ in ins[warmup][layer].items()} for layer in range(n_layers)]
+        s_ = torch.cuda.Stream(device=dev)
+        s_.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s_):
+            with torch.cuda.graph(graph, stream=s_):
+                for layer, lc in enumerate(caches):
+                    b_ = bufs[layer]
+                    lc.step(b_["k"], b_["v"], b_["q"], b_["types"], out=outs[layer])
+        torch.cuda.current_stream().wait_stream(s_)
+        graph.replay()                                     # warm replay
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(steps):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        gms = e0.elapsed_time(e1) / steps
+        for lc in caches:                                  # host mirrors: capture counted 1
+            ak.akvq_cache_advance(lc.handle, steps)
     del caches
     torch.cuda.empty_cache()
     return {"workload": wr.name, "ms_per_step": ms, "tokens_per_s": wr.batch / (ms * 1e-3),
-            "ms_per_layer": ms / n_layers}
+            "ms_per_layer": ms / n_layers, "graph_ms_per_step": gms,
+            "graph_tokens_per_s": wr.batch / (gms * 1e-3) if gms else None}
 
 
 def main():

@@ -116,6 +116,9 @@ typedef struct {
  *  ticket  [U * hg] u32                merge tickets of the fused decode, one
  *                                      per unit and GQA head group hg (zeroed
  *                                      at init, self-resetting)
+ *  state   i32 L, u32 counter          device copy of the token count L (kept by
+ *                                      prefill, append and the fused decode) and
+ *                                      the fused decode's launch-exit counter
  *  umax    [U] f32 x 2                 largest |K scale| and |V scale| of the
  *                                      unit's quantized pages (normalized
  *                                      basis; zeroed at init, raised by every
@@ -133,6 +136,7 @@ typedef struct {
   uint64_t side_off, side_entry_bytes;
   uint64_t ticket_off;
   uint64_t umax_off;
+  uint64_t state_off;
   int32_t cap, n_pages, slots, bitmask_words, side_cap, ng;
 } akvq_layout;
 
@@ -172,6 +176,14 @@ typedef struct {
  * (the one a page with an out-of-range zero-point bias takes) instead of the
  * fixed-point MMA; results must match the oracle the same way. */
 #define AKVQ_OPT_EXACT_LOGITS 16
+/* Device-resident token count: the fused decode kernel takes L from the cache
+ * buffer (state region) and advances it itself, and the item table covers every
+ * L of the current flush period.  The launches of akvq_decode_step then have
+ * the same parameters from one step to the next until the next block flush,
+ * so a step can be captured in a CUDA graph and replayed (the host mirror is
+ * brought up to date with akvq_cache_advance).  Needs the fast kernels (any
+ * supported d, G, q_per_kv); the generic split kernels return EUNSUPPORTED. */
+#define AKVQ_OPT_DEVICE_L 32
 
 typedef struct {      /* memory_report, host arithmetic           */
   double bytes_fp16, bytes_int4, bytes_int2, bytes_overhead;
@@ -280,6 +292,13 @@ akvq_status akvq_rotate_quantize_pivots(akvq_cache *c, const void *K, const void
                                         const int32_t *pivots, const int32_t *counts,
                                         int32_t n_max, int32_t units_per_row,
                                         akvq_stream_t stream);
+
+/* Host bookkeeping after CUDA-graph replays of akvq_decode_step under
+ * AKVQ_OPT_DEVICE_L: L += steps (the device copy was advanced by the replayed
+ * kernels).  Host arithmetic only.  Errors: EINVAL (steps < 0), ECAPACITY,
+ * ESTATE (the steps would have crossed a block flush, which a replay does not
+ * perform). */
+akvq_status akvq_cache_advance(akvq_cache *c, int32_t steps);
 
 /* dequantized_view: K^, V^ device f32 [U][L][d] in the rotated
  * normalized basis (R5).  Test hook.  Errors: ESTATE (L == 0). */

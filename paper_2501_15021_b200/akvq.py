@@ -25,6 +25,7 @@ AKVQ_OPT_STREAM_ONLY = 2
 AKVQ_OPT_SKIP_ROWS = 4
 AKVQ_OPT_SKIP_PAGES = 8
 AKVQ_OPT_EXACT_LOGITS = 16
+AKVQ_OPT_DEVICE_L = 32
 AKVQ_MAX_PSA_PROMPT = 49152
 
 # every symbol include/akvq.h declares
@@ -33,7 +34,7 @@ EXPORTS = (
     "akvq_append_token", "akvq_decode_workspace_bytes", "akvq_decode_workspace_bytes_max",
     "akvq_decode_attention", "akvq_select_salient", "akvq_dequantize_view",
     "akvq_memory_report", "akvq_status_str", "akvq_version", "akvq_decode_step",
-    "akvq_detect_pivots", "akvq_rotate_quantize_pivots",
+    "akvq_detect_pivots", "akvq_rotate_quantize_pivots", "akvq_cache_advance",
 )
 
 
@@ -54,7 +55,8 @@ class akvq_layout(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "total_bytes", "pages_off", "page_bytes", "pg_kscale", "pg_kzero", "pg_kcodes",
         "pg_vscale", "pg_vzero", "pg_vcodes", "ring_off", "ring_unit_bytes", "bitmask_off",
-        "side_idx_off", "side_cnt_off", "side_off", "side_entry_bytes", "ticket_off", "umax_off")] + [
+        "side_idx_off", "side_cnt_off", "side_off", "side_entry_bytes", "ticket_off", "umax_off",
+        "state_off")] + [
         (n, C.c_int32) for n in ("cap", "n_pages", "slots", "bitmask_words", "side_cap", "ng")]
 
 
@@ -118,6 +120,8 @@ def lib() -> C.CDLL:
         L.akvq_rotate_quantize_pivots.argtypes = [C.POINTER(akvq_cache), P, P, C.c_int32, P, P,
                                                   C.c_int32, C.c_int32, P]
         L.akvq_rotate_quantize_pivots.restype = S
+        L.akvq_cache_advance.argtypes = [C.POINTER(akvq_cache), C.c_int32]
+        L.akvq_cache_advance.restype = S
         L.akvq_status_str.argtypes = [S]
         L.akvq_status_str.restype = C.c_char_p
         L.akvq_version.argtypes = []
@@ -229,6 +233,10 @@ def akvq_rotate_quantize_pivots(cache, K, V, L0, pivots, counts, units_per_row, 
                                              _ptr(pivots), _ptr(counts), int(pivots.shape[1]),
                                              int(units_per_row), _stream(stream)),
            "akvq_rotate_quantize_pivots")
+
+
+def akvq_cache_advance(cache, steps: int):
+    _check(lib().akvq_cache_advance(C.byref(cache), int(steps)), "akvq_cache_advance")
 
 
 def akvq_dequantize_view(cache, K, V, stream=None):

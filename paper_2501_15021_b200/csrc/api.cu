@@ -48,6 +48,7 @@ DevCache make_dev(const akvq_cache *c) {
   d.side = b + y.side_off;
   d.ticket = reinterpret_cast<uint32_t *>(b + y.ticket_off);
   d.umax = reinterpret_cast<float2 *>(b + y.umax_off);
+  d.dstate = reinterpret_cast<DevCache::State *>(b + y.state_off);
   d.page_bytes = (uint32_t)y.page_bytes;
   d.pg_kscale = (uint32_t)y.pg_kscale; d.pg_kzero = (uint32_t)y.pg_kzero;
   d.pg_kcodes = (uint32_t)y.pg_kcodes; d.pg_vscale = (uint32_t)y.pg_vscale;
@@ -152,6 +153,11 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
     lp.n_q = n_q;
     lp.P = p.n_pages;
     lp.Rc = (L - n_q + rows - 1) / rows;
+    lp.dev_L = (c->options & AKVQ_OPT_DEVICE_L) ? 1 : 0;
+    if (lp.dev_L) {   // the ring chunks of the whole flush period: L - n_q <= R + G - 1
+      const int span = f.residual + f.group - 1 > L - n_q ? f.residual + f.group - 1 : L - n_q;
+      lp.Rc = (span + rows - 1) / rows;
+    }
     if (f.kind == AKVQ_PSA) {
       lp.Sc = (f.top_k > 0 && n_q > 0) ? (f.top_k + rows - 1) / rows : 0;   // <= rows each
     } else {
@@ -173,7 +179,7 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
       p.fast = 0;
       lp.per_u = 1;
     } else if (build_tab) {               // interleave rows between pages (Bresenham)
-      const int NR = lp.Rc + lp.Sc, n_ring = L - n_q;
+      const int NR = lp.Rc + lp.Sc, n_ring = lp.dev_L ? lp.Rc * rows : L - n_q;   // DEVICE_L: the period's span
       int k = 0, r = 0;
       auto row_item = [&](int ri) -> uint32_t {
         if (ri < lp.Rc) {
@@ -267,7 +273,10 @@ akvq_status launch_fast(const akvq_cache *c, DecodePlan &p, const void *q, const
   const_cast<akvq_cache *>(c)->launches += 1;
   // prologue prefetch: only if the preceding kernel of this stream does not
   // write this cache (the new row of a fused step is patched in after the wait)
-  p.lp.prologue = prefetch_safe(c, s) && !(c->options & AKVQ_OPT_STREAM_ONLY) ? 1 : 0;
+  // (never under DEVICE_L: a replayed graph may run this launch right after the
+  // same cache's previous step, whatever preceded it when it was recorded)
+  p.lp.prologue = prefetch_safe(c, s) && !(c->options & (AKVQ_OPT_STREAM_ONLY | AKVQ_OPT_DEVICE_L)) ? 1 : 0;
+  p.lp.appends = k != nullptr ? 1 : 0;
   const cudaError_t e =
       layer_uses_gqa(c->cfg.q_per_kv)
           ? launch_decode_gqa(d, c->cfg.dtype16, p.lp, q, k, v, types, static_cast<float *>(ws), out, flags, s)
@@ -317,6 +326,8 @@ akvq_status akvq_cache_layout(const akvq_config *f, akvq_layout *y) {
   // per unit: the largest |K scale| and |V scale| stored so far (the decode
   // kernel's fixed-point ranges; maintained by the quantize kernel)
   y->umax_off = t;     t = align_up(t + U * 8, 256);
+  // device token count L and the fused decode's launch-exit counter
+  y->state_off = t;    t = align_up(t + 16, 256);
   y->total_bytes = t;
   return AKVQ_OK;
 }
@@ -435,7 +446,8 @@ static akvq_status quantize_prompt(akvq_cache *c, const void *K, const void *V, 
   const int nb = n_q / f.group;
   cudaError_t e = launch_quantize_blocks(d, f.dtype16, src, 0, nb, nb - 1, s);
   if (e == cudaSuccess) e = launch_ring_fill(d, K, V, L0, n_q, L0, s);
-  c->launches += (nb > 0) + (L0 > n_q);
+  if (e == cudaSuccess) e = launch_state_set(d, L0, s);    // device copy of L
+  c->launches += (nb > 0) + (L0 > n_q) + 1;
   note_launch(c, s, true);
   if (e != cudaSuccess) return AKVQ_ECUDA;
   c->L = L0;
@@ -506,6 +518,7 @@ static akvq_status decode_impl(const akvq_cache *c, const void *q, float *out, v
   const DevCache d = make_dev(c);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (p.fast) return launch_fast(c, p, q, nullptr, nullptr, nullptr, out, ws, flags, s);
+  if (c->options & AKVQ_OPT_DEVICE_L) return AKVQ_EUNSUPPORTED;   // generic kernels use the host L
   const_cast<akvq_cache *>(c)->launches += 2;         // split + combine
   const cudaError_t e = launch_decode(d, c->cfg.dtype16, p, q, out, ws, flags, s);
   note_launch(const_cast<akvq_cache *>(c), s, false);
@@ -538,6 +551,16 @@ akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const 
                                      reinterpret_cast<cudaStream_t>(stream));
   if (st != AKVQ_OK) return st;
   c->L = L1;
+  return AKVQ_OK;
+}
+
+akvq_status akvq_cache_advance(akvq_cache *c, int32_t steps) {
+  if (!c || steps < 0) return AKVQ_EINVAL;
+  const akvq_config &f = c->cfg;
+  if (c->L + steps > f.capacity) return AKVQ_ECAPACITY;
+  // no block may have left the window in between (the replayed launches do not flush)
+  if (c->L + steps - f.residual - c->n_q >= f.group) return AKVQ_ESTATE;
+  c->L += steps;
   return AKVQ_OK;
 }
 

@@ -23,6 +23,8 @@ struct DevCache {
   uint8_t *side;           // [U][side_cap][side_entry]
   uint32_t *ticket;        // [U * hg] decode-merge tickets (zero between launches)
   float2 *umax;            // [U] (max |K scale|, max |V scale|) of the unit's pages
+  struct State { int32_t L; uint32_t done; int32_t pad[2]; };
+  State *dstate;           // device copy of the token count L (+ launch exit counter)
   uint32_t page_bytes, pg_kscale, pg_kzero, pg_kcodes, pg_vscale, pg_vzero, pg_vcodes;
   uint32_t side_entry;
   int32_t n_pages, slots, bm_words, side_cap;

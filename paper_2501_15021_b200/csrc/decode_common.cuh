@@ -113,7 +113,8 @@ __device__ __forceinline__ float rs_reduce(float (&v)[NV], int cq, int &mine) {
 // One sub-load of the pipeline: an item split into stage-sized pieces.  The
 // producer lane records it in the warp's descriptor ring (one per stage).
 struct LySub {
-  int u, kind;   // u: (virtual) unit; kind: 0 page K half, 1 page V half, 2 16-bit rows, 3 4-bit rows, -1 none
+  int u, kind;   // u: (virtual) unit; kind: 0 page K half, 1 page V half, 2 16-bit rows, 3 4-bit rows,
+                 // 4 empty unit marker (no data), -1 none
   int pu;        // physical unit (u / head groups), producer side only
   int a, n;      // page index | first row (ring offset from n_q / side entry) and row count
   int ring;      // 1 if ring rows
@@ -340,6 +341,26 @@ __device__ __noinline__ void merge_layer_unit(const DevCache &c, const LayerPlan
       const float tr = x[k] * c.inv_sqrt_d;
       dst[k] = (out_rot ? rot[k] + tr : tr + org[k]) * inv;
     }
+  }
+}
+
+// End of a fused-step launch: every warp of the grid reports its exit; the last
+// one advances the device token count L.  Every warp reads L right after its
+// griddepcontrol.wait, before any warp can be the last to exit, so a launch sees
+// the L of its own step; this keeps the launch parameters the same from step to
+// step (CUDA-graph replay, AKVQ_OPT_DEVICE_L).
+// The count is kept per CTA in shared memory (cta_done, zeroed before any warp
+// can exit); the last warp of a CTA reports the CTA.  No fence is needed: a
+// warp's L was loaded before its own exit, and the next launch sees the new L
+// after griddepcontrol.wait (full completion of this grid).
+__device__ __forceinline__ void ly_exit(const DevCache &c, const LayerPlan &lp, int lane,
+                                        unsigned *cta_done) {
+  if (!(lp.appends && lp.dev_L)) return;
+  __syncwarp();
+  if (lane == 0 && atomicAdd(cta_done, 1u) == (blockDim.x >> 5) - 1u &&
+      atomicAdd(&c.dstate->done, 1u) == gridDim.x - 1u) {
+    c.dstate->done = 0u;
+    c.dstate->L += 1;
   }
 }
 

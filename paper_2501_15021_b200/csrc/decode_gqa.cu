@@ -178,6 +178,11 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
   static_assert(TQ <= 32 && CQ <= 32 && G >= 32, "page shape");
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ unsigned cta_done;                 // warps of this CTA done (ly_exit)
+  if (lp.dev_L) {                               // (uniform: the barrier is legal)
+    if (threadIdx.x == 0) cta_done = 0u;
+    __syncthreads();
+  }
   const size_t SB = ly_stage_bytes(c);
   uint8_t *wsm = smem + (size_t)warp * S::warp_bytes(SB);
   float *orr = reinterpret_cast<float *>(wsm + S::orr_off(SB));             // [NH][32][4]
@@ -190,10 +195,13 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
     pdl_launch_dependents();
   }
   const int gw = blockIdx.x * kGqWarps + warp;
-  if (gw >= lp.W) return;
+  if (gw >= lp.W) { ly_exit(c, lp, lane, &cta_done); return; }
   const int ib = ly_first_item(lp, gw);
   const int ie = gw + 1 < lp.W ? ly_first_item(lp, gw + 1) : lp.T;
-  if (ib >= ie) return;
+  if (ib >= ie) { ly_exit(c, lp, lane, &cta_done); return; }
+  // this launch's token count, the new token included when it appends (DEVICE_L
+  // launches have no prologue: the griddepcontrol.wait above has been passed)
+  const int Lc = lp.dev_L ? c.dstate->L + (lp.appends ? 1 : 0) : lp.L;
   constexpr bool tsa = TSA;
   const int HG = lp.hg;
   const float alpha_k = kLog2e / (float)D;      // q~_u . K^_n / d in log2 units (pages, 4-bit rows)
@@ -209,6 +217,7 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
   int pu = ib / lp.per_u, pj = ib - (ib / lp.per_u) * lp.per_u, left = ie - ib, part_i = 0;
   int pphys = pu / HG, phg = pu - (pu / HG) * HG;
   const uint8_t *ubase = c.pages + (size_t)pphys * c.n_pages * c.page_bytes;
+  int eu = -1;                                  // last (virtual) unit a sub-load was issued for
   const uint8_t *vsrc = nullptr;
   uint2 vdesc = make_uint2(0u, 0u);
   auto produce = [&](int st) -> uint2 {
@@ -236,6 +245,10 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
         sb.kind = 0; sb.n = 0;
       } else if (kind == 2) {
         sb.kind = 2; sb.ring = 1; sb.n = n;
+        if (lp.dev_L) {                           // chunks of the period past L: skip
+          sb.n = min(n, Lc - lp.n_q - a);
+          ok = sb.n > 0;
+        }
       } else {
         const int cnt = __ldg(c.side_cnt + pphys);
         auto fdiv = [&](int x) {
@@ -262,7 +275,9 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
         }
         --left;
       }
+      const bool unit_done = next && (pj == 0 || left == 0);   // the item closed its unit's run
       if (ok) {
+        eu = sb.u;
         if (sb.kind == 0) {
           if (lane == 0) {
             mbar_expect_tx(&bar[st], kbytes);
@@ -292,6 +307,15 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
         }
         break;
       }
+      if (unit_done && eu != sb.u) {
+        // every item of this unit in the range was empty (empty side splits, ring
+        // chunks past L): an empty sub-load still reaches the consumer, which then
+        // writes the (empty) partial the unit's merge ticket counts on
+        eu = sb.u;
+        sb.kind = 4;
+        if (lane == 0) mbar_expect_tx(&bar[st], 0u);
+        break;
+      }
       sb.kind = -1;
     }
     return pack_sub(sb);
@@ -302,6 +326,8 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
     pdl_wait();
     pdl_launch_dependents();
   }
+  // host-L mode: keep the device copy current (a later DEVICE_L launch reads it)
+  if (!lp.dev_L && lp.appends && blockIdx.x == 0 && threadIdx.x == 0) c.dstate->L = lp.L;
 
   // lane roles
   const int mg = lane >> 2, mt = lane & 3;            // MMA fragment group / thread in group
@@ -760,18 +786,20 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
           }
         }
       }
+    } else if (s.kind == 4) {
+      mbar_wait(&bar[st], par);                       // empty unit marker (no data)
     } else {
       // ================= rows (rotated basis, one at a time)
       mbar_wait(&bar[st], par);
       const bool r16 = s.kind == 2;
       if (s.ring && app_k != nullptr) {
-        const int tl = lp.L - 1 - (lp.n_q + s.a);
+        const int tl = Lc - 1 - (lp.n_q + s.a);
         if (tl >= 0 && tl < s.n) {
           const int uu = cur_pu;
           const uint4 *sk = reinterpret_cast<const uint4 *>(app_k + (size_t)uu * D);
           const uint4 *svv = reinterpret_cast<const uint4 *>(app_v + (size_t)uu * D);
           uint8_t *Bw = B + (size_t)tl * 4 * D;
-          uint4 *rrow = reinterpret_cast<uint4 *>(ring_row(c, uu, (lp.L - 1) % c.slots));
+          uint4 *rrow = reinterpret_cast<uint4 *>(ring_row(c, uu, (Lc - 1) % c.slots));
           for (int i = lane; i < D / 8; i += 32) {
             const uint4 kv = sk[i], vv = svv[i];
             reinterpret_cast<uint4 *>(Bw)[i] = kv;
@@ -780,11 +808,12 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
             rrow[D / 8 + i] = vv;
           }
           if (lane == 0 && tsa && app_types != nullptr && app_types[uu] == 1)
-            atomicOr(&c.bitmask[(size_t)uu * c.bm_words + (lp.L - 1) / 32], 1u << ((lp.L - 1) % 32));
+            atomicOr(&c.bitmask[(size_t)uu * c.bm_words + (Lc - 1) / 32], 1u << ((Lc - 1) % 32));
           __syncwarp();
         }
       }
-      for (int r = 0; r < s.n; ++r) {
+      const int nrows = s.ring ? min(s.n, Lc - lp.n_q - s.a) : s.n;
+      for (int r = 0; r < nrows; ++r) {
         float k4[4], v4[4];
         if (r16) {                                    // 16-bit row (original basis) -> x . H
           const uint8_t *row = B + (size_t)r * 4 * D;
@@ -834,6 +863,7 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
     if (++st == kLyStages) { st = 0; par ^= 1u; }
   }
   if (cur_u >= 0) flush(cur_u);
+  ly_exit(c, lp, lane, &cta_done);
 }
 
 template <int D, int G, int NH>

@@ -95,6 +95,11 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   static_assert(BFLY == 4, "row groups: lane bits >= 2 index the rows");
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ unsigned cta_done;                 // warps of this CTA done (ly_exit)
+  if (lp.dev_L) {                               // (uniform: the barrier is legal)
+    if (threadIdx.x == 0) cta_done = 0u;
+    __syncthreads();
+  }
   const size_t SB = ly_stage_bytes(c);
   uint8_t *wsm = smem + (size_t)warp * S::warp_bytes(SB);
   float *qh = reinterpret_cast<float *>(wsm + S::qh_off(SB));
@@ -111,10 +116,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     pdl_launch_dependents();                    // the next layer's kernel may queue up
   }
   const int gw = blockIdx.x * kLyWarps + warp;
-  if (gw >= lp.W) return;
+  if (gw >= lp.W) { ly_exit(c, lp, lane, &cta_done); return; }
   const int ib = ly_first_item(lp, gw);
   const int ie = gw + 1 < lp.W ? ly_first_item(lp, gw + 1) : lp.T;
-  if (ib >= ie) return;
+  if (ib >= ie) { ly_exit(c, lp, lane, &cta_done); return; }
+  // this launch's token count, the new token included when it appends (DEVICE_L
+  // launches have no prologue: the griddepcontrol.wait above has been passed)
+  const int Lc = lp.dev_L ? c.dstate->L + (lp.appends ? 1 : 0) : lp.L;
   constexpr bool tsa = TSA;                     // layer kind (Table I): TSA has 4-bit text rows
   // GQA (NEXT-3): a unit's g query heads are processed in HG groups of NH heads;
   // work items, partials and tickets are per virtual unit vu = u * HG + group
@@ -135,6 +143,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   int pu = ib / lp.per_u, pj = ib - (ib / lp.per_u) * lp.per_u, left = ie - ib, part_i = 0;
   int pphys = pu / HG, phg = pu - (pu / HG) * HG;   // physical unit / head group of pu
   const uint8_t *ubase = c.pages + (size_t)pphys * c.n_pages * c.page_bytes;   // pages of pphys
+  int eu = -1;                                  // last (virtual) unit a sub-load was issued for
   const uint8_t *vsrc = nullptr;                // pending V half (issued next)
   uint2 vdesc = make_uint2(0u, 0u);
   // salient bits of a page's tokens, loaded with its K half (this lane's word:
@@ -166,6 +175,10 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         sb.kind = 0; sb.n = 0;
       } else if (kind == 2) {                     // ring chunk (rows n of it)
         sb.kind = 2; sb.ring = 1; sb.n = n;
+        if (lp.dev_L) {                           // chunks of the period past L: skip
+          sb.n = min(n, Lc - lp.n_q - a);
+          ok = sb.n > 0;
+        }
       } else {                                    // side split a: entries [lo, hi), runtime count
         const int cnt = __ldg(c.side_cnt + pphys);
         // floor(a cnt / Sc) and floor((a + 1) cnt / Sc): fp32 estimate, corrected
@@ -194,7 +207,9 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         }
         --left;
       }
+      const bool unit_done = next && (pj == 0 || left == 0);   // the item closed its unit's run
       if (ok) {
+        eu = sb.u;
         if (sb.kind == 0) {
           if (lane == 0) {
             mbar_expect_tx(&bar[st], kbytes);
@@ -225,6 +240,15 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         }
         break;
       }
+      if (unit_done && eu != sb.u) {
+        // every item of this unit in the range was empty (empty side splits, ring
+        // chunks past L): an empty sub-load still reaches the consumer, which then
+        // writes the (empty) partial the unit's merge ticket counts on
+        eu = sb.u;
+        sb.kind = 4;
+        if (lane == 0) mbar_expect_tx(&bar[st], 0u);
+        break;
+      }
       sb.kind = -1;
     }
     return pack_sub(sb);
@@ -238,6 +262,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     pdl_wait();
     pdl_launch_dependents();
   }
+  // host-L mode: keep the device copy current (a later DEVICE_L launch reads it)
+  if (!lp.dev_L && lp.appends && blockIdx.x == 0 && threadIdx.x == 0) c.dstate->L = lp.L;
 
   // lane roles
   const int ktq = lane % TQ, kcs = lane / TQ;         // page K phase
@@ -809,6 +835,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           o_rot[h][3] = fmaf(dw * 0.015625f, fmaf(65536.f, o.w, e.w), o_rot[h][3]);
         }
       }
+    } else if (s.kind == 4) {
+      mbar_wait(&bar[st], par);                       // empty unit marker (no data)
     } else {
       // ================= rows: 16-bit (ring / PSA side, original basis) or
       //                   4-bit (TSA side, rotated basis), in groups of kRows
@@ -817,13 +845,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       if (s.ring && app_k != nullptr) {
         // the newest token (Eq. 2): the stale ring slot was staged -- patch in
         // the caller's row, append it to the ring and set its TSA text bit
-        const int tl = lp.L - 1 - (lp.n_q + s.a);
+        const int tl = Lc - 1 - (lp.n_q + s.a);
         if (tl >= 0 && tl < s.n) {
           const int uu = cur_pu;                     // (every head group appends: benign, identical)
           const uint4 *sk = reinterpret_cast<const uint4 *>(app_k + (size_t)uu * D);
           const uint4 *sv = reinterpret_cast<const uint4 *>(app_v + (size_t)uu * D);
           uint8_t *Bw = B + (size_t)tl * 4 * D;
-          uint4 *rrow = reinterpret_cast<uint4 *>(ring_row(c, uu, (lp.L - 1) % c.slots));
+          uint4 *rrow = reinterpret_cast<uint4 *>(ring_row(c, uu, (Lc - 1) % c.slots));
           for (int i = lane; i < D / 8; i += 32) {
             const uint4 kv = sk[i], vv = sv[i];
             reinterpret_cast<uint4 *>(Bw)[i] = kv;
@@ -832,14 +860,16 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
             rrow[D / 8 + i] = vv;
           }
           if (lane == 0 && tsa && app_types != nullptr && app_types[uu] == 1)
-            atomicOr(&c.bitmask[(size_t)uu * c.bm_words + (lp.L - 1) / 32], 1u << ((lp.L - 1) % 32));
+            atomicOr(&c.bitmask[(size_t)uu * c.bm_words + (Lc - 1) / 32], 1u << ((Lc - 1) % 32));
           __syncwarp();
         }
       }
       const uint32_t pitch = r16 ? 4u * D : (uint32_t)c.side_entry;
       const uint32_t sbase = smem_u32(B);
-      for (int g0 = 0; g0 < s.n; g0 += kRows) {
-        const int n = min(kRows, s.n - g0);
+      // ring chunks planned for the whole flush period hold rows past L (DEVICE_L)
+      const int nrows = s.ring ? min(s.n, Lc - lp.n_q - s.a) : s.n;
+      for (int g0 = 0; g0 < nrows; g0 += kRows) {
+        const int n = min(kRows, nrows - g0);
         const uint32_t sb0 = sbase + (uint32_t)g0 * pitch;
         if (n < kRows) {   // zero-fill the group's missing rows (finite, masked below)
           uint4 *z = reinterpret_cast<uint4 *>(B + (size_t)(g0 + n) * pitch);
@@ -856,6 +886,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   }
   if constexpr (!SO)
     if (cur_u >= 0) flush(cur_u);
+  ly_exit(c, lp, lane, &cta_done);
 }
 
 template <int D, int G, int NH>

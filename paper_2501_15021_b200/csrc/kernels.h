@@ -40,6 +40,8 @@ struct LayerPlan {
   int cu, CT;
   int exact_logits;     // AKVQ_OPT_EXACT_LOGITS (test hook): fp32 page logits
   float sc_inv;         // 1 / Sc (side-split bounds without an integer division)
+  int dev_L;            // 1: take L from DevCache::dstate (plan covers the flush period)
+  int appends;          // 1: this launch appends the new token (fused step)
   int prologue;         // 1: the preceding grid does not write this cache, so the
                         // first TMA sub-loads may be issued before griddepcontrol.wait
   uint32_t tab[kLyMaxTab];
@@ -66,6 +68,7 @@ cudaError_t launch_ring_fill(const DevCache &c, const void *K, const void *V, in
                              int t1, cudaStream_t st);
 cudaError_t launch_append(const DevCache &c, const void *k, const void *v,
                           const uint8_t *types, int L, cudaStream_t st);
+cudaError_t launch_state_set(const DevCache &c, int L, cudaStream_t st);
 cudaError_t launch_decode(const DevCache &c, int dtype16, const DecodePlan &p, const void *q,
                           float *out, void *ws, uint32_t flags, cudaStream_t st);
 cudaError_t launch_decode_layer(const DevCache &c, int dtype16, const LayerPlan &lp, const void *q,

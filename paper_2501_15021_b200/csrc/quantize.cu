@@ -407,6 +407,12 @@ __global__ void k_append(DevCache c, const uint16_t *__restrict__ k,
   }
   if (threadIdx.x == 0 && c.kind == AKVQ_TSA && types && types[u] == 1)
     c.bitmask[(size_t)u * c.bm_words + L / 32] |= 1u << (L % 32);
+  if (u == 0 && threadIdx.x == 0) c.dstate->L = L + 1;   // device copy of L
+}
+
+__global__ void k_state_set(DevCache c, int L) {
+  c.dstate->L = L;
+  c.dstate->done = 0u;
 }
 
 // ============================================================ launchers
@@ -466,6 +472,11 @@ cudaError_t launch_ring_fill(const DevCache &c, const void *K, const void *V, in
   const int n = (t1 - t0) * 2 * (c.d / 8);
   dim3 grid((n + 255) / 256, c.U);
   k_ring_fill<<<grid, 256, 0, st>>>(c, (const uint16_t *)K, (const uint16_t *)V, L0, t0, t1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_state_set(const DevCache &c, int L, cudaStream_t st) {
+  k_state_set<<<1, 1, 0, st>>>(c, L);
   return cudaGetLastError();
 }
 

@@ -538,3 +538,72 @@ def test_exact_logit_path(ak, orc, sy, name, layer):
     w = sy.get(name)
     units = None if name == "tiny" else [0, 17, 31]
     _run_case(ak, orc, sy, w, layer, steps=3, units=units, options=ak.AKVQ_OPT_EXACT_LOGITS)
+
+
+# ----------------------------------------------------------------- NEXT-4: device L, graphs
+@pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
+@pytest.mark.parametrize("g", [1, 7])
+def test_device_L_steps(ak, orc, sy, kind, g):
+    """AKVQ_OPT_DEVICE_L: the fused kernel takes L from the cache buffer and the
+    item table covers the flush period; stepping through two flushes matches the
+    oracle exactly as the host-L mode does."""
+    import dataclasses
+    w = dataclasses.replace(sy.TINY, name=f"tinyg{g}", hq=4 * g, hkv=4, decode_steps=80)
+    _run_case(ak, orc, sy, w, 0, kind=kind, steps=70, check_every=7,
+              options=ak.AKVQ_OPT_DEVICE_L, fused_step=True)
+
+
+@pytest.mark.parametrize("name,layer", [("tiny", 0), ("llava7b", 2), ("qwen_gqa", 3)])
+def test_cuda_graph_replay(ak, orc, sy, name, layer):
+    """A decode step captured once in a CUDA graph (AKVQ_OPT_DEVICE_L) and replayed
+    for the following steps of the flush period, new q / k / v copied into the
+    captured input buffers before each replay: outputs match the oracle step by
+    step; the host mirror is then advanced with akvq_cache_advance."""
+    w = sy.get(name)
+    us = [0, w.U // 2, w.U - 1] if w.U > 4 else list(range(w.U))
+    gcfg, _ = _configs(ak, orc, w, layer, w.U)
+    _, ocfg = _configs(ak, orc, w, layer, len(us))
+    lc = ak.LayerCache(gcfg, options=ak.AKVQ_OPT_DEVICE_L)
+    inp = sy.layer_inputs(w, layer, device="cuda")
+    lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
+    oc = orc.OracleCache(ocfg)
+    io = sy.layer_inputs(w, layer, units=us, device="cpu")
+    oc.prefill(f16_bits(io["K"]), f16_bits(io["V"]), io["types"].numpy(), io["colsum"].numpy())
+    step0 = 0
+    while w.R + w.G - 1 - (lc.L - lc.n_q) < 3:               # a flush is due: step past it
+        di = sy.decode_inputs(w, layer, step0, device="cuda")
+        lc.step(di["k"], di["v"], di["q"], di["types"])
+        do = sy.decode_inputs(w, layer, step0, units=us, device="cpu")
+        oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
+        step0 += 1
+    nsteps = min(12, w.R + w.G - 1 - (lc.L - lc.n_q))        # stay inside the flush period
+    d0 = sy.decode_inputs(w, layer, 0, device="cuda")
+    bq, bk, bv, bt = (d0["q"].clone(), d0["k"].clone(), d0["v"].clone(), d0["types"].clone())
+    out = torch.empty(bq.shape, dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            lc.step(bk, bv, bq, bt, out=out)                 # recorded, not run (host L += 1)
+    torch.cuda.current_stream().wait_stream(s)
+    L_host0 = lc.L - 1
+    for step in range(step0, step0 + nsteps):
+        di = sy.decode_inputs(w, layer, step, device="cuda")
+        bq.copy_(di["q"]); bk.copy_(di["k"]); bv.copy_(di["v"]); bt.copy_(di["types"])
+        graph.replay()
+        do = sy.decode_inputs(w, layer, step, units=us, device="cpu")
+        oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
+        ref = oc.decode(f16_bits(do["q"]))
+        err = np.abs(out[us].double().cpu().numpy() - ref).max()
+        record_margin(_case_name(), err, OUT_TOL)
+        assert err <= OUT_TOL, f"replay {step}: {err}"
+    ak.akvq_cache_advance(lc.handle, nsteps - 1)
+    assert lc.L == L_host0 + nsteps == oc.L
+    compare_state(GpuState(lc), oc.export(), gcfg, units=us)
+    # the next (non-replayed) step continues from the device state
+    di = sy.decode_inputs(w, layer, step0 + nsteps, device="cuda")
+    o2 = lc.step(di["k"], di["v"], di["q"], di["types"])
+    do = sy.decode_inputs(w, layer, step0 + nsteps, units=us, device="cpu")
+    oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
+    assert np.abs(o2[us].double().cpu().numpy() - oc.decode(f16_bits(do["q"]))).max() <= OUT_TOL
