@@ -82,13 +82,19 @@ typedef struct {
   float clip2;        /* 2-bit clip ratio, (0,1], paper 0.8           */
   float clip4;        /* 4-bit clip ratio, (0,1], paper 1.0           */
   int32_t k_axis;     /* akvq_k_axis (0 = per channel, the graded default)    */
+  int32_t paged;      /* 0: the pages live in the cache buffer; 1: in a caller-
+                         owned page pool shared by any number of caches, found
+                         through a block table (akvq_cache_attach_pages)      */
 } akvq_config;
 
 /* Byte layout of the caller's cache buffer (all offsets from its base;
  * every region 256-byte aligned).  cap = capacity rounded up to G;
  * n_pages = cap / G; ng = d / G; slots = R + G.
  *
- *  pages   [U][n_pages][page_bytes]        one page = one G-token block:
+ *  pages   [U][n_pages][page_bytes]        one page = one G-token block (not in
+ *                                      the buffer when cfg.paged: page p of
+ *                                      unit u is pool + block_table[u][p] *
+ *                                      page_bytes, akvq_cache_attach_pages):
  *            +pg_kscale  f32 [d]     K scale per channel (normalized basis);
  *                                    per token: f32 [G][ng] (same bytes)
  *            +pg_kzero   i32 [d]     K zero point per channel; per token [G][ng]
@@ -154,9 +160,10 @@ typedef struct {
   int32_t launches;    /* kernels enqueued by the last call on this cache
                           (host counter, for launch accounting in bench.py)  */
   uint64_t last_write; /* library launch sequence number of the last launch
-                          that wrote this cache (host; decides whether the
-                          decode kernel may stream cache pages before the
-                          preceding grid has completed)                       */
+                          that wrote this cache (host)                        */
+  void *pool;          /* paged caches: device page pool (page_bytes each)    */
+  const int32_t *block_table; /* paged caches: device [U][n_pages] i32, the
+                          pool page of logical page p of unit u              */
 } akvq_cache;
 
 /* akvq_cache.options: route 2-bit pages through the generic split-K kernel
@@ -203,6 +210,18 @@ size_t akvq_cache_bytes(const akvq_config *cfg);
  * Errors: EINVAL, EUNSUPPORTED, ECAPACITY (bytes < akvq_cache_bytes). */
 akvq_status akvq_cache_init(akvq_cache *c, const akvq_config *cfg, void *dev_buf,
                             size_t bytes, akvq_stream_t stream);
+
+/* Paged caches (cfg.paged = 1, a block table as in paged KV
+ * caches): attach the caller's page pool and block table.  pool: device memory
+ * of page_bytes-sized pages (any number, shared by caches); block_table: device
+ * i32 [U][n_pages], entry (u, p) = index of the pool page holding logical page
+ * p (tokens [pG, (p+1)G)) of unit u.  The caller owns both, fills the entries
+ * of every page the cache will quantize before that happens (pages fill in
+ * order: page p is written when n_q passes (p+1) G), and never maps one pool
+ * page to two live logical pages.  Host call; no work is enqueued.
+ * Errors: EINVAL (NULL, or a cache that is not paged).  Every other call on a
+ * paged cache without attached pages returns ESTATE. */
+akvq_status akvq_cache_attach_pages(akvq_cache *c, void *pool, const int32_t *block_table);
 
 /* ---------------------------------------------------------------- prefill */
 /* prefill: for every unit, select salient

@@ -35,6 +35,7 @@ EXPORTS = (
     "akvq_decode_attention", "akvq_select_salient", "akvq_dequantize_view",
     "akvq_memory_report", "akvq_status_str", "akvq_version", "akvq_decode_step",
     "akvq_detect_pivots", "akvq_rotate_quantize_pivots", "akvq_cache_advance",
+    "akvq_cache_attach_pages",
 )
 
 
@@ -48,7 +49,8 @@ class akvq_config(C.Structure):
     _fields_ = [("n_units", C.c_int32), ("q_per_kv", C.c_int32), ("head_dim", C.c_int32),
                 ("group", C.c_int32), ("residual", C.c_int32), ("capacity", C.c_int32),
                 ("top_k", C.c_int32), ("kind", C.c_int32), ("dtype16", C.c_int32),
-                ("clip2", C.c_float), ("clip4", C.c_float), ("k_axis", C.c_int32)]
+                ("clip2", C.c_float), ("clip4", C.c_float), ("k_axis", C.c_int32),
+                ("paged", C.c_int32)]
 
 
 class akvq_layout(C.Structure):
@@ -63,7 +65,8 @@ class akvq_layout(C.Structure):
 class akvq_cache(C.Structure):
     _fields_ = [("cfg", akvq_config), ("lay", akvq_layout), ("base", C.c_void_p),
                 ("L", C.c_int32), ("n_q", C.c_int32), ("sm_count", C.c_int32),
-                ("options", C.c_int32), ("launches", C.c_int32), ("last_write", C.c_uint64)]
+                ("options", C.c_int32), ("launches", C.c_int32), ("last_write", C.c_uint64),
+                ("pool", C.c_void_p), ("block_table", C.c_void_p)]
 
 
 class akvq_mem_report(C.Structure):
@@ -120,6 +123,8 @@ def lib() -> C.CDLL:
         L.akvq_rotate_quantize_pivots.argtypes = [C.POINTER(akvq_cache), P, P, C.c_int32, P, P,
                                                   C.c_int32, C.c_int32, P]
         L.akvq_rotate_quantize_pivots.restype = S
+        L.akvq_cache_attach_pages.argtypes = [C.POINTER(akvq_cache), P, P]
+        L.akvq_cache_attach_pages.restype = S
         L.akvq_cache_advance.argtypes = [C.POINTER(akvq_cache), C.c_int32]
         L.akvq_cache_advance.restype = S
         L.akvq_status_str.argtypes = [S]
@@ -159,8 +164,8 @@ def _stream(stream: Optional[torch.cuda.Stream]):
 
 
 def make_config(U, g, d, G, R, capacity, top_k, kind, dtype16=AKVQ_BF16, clip2=0.8,
-                clip4=1.0, k_axis=0) -> akvq_config:
-    return akvq_config(U, g, d, G, R, capacity, top_k, kind, dtype16, clip2, clip4, k_axis)
+                clip4=1.0, k_axis=0, paged=0) -> akvq_config:
+    return akvq_config(U, g, d, G, R, capacity, top_k, kind, dtype16, clip2, clip4, k_axis, paged)
 
 
 # ----------------------------------------------------------------- C-ABI calls
@@ -235,6 +240,13 @@ def akvq_rotate_quantize_pivots(cache, K, V, L0, pivots, counts, units_per_row, 
            "akvq_rotate_quantize_pivots")
 
 
+def akvq_cache_attach_pages(cache, pool: torch.Tensor, block_table: torch.Tensor):
+    if block_table.dtype != torch.int32:
+        raise ValueError("block_table must be int32")
+    _check(lib().akvq_cache_attach_pages(C.byref(cache), _ptr(pool), _ptr(block_table)),
+           "akvq_cache_attach_pages")
+
+
 def akvq_cache_advance(cache, steps: int):
     _check(lib().akvq_cache_advance(C.byref(cache), int(steps)), "akvq_cache_advance")
 
@@ -252,18 +264,60 @@ def akvq_memory_report(cache, side_entries: int = -1) -> akvq_mem_report:
 
 
 # ----------------------------------------------------------------- convenience
-class LayerCache:
-    """One layer's packed cache in a torch-owned device buffer."""
+class PagePool:
+    """Device pool of cache pages shared by paged caches (akvq_config.paged = 1).
+    Host-side free list; a page is page_bytes bytes (akvq_layout.page_bytes of
+    the caches it serves, which must agree)."""
 
-    def __init__(self, cfg: akvq_config, device="cuda", stream=None, options: int = 0):
+    def __init__(self, n_pages: int, page_bytes: int, device="cuda"):
+        self.page_bytes = int(page_bytes)
+        self.n_pages = int(n_pages)
+        self.buf = torch.empty(self.n_pages * self.page_bytes, dtype=torch.uint8, device=device)
+        self.free = list(range(self.n_pages))
+
+    def alloc(self, n: int, shuffle_seed: Optional[int] = None):
+        if n > len(self.free):
+            raise RuntimeError(f"page pool exhausted ({n} > {len(self.free)} free)")
+        if shuffle_seed is not None:           # scattered pages (tests)
+            g = torch.Generator().manual_seed(shuffle_seed)
+            perm = torch.randperm(len(self.free), generator=g).tolist()
+            self.free = [self.free[i] for i in perm]
+        out, self.free = self.free[:n], self.free[n:]
+        return out
+
+    def release(self, pages):
+        self.free.extend(int(p) for p in pages)
+
+
+class LayerCache:
+    """One layer's packed cache in a torch-owned device buffer (pages in the
+    buffer, or -- cfg.paged -- in a shared PagePool through a block table)."""
+
+    def __init__(self, cfg: akvq_config, device="cuda", stream=None, options: int = 0,
+                 pool: Optional[PagePool] = None, shuffle_seed: Optional[int] = None):
         self.cfg = cfg
         self.layout = akvq_cache_layout(cfg)
         self.buf = torch.empty(int(self.layout.total_bytes), dtype=torch.uint8, device=device)
         self.handle = akvq_cache()
         akvq_cache_init(self.handle, cfg, self.buf, stream)
         self.handle.options = options
+        self.pool, self.pages = None, None
+        if cfg.paged:
+            if pool is None or pool.page_bytes != int(self.layout.page_bytes):
+                raise ValueError("a paged cache needs a PagePool of its page size")
+            n = cfg.n_units * int(self.layout.n_pages)
+            self.pool, self.pages = pool, pool.alloc(n, shuffle_seed)
+            self.block_table = torch.tensor(self.pages, dtype=torch.int32, device=device).view(
+                cfg.n_units, int(self.layout.n_pages))
+            akvq_cache_attach_pages(self.handle, pool.buf, self.block_table)
         self.ws = torch.empty(max(1, akvq_decode_workspace_bytes_max(self.handle)) // 4 + 1,
                               dtype=torch.float32, device=device)
+
+    def release_pages(self):
+        """Return a paged cache's pages to its pool (the cache is unusable after)."""
+        if self.pool is not None and self.pages:
+            self.pool.release(self.pages)
+            self.pages = []
 
     @property
     def L(self) -> int:

@@ -27,7 +27,8 @@ akvq_status check_config(const akvq_config *f) {
       !(f->clip2 > 0.f && f->clip2 <= 1.f) || !(f->clip4 > 0.f && f->clip4 <= 1.f) ||
       (f->kind != AKVQ_TSA && f->kind != AKVQ_PSA) ||
       (f->dtype16 != AKVQ_BF16 && f->dtype16 != AKVQ_FP16) ||
-      (f->k_axis != AKVQ_K_PER_CHANNEL && f->k_axis != AKVQ_K_PER_TOKEN))
+      (f->k_axis != AKVQ_K_PER_CHANNEL && f->k_axis != AKVQ_K_PER_TOKEN) ||
+      (f->paged != 0 && f->paged != 1))
     return AKVQ_EINVAL;
   if ((f->head_dim != 64 && f->head_dim != 128) || f->group < 32 || f->group > 128 ||
       f->group > f->head_dim || f->q_per_kv > 16 || f->top_k > 32)
@@ -40,7 +41,8 @@ DevCache make_dev(const akvq_cache *c) {
   const akvq_layout &y = c->lay;
   uint8_t *b = static_cast<uint8_t *>(c->base);
   DevCache d;
-  d.pages = b + y.pages_off;
+  d.pages = f.paged ? static_cast<uint8_t *>(c->pool) : b + y.pages_off;
+  d.btab = f.paged ? c->block_table : nullptr;
   d.ring = reinterpret_cast<uint16_t *>(b + y.ring_off);
   d.bitmask = reinterpret_cast<uint32_t *>(b + y.bitmask_off);
   d.side_idx = reinterpret_cast<int32_t *>(b + y.side_idx_off);
@@ -313,7 +315,7 @@ akvq_status akvq_cache_layout(const akvq_config *f, akvq_layout *y) {
   y->pg_vcodes = o; o = align_up(o + G * d / 4, 16);
   y->page_bytes = align_up(o, 128);
   uint64_t t = 0;
-  y->pages_off = t;    t = align_up(t + U * y->n_pages * y->page_bytes, 256);
+  y->pages_off = t;    t = align_up(t + (f->paged ? 0 : U * y->n_pages * y->page_bytes), 256);
   y->ring_unit_bytes = (uint64_t)y->slots * 2 * d * 2;
   y->ring_off = t;     t = align_up(t + U * y->ring_unit_bytes, 256);
   y->bitmask_off = t;  t = align_up(t + U * y->bitmask_words * 4, 256);
@@ -366,6 +368,7 @@ akvq_status akvq_cache_init(akvq_cache *c, const akvq_config *f, void *dev_buf, 
 akvq_status akvq_select_salient(akvq_cache *c, const uint8_t *types, const float *colsum,
                                 int32_t L0, akvq_stream_t stream) {
   if (!c || !c->base || L0 < 0) return AKVQ_EINVAL;
+  if (c->cfg.paged && !c->pool) return AKVQ_ESTATE;   // pages not attached
   if (c->L != 0) return AKVQ_ESTATE;
   if (L0 > c->cfg.capacity) return AKVQ_ECAPACITY;
   if (L0 == 0) return AKVQ_OK;
@@ -387,6 +390,7 @@ akvq_status akvq_rotate_quantize(akvq_cache *c, const void *K, const void *V, in
                                  const uint8_t *types, const float *colsum,
                                  akvq_stream_t stream) {
   if (!c || !c->base || L0 < 0) return AKVQ_EINVAL;
+  if (c->cfg.paged && !c->pool) return AKVQ_ESTATE;   // pages not attached
   if (c->L != 0) return AKVQ_ESTATE;
   if (L0 > c->cfg.capacity) return AKVQ_ECAPACITY;
   if (L0 > 0 && (!K || !V)) return AKVQ_EINVAL;
@@ -458,6 +462,7 @@ static akvq_status quantize_prompt(akvq_cache *c, const void *K, const void *V, 
 static akvq_status append_impl(akvq_cache *c, const void *k, const void *v, const uint8_t *types,
                         akvq_stream_t stream) {
   if (!c || !c->base || !k || !v) return AKVQ_EINVAL;
+  if (c->cfg.paged && !c->pool) return AKVQ_ESTATE;   // pages not attached
   const akvq_config &f = c->cfg;
   if (c->L >= f.capacity) return AKVQ_ECAPACITY;
   const DevCache d = make_dev(c);
@@ -512,6 +517,7 @@ size_t akvq_decode_workspace_bytes_max(const akvq_cache *c) {
 static akvq_status decode_impl(const akvq_cache *c, const void *q, float *out, void *ws,
                         size_t ws_bytes, uint32_t flags, akvq_stream_t stream) {
   if (!c || !c->base || !q || !out || !ws) return AKVQ_EINVAL;
+  if (c->cfg.paged && !c->pool) return AKVQ_ESTATE;   // pages not attached
   if (c->L == 0) return AKVQ_ESTATE;
   DecodePlan p = plan_decode(c, c->L, c->n_q);
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
@@ -535,6 +541,7 @@ akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const 
                              const void *q, float *out, void *ws, size_t ws_bytes, uint32_t flags,
                              akvq_stream_t stream) {
   if (!c || !c->base || !k || !v || !q || !out || !ws) return AKVQ_EINVAL;
+  if (c->cfg.paged && !c->pool) return AKVQ_ESTATE;   // pages not attached
   c->launches = 0;
   const akvq_config &f = c->cfg;
   if (c->L >= f.capacity) return AKVQ_ECAPACITY;
@@ -554,6 +561,13 @@ akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const 
   return AKVQ_OK;
 }
 
+akvq_status akvq_cache_attach_pages(akvq_cache *c, void *pool, const int32_t *block_table) {
+  if (!c || !pool || !block_table || !c->cfg.paged) return AKVQ_EINVAL;
+  c->pool = pool;
+  c->block_table = block_table;
+  return AKVQ_OK;
+}
+
 akvq_status akvq_cache_advance(akvq_cache *c, int32_t steps) {
   if (!c || steps < 0) return AKVQ_EINVAL;
   const akvq_config &f = c->cfg;
@@ -566,6 +580,7 @@ akvq_status akvq_cache_advance(akvq_cache *c, int32_t steps) {
 
 akvq_status akvq_dequantize_view(const akvq_cache *c, float *K, float *V, akvq_stream_t stream) {
   if (!c || !c->base || !K || !V) return AKVQ_EINVAL;
+  if (c->cfg.paged && !c->pool) return AKVQ_ESTATE;   // pages not attached
   if (c->L == 0) return AKVQ_ESTATE;
   const DevCache d = make_dev(c);
   return cuda_status(launch_view(d, c->cfg.dtype16, c->L, c->n_q, K, V,

@@ -15,7 +15,8 @@ constexpr float kLog2e = 1.4426950408889634f;
 // Device view of one layer's cache (pointers resolved on the host from
 // akvq_layout; see include/akvq.h for the byte layout).
 struct DevCache {
-  uint8_t *pages;          // [U][n_pages][page_bytes]
+  uint8_t *pages;          // [U][n_pages][page_bytes], or the page pool (paged)
+  const int32_t *btab;     // paged: [U][n_pages] pool page of (unit, page); else null
   uint16_t *ring;          // [U][slots][2][d]
   uint32_t *bitmask;       // [U][bm_words]
   int32_t *side_idx;       // [U][side_cap]
@@ -33,6 +34,7 @@ struct DevCache {
 };
 
 __device__ __forceinline__ uint8_t *page_ptr(const DevCache &c, int u, int p) {
+  if (c.btab) return c.pages + (size_t)__ldg(c.btab + (size_t)u * c.n_pages + p) * c.page_bytes;
   return c.pages + ((size_t)u * c.n_pages + p) * c.page_bytes;
 }
 __device__ __forceinline__ uint16_t *ring_row(const DevCache &c, int u, int slot) {

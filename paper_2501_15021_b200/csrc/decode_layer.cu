@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         next = !ok;
         part_i = ok ? part_i + 1 : 0;
       }
-      const uint8_t *pg = ubase + (size_t)a * c.page_bytes;   // (pages only)
+      const uint8_t *ub = ubase;                  // (pages: the unit before advancing)
       if (next) {
         if (++pj == lp.per_u) {
           pj = 0;
@@ -211,6 +211,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       if (ok) {
         eu = sb.u;
         if (sb.kind == 0) {
+          const uint8_t *pg = c.btab ? c.pages + (size_t)__ldg(c.btab + (size_t)sb.pu * c.n_pages + sb.a) * c.page_bytes
+                                     : ub + (size_t)sb.a * c.page_bytes;
           if (lane == 0) {
             mbar_expect_tx(&bar[st], kbytes);
             bulk_g2s(dst, pg, kbytes, &bar[st]);

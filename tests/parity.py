@@ -69,7 +69,11 @@ class GpuState:
         U, d, G = cfg.n_units, cfg.head_dim, cfg.group
         ng, npg, pb = y.ng, y.n_pages, int(y.page_bytes)
         self.L, self.n_q = lc.L, lc.n_q
-        pages = raw[y.pages_off: y.pages_off + U * npg * pb].reshape(U, npg, pb)
+        if getattr(cfg, "paged", 0):            # pages through the block table
+            pool = lc.pool.buf.cpu().numpy().reshape(-1, pb)
+            pages = pool[lc.block_table.cpu().numpy().reshape(-1)].reshape(U, npg, pb)
+        else:
+            pages = raw[y.pages_off: y.pages_off + U * npg * pb].reshape(U, npg, pb)
 
         def pg(off, nbytes, dt):
             return np.ascontiguousarray(pages[:, :, off: off + nbytes]).view(dt)

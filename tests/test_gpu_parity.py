@@ -51,7 +51,7 @@ def _configs(ak, orc, w, layer, units_n, kind=None, cap=None, k_axis=0, decide64
 
 def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every=1,
               flags=0, report=None, options=0, fused_step=None, k_axis=0,
-              xf_layer=None, xf_decode=None, case=None):
+              xf_layer=None, xf_decode=None, case=None, paged=None):
     """Prefill + `steps` decode steps on the GPU for all units; the oracle runs the
     sampled `units` (default all) in BOTH decision precisions: fp64 (SURVEY 8(c),
     the contract) and fp32 (R6, the kernel's).  The cache state is compared with
@@ -73,7 +73,11 @@ def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every
     inp = sy.layer_inputs(w, layer, device=dev)
     if xf_layer:
         inp = xf_layer(inp)
-    lc = ak.LayerCache(gcfg, options=options)
+    if paged is not None:                 # pages scattered over a shared pool (NEXT-4)
+        gcfg.paged = 1
+        lc = ak.LayerCache(gcfg, options=options, pool=paged, shuffle_seed=layer + 17)
+    else:
+        lc = ak.LayerCache(gcfg, options=options)
     lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
     inp_o = sy.layer_inputs(w, layer, units=us, device="cpu")
     if xf_layer:
@@ -607,3 +611,28 @@ def test_cuda_graph_replay(ak, orc, sy, name, layer):
     do = sy.decode_inputs(w, layer, step0 + nsteps, units=us, device="cpu")
     oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
     assert np.abs(o2[us].double().cpu().numpy() - oc.decode(f16_bits(do["q"]))).max() <= OUT_TOL
+
+
+@pytest.mark.parametrize("name,layer", [("tiny", 0), ("llava7b", 0), ("llava7b", 2), ("qwen_gqa", 3)])
+def test_paged_block_table(ak, orc, sy, name, layer):
+    """Paged caches (akvq_config.paged, NEXT-4): pages come from a shared pool in a
+    shuffled order through the block table -- two caches share the pool (the
+    second one reserves pages in between) and both match the oracle across a
+    flush, fused and split steps alike."""
+    w = sy.get(name)
+    dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
+    cfg = ak.make_config(w.U, w.g, w.d, w.G, w.R, w.capacity, w.top_k, w.kind(layer), dt,
+                         paged=1)
+    y = ak.akvq_cache_layout(cfg)
+    pool = ak.PagePool(2 * w.U * y.n_pages + 7, y.page_bytes)
+    other = ak.LayerCache(cfg, pool=pool, shuffle_seed=3)        # interleaved owner
+    units = None if w.U <= 32 else [0, w.U // 2, w.U - 1]
+    steps = 16 if name == "tiny" else 3
+    _run_case(ak, orc, sy, w, layer, steps=steps, units=units, paged=pool)
+    other.release_pages()
+    with pytest.raises(ak.AkvqError) as e:                      # not attached -> ESTATE
+        c = ak.akvq_cache()
+        ak.akvq_cache_init(c, cfg, torch.empty(y.total_bytes, dtype=torch.uint8, device="cuda"))
+        ak.akvq_rotate_quantize(c, torch.zeros((w.U, 1, w.d), dtype=torch.bfloat16, device="cuda"),
+                                torch.zeros((w.U, 1, w.d), dtype=torch.bfloat16, device="cuda"), 1)
+    assert e.value.status == ak.AKVQ_ESTATE
