@@ -146,8 +146,11 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
   p.fast = 0;
   memset(&p.lp, 0, offsetof(LayerPlan, tab));
   p.lp.per_u = 1;
+  // (the single-pass GQA kernel has no per-token-K variant: the generic kernels
+  // serve that combination)
   if (!(c->options & AKVQ_OPT_GENERIC_PAGES) &&
-      layer_supported(f.head_dim, f.group, f.q_per_kv)) {
+      layer_supported(f.head_dim, f.group, f.q_per_kv) &&
+      !(layer_uses_gqa(f.q_per_kv) && f.k_axis == AKVQ_K_PER_TOKEN)) {
     p.fast = 1;
     LayerPlan &lp = p.lp;
     const int rows = layer_rows_per_chunk();

@@ -636,3 +636,12 @@ def test_paged_block_table(ak, orc, sy, name, layer):
         ak.akvq_rotate_quantize(c, torch.zeros((w.U, 1, w.d), dtype=torch.bfloat16, device="cuda"),
                                 torch.zeros((w.U, 1, w.d), dtype=torch.bfloat16, device="cuda"), 1)
     assert e.value.status == ak.AKVQ_ESTATE
+
+
+@pytest.mark.parametrize("g", [3, 7])
+def test_gqa_per_token_k(ak, orc, sy, g):
+    """Per-token K (NEXT-1) with g >= 3 query heads per kv head runs on the generic
+    split kernels (the single-pass GQA kernel is per-channel only)."""
+    import dataclasses
+    w = dataclasses.replace(sy.TINY, name=f"tiny_kt_g{g}", hq=4 * g, hkv=4)
+    _run_case(ak, orc, sy, w, 0, kind=1, steps=12, k_axis=1)

@@ -10,6 +10,13 @@ Reports cosine similarity and relative L2 error per layer kind (mean / min
 over sampled units and steps).  Product path only (no oracle): this measures the
 METHOD's approximation, not kernel parity (that is tests/test_gpu_parity.py).
 
+WHT arms (the paper's "+ WHT" ablation row, Table III; motivation
+P:305-308): "on" is the library as is.  "off" feeds every row already
+multiplied by H (K.H, V.H, q.H): the library's own rotation then gives
+K.H.H = K (H is an involution), so the cache quantizes the UNROTATED channels,
+while attention is unchanged (H orthonormal); outputs are compared with plain
+attention over the same fed rows.
+
     python tools/quality_report.py [--workload llava7b] [--steps 8] [--units 64]
 """
 import argparse
@@ -31,18 +38,27 @@ def reference(Kall, Vall, q):
     return torch.einsum("ngl,nld->ngd", torch.softmax(s, -1), Vall)
 
 
-def run(w, layer, k_axis, steps, units):
+def run(w, layer, k_axis, steps, units, wht=True):
     dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
     cfg = ak.make_config(w.U, w.g, w.d, w.G, w.R, w.L0 + steps, w.top_k, w.kind(layer), dt,
                          w.clip2, w.clip4, k_axis)
     lc = ak.LayerCache(cfg)
     inp = synth.layer_inputs(w, layer, device="cuda")
+    tdt = inp["K"].dtype
+    if not wht:
+        import scipy.linalg
+        H = torch.tensor(scipy.linalg.hadamard(w.d) / w.d ** 0.5, dtype=torch.float32, device="cuda")
+        pre = lambda x: (x.float() @ H).to(tdt)
+        inp = dict(inp, K=pre(inp["K"]), V=pre(inp["V"]))
+    else:
+        pre = lambda x: x
     lc.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
     Kall = inp["K"][units].double().cpu()
     Vall = inp["V"][units].double().cpu()
     cos, rel = [], []
     for s in range(steps):
         di = synth.decode_inputs(w, layer, s, device="cuda")
+        di = dict(di, k=pre(di["k"]), v=pre(di["v"]), q=pre(di["q"]))
         out = lc.step(di["k"], di["v"], di["q"], di["types"])[units].double().cpu()
         Kall = torch.cat([Kall, di["k"][units].double().cpu()[:, None]], 1)
         Vall = torch.cat([Vall, di["v"][units].double().cpu()[:, None]], 1)
@@ -66,15 +82,17 @@ def main():
     tsa = next((l for l in range(w.n_layers) if w.kind(l) == 0), None)
     rows = []
     for layer in [l for l in (tsa, psa) if l is not None]:
-        for k_axis, name in ((0, "per-channel K (R1)"), (1, "per-token K (P:246)")):
-            r = run(w, layer, k_axis, a.steps, units)
-            r.update(layer=layer, kind="TSA" if w.kind(layer) == 0 else "PSA", k_axis=name)
-            rows.append(r)
-            print(json.dumps(r), flush=True)
-    print("\n| layer | kind | K axis | cos mean | cos min | rel L2 mean | rel L2 max |")
-    print("|---|---|---|---|---|---|---|")
+        for wht in (True, False):
+            for k_axis, name in ((0, "per-channel K (R1)"), (1, "per-token K (P:246)")):
+                r = run(w, layer, k_axis, a.steps, units, wht)
+                r.update(layer=layer, kind="TSA" if w.kind(layer) == 0 else "PSA", k_axis=name,
+                         wht="on" if wht else "off")
+                rows.append(r)
+                print(json.dumps(r), flush=True)
+    print("\n| layer | kind | WHT | K axis | cos mean | cos min | rel L2 mean | rel L2 max |")
+    print("|---|---|---|---|---|---|---|---|")
     for r in rows:
-        print(f"| {r['layer']} | {r['kind']} | {r['k_axis']} | {r['cos_mean']:.5f} | "
+        print(f"| {r['layer']} | {r['kind']} | {r['wht']} | {r['k_axis']} | {r['cos_mean']:.5f} | "
               f"{r['cos_min']:.5f} | {r['rel_l2_mean']:.4f} | {r['rel_l2_max']:.4f} |")
 
 
