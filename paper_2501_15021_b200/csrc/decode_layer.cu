@@ -75,7 +75,7 @@ struct LySmem {
   }
 };
 
-template <int D, int G, int DT, int NH, bool TSA, int KM>
+template <int D, int G, int DT, int NH, bool TSA, int KM, bool DL>
 __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     k_decode_layer(const __grid_constant__ DevCache c, const __grid_constant__ LayerPlan lp, const uint16_t *__restrict__ q,
                    const uint16_t *__restrict__ app_k, const uint16_t *__restrict__ app_v,
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ unsigned cta_done;                 // warps of this CTA done (ly_exit)
-  if (lp.dev_L) {                               // (uniform: the barrier is legal)
+  if constexpr (DL) {                           // DEVICE_L: per-CTA exit count
     if (threadIdx.x == 0) cta_done = 0u;
     __syncthreads();
   }
@@ -116,13 +116,13 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     pdl_launch_dependents();                    // the next layer's kernel may queue up
   }
   const int gw = blockIdx.x * kLyWarps + warp;
-  if (gw >= lp.W) { ly_exit(c, lp, lane, &cta_done); return; }
+  if (gw >= lp.W) { if constexpr (DL) ly_exit(c, lp, lane, &cta_done); return; }
   const int ib = ly_first_item(lp, gw);
   const int ie = gw + 1 < lp.W ? ly_first_item(lp, gw + 1) : lp.T;
-  if (ib >= ie) { ly_exit(c, lp, lane, &cta_done); return; }
+  if (ib >= ie) { if constexpr (DL) ly_exit(c, lp, lane, &cta_done); return; }
   // this launch's token count, the new token included when it appends (DEVICE_L
   // launches have no prologue: the griddepcontrol.wait above has been passed)
-  const int Lc = lp.dev_L ? c.dstate->L + (lp.appends ? 1 : 0) : lp.L;
+  const int Lc = DL ? c.dstate->L + (lp.appends ? 1 : 0) : lp.L;
   constexpr bool tsa = TSA;                     // layer kind (Table I): TSA has 4-bit text rows
   // GQA (NEXT-3): a unit's g query heads are processed in HG groups of NH heads;
   // work items, partials and tickets are per virtual unit vu = u * HG + group
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         sb.kind = 0; sb.n = 0;
       } else if (kind == 2) {                     // ring chunk (rows n of it)
         sb.kind = 2; sb.ring = 1; sb.n = n;
-        if (lp.dev_L) {                           // chunks of the period past L: skip
+        if constexpr (DL) {                       // chunks of the period past L: skip
           sb.n = min(n, Lc - lp.n_q - a);
           ok = sb.n > 0;
         }
@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     pdl_launch_dependents();
   }
   // host-L mode: keep the device copy current (a later DEVICE_L launch reads it)
-  if (!lp.dev_L && lp.appends && blockIdx.x == 0 && threadIdx.x == 0) c.dstate->L = lp.L;
+  if constexpr (!DL)
+    if (lp.appends && blockIdx.x == 0 && threadIdx.x == 0) c.dstate->L = lp.L;
 
   // lane roles
   const int ktq = lane % TQ, kcs = lane / TQ;         // page K phase
@@ -888,7 +889,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   }
   if constexpr (!SO)
     if (cur_u >= 0) flush(cur_u);
-  ly_exit(c, lp, lane, &cta_done);
+  if constexpr (DL) ly_exit(c, lp, lane, &cta_done);
 }
 
 template <int D, int G, int NH>
@@ -902,11 +903,14 @@ static cudaError_t launch_ly(const DevCache &c, const LayerPlan &lp, const void 
                              uint32_t flags, cudaStream_t st) {
   const size_t smem = ly_smem<D, G, NH>(c);
   const int km = c.k_axis == AKVQ_K_PER_TOKEN ? 1 : 0;
-  auto kern = c.kind == AKVQ_TSA ? (km ? k_decode_layer<D, G, DT, NH, true, 1> : k_decode_layer<D, G, DT, NH, true, 0>)
-                                 : (km ? k_decode_layer<D, G, DT, NH, false, 1> : k_decode_layer<D, G, DT, NH, false, 0>);
+  auto kern = lp.dev_L
+      ? (c.kind == AKVQ_TSA ? (km ? k_decode_layer<D, G, DT, NH, true, 1, true> : k_decode_layer<D, G, DT, NH, true, 0, true>)
+                            : (km ? k_decode_layer<D, G, DT, NH, false, 1, true> : k_decode_layer<D, G, DT, NH, false, 0, true>))
+      : (c.kind == AKVQ_TSA ? (km ? k_decode_layer<D, G, DT, NH, true, 1, false> : k_decode_layer<D, G, DT, NH, true, 0, false>)
+                            : (km ? k_decode_layer<D, G, DT, NH, false, 1, false> : k_decode_layer<D, G, DT, NH, false, 0, false>));
   if (lp.stream_only) {                      // profiling variant: single-head MHA caches only
     if constexpr (NH == 1)
-      kern = c.kind == AKVQ_TSA ? k_decode_layer<D, G, DT, NH, true, 2> : k_decode_layer<D, G, DT, NH, false, 2>;
+      kern = c.kind == AKVQ_TSA ? k_decode_layer<D, G, DT, NH, true, 2, false> : k_decode_layer<D, G, DT, NH, false, 2, false>;
     else
       return cudaErrorNotSupported;
   }
