@@ -899,7 +899,10 @@ static cudaError_t launch_gq(const DevCache &c, const LayerPlan &lp, const void 
                             (const uint16_t *)v, types, part, out, flags);
 }
 
-int gqa_heads(int g) { return g <= 4 ? 4 : 8; }
+#ifndef AKVQ_GQ_MAXH
+#define AKVQ_GQ_MAXH 8
+#endif
+int gqa_heads(int g) { return g <= 4 ? 4 : AKVQ_GQ_MAXH; }
 int gqa_warps_per_cta() { return kGqWarps; }
 int gqa_ctas_per_sm() { return AKVQ_GQ_CTAS; }
 size_t gqa_record_floats(int d) { return (size_t)d + 4; }

@@ -645,3 +645,89 @@ def test_gqa_per_token_k(ak, orc, sy, g):
     import dataclasses
     w = dataclasses.replace(sy.TINY, name=f"tiny_kt_g{g}", hq=4 * g, hkv=4)
     _run_case(ak, orc, sy, w, 0, kind=1, steps=12, k_axis=1)
+
+
+# ------------------------------------------------- sharding equivalence
+_STATE_FIELDS = ("kscale", "kzero", "kcodes", "vscale", "vzero", "vcodes", "ring", "salient",
+                 "side_idx", "side_cnt")
+_SIDE_FIELDS = {1: ("side16",), 0: ("side4_kscale", "side4_kzero", "side4_vscale", "side4_vzero",
+                                     "side4_k", "side4_v")}
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("layer", [2, 0], ids=["PSA-L2", "TSA-L0"])
+def test_sharding_equivalence(ak, orc, sy, world, layer):
+    """SURVEY 8(e) on one GPU: every rank's unit range (shard.unit_range, b-major
+    batch x kv-head units) run as its own cache -- the per-rank shape a world-N
+    job runs -- gives the same cache state bit for bit and the same outputs (within
+    1e-5; the only difference is the item split across warps, i.e. the order of the
+    segment merge) as the unsharded cache, across a flush; the first unit of every
+    rank is also checked against the oracle (2e-3).  sweep@b16 shape (BJ:9)."""
+    from paper_2501_15021_b200 import shard
+    w = sy.get("sweep@b16")
+    U = w.U
+    steps = 4
+    gcfg, _ = _configs(ak, orc, w, layer, U)
+    inp = sy.layer_inputs(w, layer, device="cuda")
+    full = ak.LayerCache(gcfg)
+    full.prefill(inp["K"], inp["V"], inp["types"], inp["colsum"])
+    shards = []
+    for r in range(world):
+        lo, hi = shard.unit_range(U, world, r)
+        cfg_r, _ = _configs(ak, orc, w, layer, hi - lo)
+        lc = ak.LayerCache(cfg_r)
+        lc.prefill(inp["K"][lo:hi], inp["V"][lo:hi], inp["types"][lo:hi], inp["colsum"][lo:hi])
+        shards.append((lo, hi, lc))
+    firsts = [lo for lo, _, _ in shards]
+    _, ocfg = _configs(ak, orc, w, layer, len(firsts))
+    oc = orc.OracleCache(ocfg)
+    io = sy.layer_inputs(w, layer, units=firsts, device="cpu")
+    assert oc.prefill(f16_bits(io["K"]), f16_bits(io["V"]), io["types"].numpy(),
+                      io["colsum"].numpy()) == 0
+
+    def same_state():
+        gs = GpuState(full)
+        for lo, hi, lc in shards:
+            s = GpuState(lc)
+            assert (s.L, s.n_q) == (gs.L, gs.n_q)
+            assert np.array_equal(gs.side_cnt[lo:hi], s.side_cnt)
+            sc = int(s.side_cnt.max(initial=0))
+            for f in _STATE_FIELDS + _SIDE_FIELDS[gcfg.kind]:
+                a, b = getattr(gs, f)[lo:hi], getattr(s, f)
+                # live regions only: pages / token rows below n_q, ring rows
+                # [n_q, L), bits below L, side entries below the largest count
+                n = {"kscale": s.n_q // w.G, "kzero": s.n_q // w.G, "ring": s.L - s.n_q,
+                     "salient": s.L}.get(f, sc if f.startswith("side") and f != "side_cnt" else s.n_q)
+                if f == "ring":                                   # slot of token t: t % slots
+                    live = np.arange(s.n_q, s.L) % s.ring.shape[1]
+                    a, b = a[:, live], b[:, live]
+                elif f != "side_cnt":
+                    a, b = a[:, :n], b[:, :n]
+                if f.startswith("side") and f != "side_cnt":     # per-unit counts
+                    keep = np.arange(n)[None, :] < s.side_cnt[:, None]
+                    a, b = a[keep], b[keep]
+                assert np.array_equal(np.ascontiguousarray(a).view(np.uint8),
+                                      np.ascontiguousarray(b).view(np.uint8)), f"{f} differs on [{lo},{hi})"
+
+    same_state()
+    # step past the next flush (n_q + G + R - L steps, Eq. 2 / R4 schedule)
+    nq_start = full.n_q
+    steps = max(steps, nq_start + w.G + w.R - full.L + 2)
+    worst_shard, worst_orc = 0.0, 0.0
+    for step in range(steps):
+        di = sy.decode_inputs(w, layer, step, device="cuda")
+        nq0 = full.n_q
+        out = full.step(di["k"], di["v"], di["q"], di["types"]).clone()
+        do = sy.decode_inputs(w, layer, step, units=firsts, device="cpu")
+        oc.append(f16_bits(do["k"]), f16_bits(do["v"]), do["types"].numpy())
+        ref = oc.decode(f16_bits(do["q"]))
+        for j, (lo, hi, lc) in enumerate(shards):
+            o = lc.step(di["k"][lo:hi], di["v"][lo:hi], di["q"][lo:hi], di["types"][lo:hi])
+            worst_shard = max(worst_shard, float((o - out[lo:hi]).abs().max()))
+            worst_orc = max(worst_orc, float(np.abs(o[0].double().cpu().numpy() - ref[j]).max()))
+        if full.n_q != nq0:
+            same_state()
+    record_margin(_case_name(), worst_shard, 1e-5, None, worst_out_err_oracle=worst_orc)
+    assert full.n_q > nq_start, "no flush exercised"
+    assert worst_shard <= 1e-5, worst_shard
+    assert worst_orc <= OUT_TOL, worst_orc

@@ -20,7 +20,8 @@ def one(spec):
     for s in b.SOURCES:
         o = os.path.join(b.BUILD, s.replace(".cu", ".o"))
         api_only = "AKVQ_C" in flags and "AKVQ_MAX_TAB" not in flags
-        if (s == "decode_layer.cu" and not api_only) or (s == "api.cu" and ("AKVQ_MAX_TAB" in flags or api_only)):
+        if (s == "decode_layer.cu" and not api_only) or (s == "api.cu" and ("AKVQ_MAX_TAB" in flags or api_only)) \
+                or (s == "decode_gqa.cu" and "AKVQ_GQ" in flags):
             o = os.path.join(out, s.replace(".cu", ".o"))
             subprocess.run([b.NVCC, *b.FLAGS, *flags.split(), "-c", os.path.join(b.CSRC, s), "-o", o], check=True)
         objs.append(o)
