@@ -8,7 +8,8 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > $OUT/smi.txt 2>&1
 for w in $WHAT; do
   case $w in
-    tests)  timeout -k 10 1800 python -m pytest tests -m gpu -q -rf --timeout 400 -o timeout_method=thread > $OUT/tests.log 2>&1; echo "tests rc=$?" ;;
+    tests)  AKVQ_MARGINS_OUT=$OUT/parity_margins.json timeout -k 10 1800 python -m pytest tests -m gpu -q -rf --timeout 400 -o timeout_method=thread > $OUT/tests.log 2>&1; echo "tests rc=$?" ;;
+    shapes) bash tools/gpu_shapes.sh $TAG/shapes ;;
     smoke)  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" ;;
     bench)  timeout -k 10 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; cat $OUT/bench.json ;;
     launches) timeout -k 10 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
