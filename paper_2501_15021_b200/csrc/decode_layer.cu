@@ -297,6 +297,10 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   // qinv = q~ * inv for the lane's channel quad; dA = alpha_k / inv.  V weights:
   // W_t = rn(p_t s^V_t winv) with winv = kQMax / umax.V (p <= 1), dw = 1 / winv.
   float qinv[NH][4], dAu[NH], winv = 0.f, dwu = 0.f;
+  // per-token K (KT): this lane's delta and limb sums, fixed per unit
+  float kt_d = 0.f, kt_s[2][NG];
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) { kt_s[0][gi] = 0.f; kt_s[1][gi] = 0.f; }
   float lg[NH][4];                                    // page logits of the lane's token quad
   int cur_u = -1, cur_pu = 0, cur_hg = 0;      // virtual unit, its physical unit and head group
   const int u_first = ib / lp.per_u;
@@ -425,6 +429,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
 
   int st = 0;
   uint32_t par = 0;
+  bool unit_fresh = false;                          // KT: q limbs of the new unit pending
   for (;;) {
     const LySub s = unpack_sub(st ? dsc1 : dsc0);
     if (s.kind < 0) break;
@@ -439,6 +444,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     if (s.u != cur_u) {
       if (cur_u >= 0) flush(cur_u);
       cur_u = s.u;
+      unit_fresh = true;
       cur_pu = s.u / HG;
       cur_hg = s.u - cur_pu * HG;
       // q~ = q . H_s (unnormalized FWHT: in-register then shuffle butterflies)
@@ -494,6 +500,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           const float um_v = c.umax[cur_pu].y;
           winv = um_v > 0.f ? __fdividef((float)kQMax, um_v) : 0.f;
           dwu = um_v * (1.0f / (float)kQMax);
+          qinv[h][0] = t4.x; qinv[h][1] = t4.y; qinv[h][2] = t4.z; qinv[h][3] = t4.w;   // q~ (KT)
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) { qk[h][k] *= alpha_o; o_rot[h][k] = 0.f; o_org[h][k] = 0.f; }
@@ -504,36 +511,27 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       }
     }
 
-    if (s.kind == 0) {
-      // ================= page K half: logits of the page's G tokens
-      const uint32_t sbits = ((st ? bits1 : bits0) >> (4 * (ktq & 7))) & 15u;
-      mbar_wait(&bar[st], par);
-      const float4 *ks4 = reinterpret_cast<const float4 *>(B + c.pg_kscale);
-      const int4 *kz4 = reinterpret_cast<const int4 *>(B + c.pg_kzero);
-      if constexpr (KT) {                      // per-token K variant (compile time)
-        // ---- per-token K (NEXT-1): Q_c = rn(q~_c / delta) once per page,
-        // logit_t = alpha delta sum_g s_tg sum_k 256^k (C_k,tg - z_tg SQ_k,g) with
-        // C_k,tg = sum_{c in g} limb_k,c code_tc (the warp MMA, folded per
-        // channel group: a 32-channel chunk lies in one group since G >= 32) and
-        // SQ_k,g = sum_{c in g} limb_k,c
-        const float *ksT = reinterpret_cast<const float *>(B + c.pg_kscale);    // [G][NG]
-        const int32_t *kzT = reinterpret_cast<const int32_t *>(B + c.pg_kzero);
-        float dT[NH], sqg[NH][2][NG];            // per head: delta; this lane's limb sums
+    if constexpr (KT) {
+      if (unit_fresh) {
+        // ---- per-token K (NEXT-1): Q_c = rn(q~_c / delta) once per unit
+        // (it does not depend on the page); the limb words replace q~ in qh (KT
+        // reads q~ only here), the page loop reloads them as B fragments.
+        // SQ_k,g = sum_{c in g} limb_k,c for the zero-point term.
+        unit_fresh = false;
+        __syncwarp();                            // every lane has read its q~ quad
+        uint32_t *ql = reinterpret_cast<uint32_t *>(qh);
+        float dT[NH], sqg[NH][2][NG];
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-          float qv4[4] = {0.f, 0.f, 0.f, 0.f}, am = 0.f;
-          if (lane < CQ) {
-            const float4 qv = reinterpret_cast<const float4 *>(qh + h * D)[lane];
-            qv4[0] = qv.x; qv4[1] = qv.y; qv4[2] = qv.z; qv4[3] = qv.w;
-            am = fmaxf(fmaxf(fabsf(qv.x), fabsf(qv.y)), fmaxf(fabsf(qv.z), fabsf(qv.w)));
-          }
+          const bool in = lane < CQ;
+          const float am = in ? fmaxf(fmaxf(fabsf(qinv[h][0]), fabsf(qinv[h][1])),
+                                      fmaxf(fabsf(qinv[h][2]), fabsf(qinv[h][3]))) : 0.f;
           const float M = warp_max(am);
           const float inv = M > 0.f ? __fdividef((float)kQMax, M) : 0.f;
           dT[h] = alpha_k * M * (1.0f / (float)kQMax);
           uint32_t x[4];
 #pragma unroll
-          for (int b = 0; b < 4; ++b) x[b] = (uint32_t)__float2int_rn(qv4[b] * inv) + kQOff;
-          // SQ_k,g over channel group g (lanes g*G/4 .. (g+1)*G/4 - 1), k = 0..2
+          for (int b = 0; b < 4; ++b) x[b] = (uint32_t)__float2int_rn(in ? qinv[h][b] * inv : 0.f) + kQOff;
           int sq[3];
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
@@ -552,32 +550,53 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
             sqg[h][0][gi] = rodd ? s2 : s0;
             sqg[h][1][gi] = rodd ? 0.f : s1;
           }
-          if (lane < CQ) {
-            qlimb[(4 * h) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0040), prmt(x[2], x[3], 0x0040), 0x5410) ^ 0x80808080u;
-            qlimb[(4 * h + 1) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0051), prmt(x[2], x[3], 0x0051), 0x5410) ^ 0x80808080u;
-            qlimb[(4 * h + 2) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0062), prmt(x[2], x[3], 0x0062), 0x5410) ^ 0x80808080u;
+          __syncwarp();
+          if (in) {
+            ql[(4 * h) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0040), prmt(x[2], x[3], 0x0040), 0x5410) ^ 0x80808080u;
+            ql[(4 * h + 1) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0051), prmt(x[2], x[3], 0x0051), 0x5410) ^ 0x80808080u;
+            ql[(4 * h + 2) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0062), prmt(x[2], x[3], 0x0062), 0x5410) ^ 0x80808080u;
           }
         }
-        __syncwarp();
-        constexpr int KC = D / 32, CPG = G / 32;     // chunks, chunks per channel group
-        uint32_t bq[KC][2];
-#pragma unroll
-        for (int cc = 0; cc < KC; ++cc) {
-          const uint2 b = *reinterpret_cast<const uint2 *>(qlimb + mcol * CQ + 8 * cc + 2 * mt);
-          bq[cc][0] = b.x;
-          bq[cc][1] = b.y;
-        }
         const int hsel = min(rhead, NH - 1);
-        float dsel = dT[0], ssel[2][NG];
+        kt_d = dT[0];
 #pragma unroll
-        for (int gi = 0; gi < NG; ++gi) { ssel[0][gi] = sqg[0][0][gi]; ssel[1][gi] = sqg[0][1][gi]; }
+        for (int gi = 0; gi < NG; ++gi) { kt_s[0][gi] = sqg[0][0][gi]; kt_s[1][gi] = sqg[0][1][gi]; }
 #pragma unroll
         for (int h = 1; h < NH; ++h)
           if (hsel == h) {
-            dsel = dT[h];
+            kt_d = dT[h];
 #pragma unroll
-            for (int gi = 0; gi < NG; ++gi) { ssel[0][gi] = sqg[h][0][gi]; ssel[1][gi] = sqg[h][1][gi]; }
+            for (int gi = 0; gi < NG; ++gi) { kt_s[0][gi] = sqg[h][0][gi]; kt_s[1][gi] = sqg[h][1][gi]; }
           }
+        __syncwarp();
+      }
+    }
+
+    if (s.kind == 0) {
+      // ================= page K half: logits of the page's G tokens
+      const uint32_t sbits = ((st ? bits1 : bits0) >> (4 * (ktq & 7))) & 15u;
+      mbar_wait(&bar[st], par);
+      const float4 *ks4 = reinterpret_cast<const float4 *>(B + c.pg_kscale);
+      const int4 *kz4 = reinterpret_cast<const int4 *>(B + c.pg_kzero);
+      if constexpr (KT) {                      // per-token K variant (compile time)
+        // ---- per-token K (NEXT-1): Q_c = rn(q~_c / delta) (once per unit),
+        // logit_t = alpha delta sum_g s_tg sum_k 256^k (C_k,tg - z_tg SQ_k,g) with
+        // C_k,tg = sum_{c in g} limb_k,c code_tc (the warp MMA, folded per
+        // channel group: a 32-channel chunk lies in one group since G >= 32) and
+        // SQ_k,g = sum_{c in g} limb_k,c
+        const float *ksT = reinterpret_cast<const float *>(B + c.pg_kscale);    // [G][NG]
+        const int32_t *kzT = reinterpret_cast<const int32_t *>(B + c.pg_kzero);
+        constexpr int KC = D / 32, CPG = G / 32;     // chunks, chunks per channel group
+        const uint32_t *ql = reinterpret_cast<const uint32_t *>(qh);   // q limbs (unit switch)
+        uint32_t bq[KC][2];
+#pragma unroll
+        for (int cc = 0; cc < KC; ++cc) {
+          const uint2 b = *reinterpret_cast<const uint2 *>(ql + mcol * CQ + 8 * cc + 2 * mt);
+          bq[cc][0] = b.x;
+          bq[cc][1] = b.y;
+        }
+        const float dsel = kt_d;
+        const float (&ssel)[2][NG] = kt_s;
         // even lanes: limbs 0 (x 1) and 1 (x 256); odd lanes: limb 2 (x 65536)
         const float wA = rodd ? 65536.f : 1.f, wB = rodd ? 0.f : 256.f;
         const uint32_t *kcw = reinterpret_cast<const uint32_t *>(B + c.pg_kcodes);
