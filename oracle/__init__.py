@@ -46,7 +46,8 @@ class _Cfg(C.Structure):
     _fields_ = [("U", C.c_int), ("g", C.c_int), ("d", C.c_int), ("G", C.c_int),
                 ("R", C.c_int), ("capacity", C.c_int), ("top_k", C.c_int),
                 ("kind", C.c_int), ("dtype16", C.c_int), ("clip2", C.c_float),
-                ("clip4", C.c_float), ("k_axis", C.c_int), ("decide64", C.c_int)]
+                ("clip4", C.c_float), ("k_axis", C.c_int), ("decide64", C.c_int),
+                ("exact_r", C.c_int)]
 
 
 class _Export(C.Structure):
@@ -207,6 +208,7 @@ class OracleConfig:
     clip4: float = 1.0
     k_axis: int = 0          # 0 per channel (R1), 1 per token (NEXT-1)
     decide64: int = 1        # quantizer decisions in fp64; 0: fp32 (R6)
+    exact_r: int = 0         # per-token K: exactly R tokens stay 16-bit (R26)
 
 
 class OracleCache:
@@ -215,7 +217,7 @@ class OracleCache:
     def __init__(self, cfg: OracleConfig):
         self.cfg = cfg
         c = _Cfg(cfg.U, cfg.g, cfg.d, cfg.G, cfg.R, cfg.capacity, cfg.top_k, cfg.kind,
-                 cfg.dtype16, cfg.clip2, cfg.clip4, cfg.k_axis, cfg.decide64)
+                 cfg.dtype16, cfg.clip2, cfg.clip4, cfg.k_axis, cfg.decide64, cfg.exact_r)
         st = C.c_int(0)
         self._h = lib().orc_new(C.byref(c), C.byref(st))
         if not self._h:

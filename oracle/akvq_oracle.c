@@ -377,7 +377,8 @@ orc_cache *orc_new(const orc_config *cfg, int *status) {
       !(cfg->clip4 > 0.0f && cfg->clip4 <= 1.0f) ||
       (cfg->kind != ORC_TSA && cfg->kind != ORC_PSA) ||
       (cfg->k_axis != 0 && cfg->k_axis != 1) ||
-      (cfg->decide64 != 0 && cfg->decide64 != 1)) {
+      (cfg->decide64 != 0 && cfg->decide64 != 1) ||
+      (cfg->exact_r != 0 && cfg->exact_r != 1) || (cfg->exact_r && cfg->k_axis != 1)) {
     if (status) *status = ORC_EINVAL;
     return NULL;
   }
@@ -516,6 +517,47 @@ static void quantize_block(orc_cache *c, int u, int j) {
   }
 }
 
+/* One token leaving the window under the exact-R schedule (R26; per-token */
+/* K only): the per-token steps of quantize_block for token t alone --     */
+/* K and V per token over G-channel groups (Eqs. 3-6, clip2), salient ->   */
+/* codes 0 and meta (0, 0) plus the side entry (TSA: 4-bit rows, clip4).    */
+static void quantize_token(orc_cache *c, int u, int t) {
+  const int d = c->cfg.d, G = c->cfg.G, ng = d / G, D64 = c->cfg.decide64;
+  const int sal = c->sal[(long)u * c->cap + t];
+  rotate_row(c, c->K + ROW(c, u, t), c->xk + ROW(c, u, t));
+  rotate_row(c, c->V + ROW(c, u, t), c->xv + ROW(c, u, t));
+  const long m = ((long)u * c->cap + t) * ng;
+  for (int kv = 0; kv < 2; ++kv) {
+    double *sc = kv ? c->vs : c->ks, *zp = kv ? c->vzp : c->kzp;
+    int32_t *z = kv ? c->vz : c->kz;
+    uint8_t *codes = (kv ? c->vc : c->kc) + ROW(c, u, t);
+    const double *x = (kv ? c->xv : c->xk) + ROW(c, u, t);
+    for (int gi = 0; gi < ng; ++gi) {
+      if (sal) {
+        sc[m + gi] = 0.0; z[m + gi] = 0; zp[m + gi] = NAN;
+        memset(codes + gi * G, 0, (size_t)G);
+      } else {
+        qgroup(D64, x + gi * G, NULL, G, 1, 2, c->cfg.clip2, &sc[m + gi], &z[m + gi],
+               &zp[m + gi], codes + gi * G, 1);
+      }
+    }
+  }
+  if (!sal) return;
+  const int e = c->side_cnt[u]++;
+  c->side_idx[(long)u * c->side_cap + e] = t;
+  c->side_pos[(long)u * c->cap + t] = e;
+  if (c->cfg.kind == ORC_TSA) {
+    for (int kv = 0; kv < 2; ++kv) {
+      const double *x = (kv == 0 ? c->xk : c->xv) + ROW(c, u, t);
+      const long base = (((long)u * c->side_cap + e) * 2 + kv);
+      for (int gi = 0; gi < ng; ++gi)
+        qgroup(D64, x + gi * G, NULL, G, 1, 4, c->cfg.clip4,
+               &c->s4s[base * ng + gi], &c->s4z[base * ng + gi], &c->s4zp[base * ng + gi],
+               c->s4c + base * d + gi * G, 1);
+    }
+  }
+}
+
 /* Prefill: store rows, select salient tokens,     */
 /* quantize blocks [0, n_q) with n_q = G floor(max(0, L0 - R)/G) (R9).    */
 /* mask != NULL (PSA with explicit pivots, NEXT-2): salient = mask[u][t]. */
@@ -536,7 +578,7 @@ static int prefill_impl(orc_cache *c, const uint16_t *K, const uint16_t *V, int 
     }
   }
   const int d = f->d;
-  const int nq = L0 > f->R ? (L0 - f->R) / f->G * f->G : 0;
+  const int nq = L0 > f->R ? (f->exact_r ? L0 - f->R : (L0 - f->R) / f->G * f->G) : 0;
 #ifdef _OPENMP
 #pragma omp parallel for schedule(dynamic)
 #endif
@@ -553,7 +595,10 @@ static int prefill_impl(orc_cache *c, const uint16_t *K, const uint16_t *V, int 
                          colsum ? colsum + (long)u * f->g * L0 : NULL,
                          c->sal + (long)u * c->cap);
     }
-    for (int j = 0; j < nq / f->G; ++j) quantize_block(c, u, j);
+    if (f->exact_r)
+      for (int t = 0; t < nq; ++t) quantize_token(c, u, t);
+    else
+      for (int j = 0; j < nq / f->G; ++j) quantize_block(c, u, j);
   }
   c->L = L0;
   c->nq = nq;
@@ -585,7 +630,10 @@ int orc_append(orc_cache *c, const uint16_t *k, const uint16_t *v,
         (f->kind == ORC_TSA && types && types[u] == 1) ? 1 : 0;
   }
   c->L = t + 1;
-  if (c->L - f->R - c->nq >= f->G) {
+  if (f->exact_r && c->L - f->R > c->nq) {   /* token n_q leaves the window (R26) */
+    for (int u = 0; u < f->U; ++u) quantize_token(c, u, c->nq);
+    c->nq += 1;
+  } else if (!f->exact_r && c->L - f->R - c->nq >= f->G) {
     const int j = c->nq / f->G;
 #ifdef _OPENMP
 #pragma omp parallel for schedule(dynamic)

@@ -48,6 +48,10 @@ typedef struct {
                      "per-token dynamic" rule of P:246       */
   int decide64;   /* 1: quantizer decisions in fp64 (default); 0: in IEEE
                      fp32 on the fp32-rounded x.H_s (R6)                     */
+  int exact_r;    /* per-token K only (k_axis 1): 1 = exactly the last R
+                     tokens stay 16-bit, n_q = max(0, L - R), every token
+                     quantized on its own when it leaves the window (P:246,
+                     "residual" R, DESIGN R26); 0 = the block schedule R9    */
 } orc_config;
 
 typedef struct orc_cache orc_cache;

@@ -763,3 +763,98 @@ def test_tsa_4bit_view_bounds_and_on_grid(orc, d64):
             assert np.all(np.abs(Xh[u, idx] - Xf[u, idx]) <= s / 2 * (1 + 1e-6) + 1e-12)
         assert np.abs(Kh[u, nq:] - Kf[u, nq:]).max() <= 1e-12
     assert np.abs(Kh[1, :16] - Xg / math.sqrt(d)).max() <= 1e-12
+
+
+# --------------------------------------------- exact residual window (R26, NEXT-1)
+def test_exact_r_schedule_and_window(orc):
+    """Per-token K with an exact residual window ("per-token", R = the
+    16-bit recent window of P:204; DESIGN R26): after prefill and after every
+    append exactly min(L, R) tokens stay 16-bit, n_q = max(0, L - R); the view of
+    the last R tokens is their original rows (16-bit tier, exact up to the fp64
+    rotation), every older non-salient token is quantized (within scale/2 of its
+    rotated row).  Invalid combinations are refused."""
+    rng = np.random.default_rng(31)
+    d, G, R = 64, 32, 8
+    with pytest.raises(ValueError):
+        orc.OracleCache(_cfg(orc, d=d, G=G, R=R, k_axis=0, exact_r=1))
+    for kind, L0 in ((orc.PSA, 5), (orc.PSA, 45), (orc.TSA, 77)):
+        cfg = _cfg(orc, U=2, d=d, G=G, R=R, capacity=L0 + 40, kind=kind, top_k=2,
+                   k_axis=1, exact_r=1)
+        c = orc.OracleCache(cfg)
+        K = _f16_bits(rng.normal(size=(2, L0, d)))
+        V = _f16_bits(rng.normal(size=(2, L0, d)))
+        types = (rng.random((2, L0)) < 0.3).astype(np.uint8)
+        assert c.prefill(K, V, types=types, colsum=rng.random((2, 1, L0)).astype(np.float32)) == 0
+        assert c.nq == max(0, L0 - R)
+        H = scipy.linalg.hadamard(d) / np.sqrt(d)
+        ks, vs = [K], [V]
+        for step in range(40):
+            k = _f16_bits(rng.normal(size=(2, d)))
+            v = _f16_bits(rng.normal(size=(2, d)))
+            ks.append(k[:, None]); vs.append(v[:, None])
+            assert c.append(k, v, np.ones(2, np.uint8)) == 0
+            assert c.L == L0 + step + 1 and c.nq == max(0, c.L - R)
+        Kh, Vh = c.view()
+        e = c.export()
+        Ko = np.concatenate(ks, 1).view(np.float16).astype(np.float64)
+        Vo = np.concatenate(vs, 1).view(np.float16).astype(np.float64)
+        assert np.abs(Kh[:, c.nq: c.L] - Ko[:, c.nq:] @ H).max() < 1e-12
+        assert np.abs(Vh[:, c.nq: c.L] - Vo[:, c.nq:] @ H).max() < 1e-12
+        sal = e["salient"][:, : c.L].astype(bool)
+        xs = e["xs_k"][:, : c.nq] / np.sqrt(d)
+        sc = np.repeat(e["kscale"][:, : c.nq], G, axis=-1)
+        ok = np.abs(xs - Kh[:, : c.nq]) <= sc / 2 + 1e-9
+        zf = np.repeat(e["kzero"][:, : c.nq], G, axis=-1).astype(np.float64)
+        lo, hi = sc * (0 - zf), sc * (3 - zf)
+        inclip = (xs >= np.minimum(lo, hi) - 1e-9) & (xs <= np.maximum(lo, hi) + 1e-9)
+        assert (ok | ~inclip)[~sal[:, : c.nq]].all()
+        assert c.L - c.nq == R
+
+
+def test_exact_r_equals_block_schedule_per_token(orc):
+    """Per-token quantization of a token depends only on its own row and salient
+    flag, so the exact-R schedule (token by token, R26) and the block schedule
+    (R9, quantize_block) must give identical codes, meta and side entries for
+    every token both have quantized -- two independent code paths of the oracle
+    checked against each other; plus prefill == incremental append under
+    exact R."""
+    rng = np.random.default_rng(32)
+    d, G, R, L0, n_app = 64, 32, 8, 90, 37
+    for kind in (orc.TSA, orc.PSA):
+        K = _f16_bits(rng.normal(size=(2, L0 + n_app, d)) * np.where(np.arange(d) == 3, 15, 1))
+        V = _f16_bits(rng.normal(size=(2, L0 + n_app, d)))
+        types = (rng.random((2, L0 + n_app)) < 0.25).astype(np.uint8)
+        cs = rng.random((2, 1, L0)).astype(np.float32)
+        caches = []
+        for ex in (1, 0):
+            c = orc.OracleCache(_cfg(orc, U=2, d=d, G=G, R=R, capacity=L0 + n_app, kind=kind,
+                                     top_k=3, k_axis=1, exact_r=ex))
+            assert c.prefill(K[:, :L0], V[:, :L0], types=types[:, :L0], colsum=cs) == 0
+            for t in range(L0, L0 + n_app):
+                assert c.append(K[:, t], V[:, t], types[:, t]) == 0
+            caches.append(c)
+        a, b = caches                                    # exact, block
+        assert a.nq == L0 + n_app - R and b.nq == (L0 + n_app - R) // G * G
+        ea, eb = a.export(), b.export()
+        n = b.nq
+        for key in ("kcodes", "vcodes", "kscale_raw", "kzero", "vscale_raw", "vzero",
+                    "kpre", "vpre"):
+            assert np.array_equal(ea[key][:, :n], eb[key][:, :n],
+                                  equal_nan=ea[key].dtype.kind == "f"), key
+        cnt = eb["side_count"]
+        assert np.all(ea["side_count"] >= cnt)
+        for u in range(2):
+            m = int(cnt[u])
+            assert np.array_equal(ea["side_index"][u, :m], eb["side_index"][u, :m])
+            if kind == orc.TSA:
+                assert np.array_equal(ea["side4"][u, :m], eb["side4"][u, :m])
+                assert np.array_equal(ea["side4_zero"][u, :m], eb["side4_zero"][u, :m])
+        if kind == orc.TSA:                              # prefill == append (no pivots)
+            c2 = orc.OracleCache(_cfg(orc, U=2, d=d, G=G, R=R, capacity=L0 + n_app, kind=kind,
+                                      top_k=3, k_axis=1, exact_r=1))
+            T = L0 + n_app
+            assert c2.prefill(K, V, types=types, colsum=np.zeros((2, 1, T), np.float32)) == 0
+            e2 = c2.export()
+            assert c2.nq == a.nq
+            for key in ea:
+                assert np.array_equal(ea[key], e2[key], equal_nan=ea[key].dtype.kind == "f"), key
