@@ -85,6 +85,12 @@ typedef struct {
   int32_t paged;      /* 0: the pages live in the cache buffer; 1: in a caller-
                          owned page pool shared by any number of caches, found
                          through a block table (akvq_cache_attach_pages)      */
+  int32_t exact_r;    /* per-token K only (k_axis 1, else EINVAL): 1 = exactly
+                         the last R tokens stay 16-bit, n_q = max(0, L - R),
+                         each token quantized on its own as it leaves the
+                         window ("residual" R; DESIGN R26); 0 = whole
+                         G-blocks leave the window (R9).  The last page is then
+                         partly filled.  Not with AKVQ_OPT_DEVICE_L.          */
 } akvq_config;
 
 /* Byte layout of the caller's cache buffer (all offsets from its base;
@@ -148,7 +154,8 @@ typedef struct {
 
 /* Caller-owned handle.  L and n_q are host mirrors of the (uniform across
  * units) token count and quantized-region length n_q = G*floor(max(0,L-R)/G)
- * (R9); the host needs them to schedule flushes without device->host syncs. */
+ * (R9; max(0, L-R) with cfg.exact_r, R26); the host needs them to schedule
+ * flushes without device->host syncs. */
 typedef struct {
   akvq_config cfg;
   akvq_layout lay;
@@ -244,7 +251,8 @@ akvq_status akvq_rotate_quantize(akvq_cache *c, const void *K, const void *V,
 /* append_decode (Eq. 2): store each unit's new row in
  * ring slot L % slots, mark it salient if TSA and types[u] == 1, L += 1; if
  * L - R - n_q >= G, quantize block [n_q, n_q + G) from the ring exactly as
- * prefill would and n_q += G.
+ * prefill would and n_q += G.  cfg.exact_r: if L - R > n_q, quantize
+ * token n_q alone from the ring (K and V per token, R26) and n_q += 1.
  *   k, v   device [U][d] 16-bit;  types device [U] u8 (NULL = all vision)
  * Errors: ECAPACITY (L == capacity; nothing changes). */
 akvq_status akvq_append_token(akvq_cache *c, const void *k, const void *v,

@@ -50,7 +50,7 @@ class akvq_config(C.Structure):
                 ("group", C.c_int32), ("residual", C.c_int32), ("capacity", C.c_int32),
                 ("top_k", C.c_int32), ("kind", C.c_int32), ("dtype16", C.c_int32),
                 ("clip2", C.c_float), ("clip4", C.c_float), ("k_axis", C.c_int32),
-                ("paged", C.c_int32)]
+                ("paged", C.c_int32), ("exact_r", C.c_int32)]
 
 
 class akvq_layout(C.Structure):
@@ -164,8 +164,9 @@ def _stream(stream: Optional[torch.cuda.Stream]):
 
 
 def make_config(U, g, d, G, R, capacity, top_k, kind, dtype16=AKVQ_BF16, clip2=0.8,
-                clip4=1.0, k_axis=0, paged=0) -> akvq_config:
-    return akvq_config(U, g, d, G, R, capacity, top_k, kind, dtype16, clip2, clip4, k_axis, paged)
+                clip4=1.0, k_axis=0, paged=0, exact_r=0) -> akvq_config:
+    return akvq_config(U, g, d, G, R, capacity, top_k, kind, dtype16, clip2, clip4, k_axis, paged,
+                       exact_r)
 
 
 # ----------------------------------------------------------------- C-ABI calls

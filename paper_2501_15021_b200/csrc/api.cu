@@ -28,7 +28,8 @@ akvq_status check_config(const akvq_config *f) {
       (f->kind != AKVQ_TSA && f->kind != AKVQ_PSA) ||
       (f->dtype16 != AKVQ_BF16 && f->dtype16 != AKVQ_FP16) ||
       (f->k_axis != AKVQ_K_PER_CHANNEL && f->k_axis != AKVQ_K_PER_TOKEN) ||
-      (f->paged != 0 && f->paged != 1))
+      (f->paged != 0 && f->paged != 1) || (f->exact_r != 0 && f->exact_r != 1) ||
+      (f->exact_r && f->k_axis != AKVQ_K_PER_TOKEN))
     return AKVQ_EINVAL;
   if ((f->head_dim != 64 && f->head_dim != 128) || f->group < 32 || f->group > 128 ||
       f->group > f->head_dim || f->q_per_kv > 16 || f->top_k > 32)
@@ -66,6 +67,24 @@ DevCache make_dev(const akvq_cache *c) {
 }
 
 akvq_status cuda_status(cudaError_t e) { return e == cudaSuccess ? AKVQ_OK : AKVQ_ECUDA; }
+
+// Quantized-region length for L tokens: whole G-blocks (R9) or, with the exact
+// residual window (R26), every token but the last R.
+int nq_for(const akvq_config &f, int L) {
+  if (L <= f.residual) return 0;
+  return f.exact_r ? L - f.residual : (L - f.residual) / f.group * f.group;
+}
+
+// Ring rows of tokens [t0, t1) as a quantize source (flush / exact-R step).
+QuantSrc ring_src(const DevCache &d) {
+  QuantSrc src;
+  src.K = d.ring;
+  src.V = d.ring + d.d;
+  src.unit_stride = (size_t)d.slots * 2 * d.d;
+  src.tok_stride = (size_t)2 * d.d;
+  src.ring_slots = d.slots;
+  return src;
+}
 
 // Per-stream record of the library's last kernel launch on that stream and the
 // cache buffer it wrote (NULL: it wrote no cache).  The decode kernel is
@@ -123,7 +142,7 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
   DecodePlan p;
   p.L = L;
   p.n_q = n_q;
-  p.n_pages = n_q / f.group;
+  p.n_pages = (n_q + f.group - 1) / f.group;         // exact R: the last page partial
   const int sms = c->sm_count > 0 ? c->sm_count : 148;
   const long target = 4L * sms;                       // CTAs to keep every SM busy
   long pps = ((long)f.n_units * p.n_pages + target - 1) / target;
@@ -441,7 +460,7 @@ akvq_status akvq_detect_pivots(const void *residual, int32_t n_rows, int32_t L0,
 static akvq_status quantize_prompt(akvq_cache *c, const void *K, const void *V, int32_t L0,
                                    akvq_stream_t stream) {
   const akvq_config &f = c->cfg;
-  const int n_q = L0 > f.residual ? (L0 - f.residual) / f.group * f.group : 0;   // R9
+  const int n_q = nq_for(f, L0);                     // R9 / R26
   const DevCache d = make_dev(c);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   QuantSrc src;
@@ -452,9 +471,11 @@ static akvq_status quantize_prompt(akvq_cache *c, const void *K, const void *V, 
   src.ring_slots = 0;
   const int nb = n_q / f.group;
   cudaError_t e = launch_quantize_blocks(d, f.dtype16, src, 0, nb, nb - 1, s);
+  // exact R: the tokens of the partial last page, one at a time (R26)
+  if (e == cudaSuccess) e = launch_quantize_tokens(d, f.dtype16, src, nb * f.group, n_q, s);
   if (e == cudaSuccess) e = launch_ring_fill(d, K, V, L0, n_q, L0, s);
   if (e == cudaSuccess) e = launch_state_set(d, L0, s);    // device copy of L
-  c->launches += (nb > 0) + (L0 > n_q) + 1;
+  c->launches += (nb > 0) + (n_q > nb * f.group) + (L0 > n_q) + 1;
   note_launch(c, s, true);
   if (e != cudaSuccess) return AKVQ_ECUDA;
   c->L = L0;
@@ -475,15 +496,15 @@ static akvq_status append_impl(akvq_cache *c, const void *k, const void *v, cons
   c->launches += 1;
   note_launch(c, s, true);
   c->L += 1;
-  if (c->L - f.residual - c->n_q >= f.group) {        // block leaves the window (R9)
-    QuantSrc src;
-    src.K = d.ring;
-    src.V = d.ring + f.head_dim;
-    src.unit_stride = (size_t)d.slots * 2 * f.head_dim;
-    src.tok_stride = (size_t)2 * f.head_dim;
-    src.ring_slots = d.slots;
+  if (f.exact_r && c->L - f.residual > c->n_q) {      // token n_q leaves the window (R26)
+    e = launch_quantize_tokens(d, f.dtype16, ring_src(d), c->n_q, c->n_q + 1, s);
+    if (e != cudaSuccess) return AKVQ_ECUDA;
+    c->launches += 1;
+    note_launch(c, s, true);
+    c->n_q += 1;
+  } else if (!f.exact_r && c->L - f.residual - c->n_q >= f.group) {   // block leaves the window (R9)
     const int j = c->n_q / f.group;
-    e = launch_quantize_blocks(d, f.dtype16, src, j, 1, j, s);
+    e = launch_quantize_blocks(d, f.dtype16, ring_src(d), j, 1, j, s);
     if (e != cudaSuccess) return AKVQ_ECUDA;
     c->launches += 1;
     note_launch(c, s, true);
@@ -508,12 +529,10 @@ size_t akvq_decode_workspace_bytes_max(const akvq_cache *c) {
   size_t best = 0;
   const akvq_config &f = c->cfg;
   for (int L = 1; L <= f.capacity; ++L) {     // plans are cheap; the size is not monotone in L
-    const int n_q = L > f.residual ? (L - f.residual) / f.group * f.group : 0;
-    const size_t b = ws_bytes_for(c, plan_decode(c, L, n_q, false));
+    const size_t b = ws_bytes_for(c, plan_decode(c, L, nq_for(f, L), false));
     if (b > best) best = b;
   }
-  const int n_q = f.capacity > f.residual ? (f.capacity - f.residual) / f.group * f.group : 0;
-  const size_t b = ws_bytes_for(c, plan_decode(c, f.capacity, n_q, false));
+  const size_t b = ws_bytes_for(c, plan_decode(c, f.capacity, nq_for(f, f.capacity), false));
   return b > best ? b : best;
 }
 
@@ -526,6 +545,7 @@ static akvq_status decode_impl(const akvq_cache *c, const void *q, float *out, v
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
   const DevCache d = make_dev(c);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((c->options & AKVQ_OPT_DEVICE_L) && c->cfg.exact_r) return AKVQ_EUNSUPPORTED;
   if (p.fast) return launch_fast(c, p, q, nullptr, nullptr, nullptr, out, ws, flags, s);
   if (c->options & AKVQ_OPT_DEVICE_L) return AKVQ_EUNSUPPORTED;   // generic kernels use the host L
   const_cast<akvq_cache *>(c)->launches += 2;         // split + combine
@@ -549,17 +569,33 @@ akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const 
   const akvq_config &f = c->cfg;
   if (c->L >= f.capacity) return AKVQ_ECAPACITY;
   const int L1 = c->L + 1;
-  const bool flush = L1 - f.residual - c->n_q >= f.group;
-  DecodePlan p = plan_decode(c, L1, flush ? c->n_q + f.group : c->n_q);
+  if ((c->options & AKVQ_OPT_DEVICE_L) && f.exact_r) return AKVQ_EUNSUPPORTED;
+  // exact R (R26): token n_q leaves the window at this step; it is quantized
+  // from the ring before the fused launch (it does not depend on the new token)
+  const bool leave1 = f.exact_r && L1 - f.residual > c->n_q;
+  const bool flush = !f.exact_r && L1 - f.residual - c->n_q >= f.group;
+  DecodePlan p = plan_decode(c, L1, flush ? c->n_q + f.group : c->n_q + (leave1 ? 1 : 0));
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
+  if (leave1) {
+    const DevCache d = make_dev(c);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (launch_quantize_tokens(d, f.dtype16, ring_src(d), c->n_q, c->n_q + 1, s) != cudaSuccess)
+      return AKVQ_ECUDA;
+    note_launch(c, s, true);
+    c->n_q += 1;
+  }
+  const int pre = leave1 ? 1 : 0;
   if (flush || !p.fast || p.lp.T <= 0) {   // flush step (every G tokens) or generic path
     akvq_status st = append_impl(c, k, v, types, stream);
     if (st != AKVQ_OK) return st;
-    return decode_impl(c, q, out, ws, ws_bytes, flags, stream);
+    st = decode_impl(c, q, out, ws, ws_bytes, flags, stream);
+    c->launches += pre;
+    return st;
   }
   const akvq_status st = launch_fast(c, p, q, k, v, types, out, ws, flags,
                                      reinterpret_cast<cudaStream_t>(stream));
   if (st != AKVQ_OK) return st;
+  c->launches += pre;
   c->L = L1;
   return AKVQ_OK;
 }
@@ -576,7 +612,7 @@ akvq_status akvq_cache_advance(akvq_cache *c, int32_t steps) {
   const akvq_config &f = c->cfg;
   if (c->L + steps > f.capacity) return AKVQ_ECAPACITY;
   // no block may have left the window in between (the replayed launches do not flush)
-  if (c->L + steps - f.residual - c->n_q >= f.group) return AKVQ_ESTATE;
+  if (c->L + steps - f.residual - c->n_q >= (f.exact_r ? 1 : f.group)) return AKVQ_ESTATE;
   c->L += steps;
   return AKVQ_OK;
 }

@@ -83,6 +83,9 @@ __global__ void __launch_bounds__(kThreads) k_decode_split(DevCache c, DecodePla
     const int p1 = min(p0 + p.pages_per_split, p.n_pages);
     item0 = p0 * (G / 32);
     n_items = (p1 - p0) * (G / 32);
+    // exact R (R26): the last page is partial; chunks past n_q are skipped and
+    // the tokens >= n_q of the last chunk are masked like salient ones
+    n_items = min(n_items, (p.n_q + 31) / 32 - item0);
   } else if (s < p.n_page_splits + p.n_ring_splits) {
     kind = kRing;
     const int r = s - p.n_page_splits;
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(kThreads) k_decode_split(DevCache c, DecodePla
         }
       }
       __syncwarp();
-      const bool sal = (bm[t0 / 32] >> lane) & 1u;
+      const bool sal = ((bm[t0 / 32] >> lane) & 1u) || t0 + lane >= p.n_q;
 #pragma unroll
       for (int h = 0; h < MAXG; ++h)
         if (h < g) logit[h] = sal ? -INFINITY : lg[h * 32 + lane];

@@ -218,6 +218,10 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
             bulk_g2s(dst, pg, kbytes, &bar[st]);
           }
           pbits = __ldg(c.bitmask + (size_t)sb.pu * c.bm_words + (size_t)a * (G / 32) + pbw);
+          if constexpr (KT) {                     // exact R (R26): the last page is partial;
+            const int lim = lp.n_q - a * G - pbw * 32;   // its tokens >= n_q act as salient
+            if (lim < 32) pbits |= lim <= 0 ? ~0u : (~0u << lim);
+          }
           vsrc = pg + kbytes;
           LySub vb = sb;
           vb.kind = 1;

@@ -51,7 +51,7 @@ struct LayerPlan {
 // Decode split plan (host-computed, uniform across units).
 struct DecodePlan {
   int L, n_q;
-  int n_pages;           // quantized pages in use = n_q / G
+  int n_pages;           // quantized pages in use = ceil(n_q / G) (exact R: last one partial)
   int pages_per_split, n_page_splits;
   int ring_per_split, n_ring_splits;
   int n_side_splits;     // side entries are shared equally among these splits
@@ -64,6 +64,9 @@ cudaError_t launch_salient(const DevCache &c, const uint8_t *types, const float 
                            int L0, int top_k, cudaStream_t st);
 cudaError_t launch_quantize_blocks(const DevCache &c, int dtype16, const QuantSrc &src,
                                    int block0, int nblocks, int last_block, cudaStream_t st);
+// exact residual window (R26): tokens [t0, t1) quantized one at a time
+cudaError_t launch_quantize_tokens(const DevCache &c, int dtype16, const QuantSrc &src, int t0,
+                                   int t1, cudaStream_t st);
 cudaError_t launch_ring_fill(const DevCache &c, const void *K, const void *V, int L0, int t0,
                              int t1, cudaStream_t st);
 cudaError_t launch_append(const DevCache &c, const void *k, const void *v,

@@ -375,6 +375,127 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
   }
 }
 
+// ============================================================ K1e: exact R
+// Tokens [t0, t1) quantized one at a time (per-token K only; exact residual
+// window, DESIGN R26): the per-token steps of k_quantize_blocks<KT> for
+// each token alone -- FWHT, K and V meta per G-channel group (Eqs. 3-6, clip2),
+// 2-bit codes written into the token's bits of the page's tile words (K words
+// hold 4 tokens per byte: read-modify-write of the token's 2 bits), salient ->
+// codes 0, meta (0, 0) and the next side entry (TSA 4-bit, clip4; PSA the
+// 16-bit rows).  One warp per unit; the 4 row groups of 8 lanes all transform
+// the same row (the shuffle FWHT needs every lane), row group 0 writes.  A
+// token that opens a page first zeroes the page, so the decode kernels read
+// scale 0 / codes 0 for the tokens not yet quantized (masked like salient).
+template <int D, int G, int DT>
+__global__ void __launch_bounds__(32) k_quantize_tokens(DevCache c, QuantSrc src, int t0, int t1) {
+  constexpr int CPL = D / 8, GL = G / CPL, NG = D / G, TQ = G / 4, CQ = D / 4;
+  const int u = blockIdx.x, lane = threadIdx.x, cl = lane & 7;
+  const bool w0 = lane < 8;                  // row group 0 writes
+  const uint32_t *bm = c.bitmask + (size_t)u * c.bm_words;
+  const bool tsa = c.kind == AKVQ_TSA;
+  int cnt = c.side_cnt[u];
+  unsigned kmax_l = 0u, vmax_l = 0u;
+  for (int tok = t0; tok < t1; ++tok) {
+    const int j = tok / G, t = tok % G;
+    uint8_t *pg = page_ptr(c, u, j);
+    if (t == 0) {                            // a fresh page: zero it
+      uint4 *z = reinterpret_cast<uint4 *>(pg);
+      for (int i = lane; i < (int)(c.page_bytes / 16); i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
+      __syncwarp();
+    }
+    const bool sal = (bm[tok >> 5] >> (tok & 31)) & 1u;
+    const size_t roff = (size_t)u * src.unit_stride +
+                        (size_t)(src.ring_slots ? tok % src.ring_slots : tok) * src.tok_stride;
+    const uint4 *kr = reinterpret_cast<const uint4 *>(src.K + roff + cl * CPL);
+    const uint4 *vr = reinterpret_cast<const uint4 *>(src.V + roff + cl * CPL);
+    uint4 kraw[CPL / 8], vraw[CPL / 8];
+#pragma unroll
+    for (int i = 0; i < CPL / 8; ++i) { kraw[i] = kr[i]; vraw[i] = vr[i]; }
+    float k[CPL], v[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL / 8; ++i) { cvt8<DT>(kraw[i], k + 8 * i); cvt8<DT>(vraw[i], v + 8 * i); }
+    fwht_lanes8<CPL>(k, cl);
+    fwht_lanes8<CPL>(v, cl);
+    const int gi = (cl * CPL) / G, mi = t * NG + gi;
+    float mnk = k[0], mxk = k[0], mnv = v[0], mxv = v[0];
+#pragma unroll
+    for (int i = 1; i < CPL; ++i) {
+      mnk = fminf(mnk, k[i]); mxk = fmaxf(mxk, k[i]);
+      mnv = fminf(mnv, v[i]); mxv = fmaxf(mxv, v[i]);
+    }
+    group_minmax<GL>(mnk, mxk);
+    group_minmax<GL>(mnv, mxv);
+    const QMeta mk = q_meta(mnk, mxk, !sal, c.clip2, 3.f);
+    const QMeta mv = q_meta(mnv, mxv, !sal, c.clip2, 3.f);
+    const uint32_t ck = q_codes2<CPL>(k, mk, mk.mode == 0 ? __frcp_rn(mk.s) : 0.f);
+    const uint32_t cv = q_codes2<CPL>(v, mv, mv.mode == 0 ? __frcp_rn(mv.s) : 0.f);
+    if (w0) {
+      if ((cl % GL) == 0) {
+        const float ks = sal ? 0.f : __fmul_rn(mk.s, c.inv_sqrt_d);
+        const float vs = sal ? 0.f : __fmul_rn(mv.s, c.inv_sqrt_d);
+        reinterpret_cast<float *>(pg + c.pg_kscale)[mi] = ks;
+        reinterpret_cast<int32_t *>(pg + c.pg_kzero)[mi] = sal ? 0 : zero_i32(mk.zf);
+        reinterpret_cast<float *>(pg + c.pg_vscale)[mi] = vs;
+        reinterpret_cast<int32_t *>(pg + c.pg_vzero)[mi] = sal ? 0 : zero_i32(mv.zf);
+        kmax_l = max(kmax_l, __float_as_uint(fabsf(ks)));
+        vmax_l = max(vmax_l, __float_as_uint(fabsf(vs)));
+      }
+      uint8_t *kc = pg + c.pg_kcodes, *vc = pg + c.pg_vcodes;
+      const int sh = 2 * (t & 3);
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) {        // K: the token's 2 bits of channel ch's byte
+        const int ch = cl * CPL + i;
+        uint8_t *b = kc + 4 * kword_idx(ch >> 2, t >> 2, TQ) + (ch & 3);
+        *b = (uint8_t)((*b & ~(3u << sh)) | (((ck >> (2 * i)) & 3u) << sh));
+      }
+#pragma unroll
+      for (int i = 0; i < CPL / 4; ++i)      // V: the token's S:146 byte per channel quad
+        vc[4 * vword_idx(cl * (CPL / 4) + i, t >> 2, CQ) + (t & 3)] = (uint8_t)(cv >> (8 * i));
+    }
+    if (sal) {                               // next side entry (ascending token order)
+      uint8_t *se = side_ptr(c, u, cnt);
+      if (lane == 0) c.side_idx[(size_t)u * c.side_cap + cnt] = tok;
+      if (tsa) {   // 4-bit per token over G-channel groups, clip4 (R11)
+        const QMeta mk4 = q_meta(mnk, mxk, true, c.clip4, 15.f);
+        const QMeta mv4 = q_meta(mnv, mxv, true, c.clip4, 15.f);
+        if (w0) {
+          if ((cl % GL) == 0) {
+            reinterpret_cast<float *>(se)[gi] = __fmul_rn(mk4.s, c.inv_sqrt_d);
+            reinterpret_cast<int32_t *>(se + 4 * NG)[gi] = zero_i32(mk4.zf);
+            reinterpret_cast<float *>(se + 8 * NG)[gi] = __fmul_rn(mv4.s, c.inv_sqrt_d);
+            reinterpret_cast<int32_t *>(se + 12 * NG)[gi] = zero_i32(mv4.zf);
+          }
+          uint32_t c4k[CPL / 8], c4v[CPL / 8];
+#pragma unroll
+          for (int i = 0; i < CPL / 8; ++i) { c4k[i] = 0; c4v[i] = 0; }
+#pragma unroll
+          for (int i = 0; i < CPL; ++i) {
+            c4k[i / 8] |= q_code(k[i], mk4, 15.f) << (4 * (i % 8));
+            c4v[i / 8] |= q_code(v[i], mv4, 15.f) << (4 * (i % 8));
+          }
+          uint32_t *dk = reinterpret_cast<uint32_t *>(se + 16 * NG + cl * (CPL / 2));
+          uint32_t *dv = reinterpret_cast<uint32_t *>(se + 16 * NG + D / 2 + cl * (CPL / 2));
+#pragma unroll
+          for (int i = 0; i < CPL / 8; ++i) { dk[i] = c4k[i]; dv[i] = c4v[i]; }
+        }
+      } else if (w0) {   // PSA pivot: original 16-bit K and V rows (R10)
+        uint4 *dk = reinterpret_cast<uint4 *>(se) + cl * (CPL / 8);
+        uint4 *dv = reinterpret_cast<uint4 *>(se + 2 * D) + cl * (CPL / 8);
+#pragma unroll
+        for (int i = 0; i < CPL / 8; ++i) { dk[i] = kraw[i]; dv[i] = vraw[i]; }
+      }
+      ++cnt;
+    }
+    __syncwarp();
+  }
+  const unsigned kw = __reduce_max_sync(0xffffffffu, kmax_l), vw = __reduce_max_sync(0xffffffffu, vmax_l);
+  if (lane == 0) {
+    c.side_cnt[u] = cnt;
+    atomicMax(reinterpret_cast<unsigned *>(&c.umax[u].x), kw);
+    atomicMax(reinterpret_cast<unsigned *>(&c.umax[u].y), vw);
+  }
+}
+
 // ============================================================ K1t / K3
 // Copy rows [t0, t1) of K and V (16-bit originals) into the ring (R10).
 __global__ void k_ring_fill(DevCache c, const uint16_t *__restrict__ K,
@@ -463,6 +584,24 @@ cudaError_t launch_quantize_blocks(const DevCache &c, int dtype16, const QuantSr
   AKVQ_QCASE(128, 64)
   AKVQ_QCASE(128, 128)
 #undef AKVQ_QCASE
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_quantize_tokens(const DevCache &c, int dtype16, const QuantSrc &src, int t0,
+                                   int t1, cudaStream_t st) {
+  if (t1 <= t0) return cudaSuccess;
+#define AKVQ_TCASE(D_, G_)                                                              \
+  if (c.d == D_ && c.G == G_) {                                                         \
+    if (dtype16 == AKVQ_BF16) k_quantize_tokens<D_, G_, AKVQ_BF16><<<c.U, 32, 0, st>>>(c, src, t0, t1); \
+    else k_quantize_tokens<D_, G_, AKVQ_FP16><<<c.U, 32, 0, st>>>(c, src, t0, t1);       \
+    return cudaGetLastError();                                                          \
+  }
+  AKVQ_TCASE(64, 32)
+  AKVQ_TCASE(64, 64)
+  AKVQ_TCASE(128, 32)
+  AKVQ_TCASE(128, 64)
+  AKVQ_TCASE(128, 128)
+#undef AKVQ_TCASE
   return cudaErrorInvalidValue;
 }
 

@@ -37,21 +37,21 @@ def _case_name():
     return os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0].split("::")[-1]
 
 
-def _configs(ak, orc, w, layer, units_n, kind=None, cap=None, k_axis=0, decide64=1):
+def _configs(ak, orc, w, layer, units_n, kind=None, cap=None, k_axis=0, decide64=1, exact_r=0):
     kind = w.kind(layer) if kind is None else kind
     dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
     cap = w.capacity if cap is None else cap
     gcfg = ak.make_config(units_n, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4,
-                          k_axis)
+                          k_axis, exact_r=exact_r)
     ocfg = orc.OracleConfig(units_n, w.g, w.d, w.G, w.R, cap, w.top_k, kind,
                             orc.BF16 if dt == ak.AKVQ_BF16 else orc.FP16, w.clip2, w.clip4,
-                            k_axis, decide64)
+                            k_axis, decide64, exact_r)
     return gcfg, ocfg
 
 
 def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every=1,
               flags=0, report=None, options=0, fused_step=None, k_axis=0,
-              xf_layer=None, xf_decode=None, case=None, paged=None):
+              xf_layer=None, xf_decode=None, case=None, paged=None, exact_r=0):
     """Prefill + `steps` decode steps on the GPU for all units; the oracle runs the
     sampled `units` (default all) in BOTH decision precisions: fp64 (SURVEY 8(c),
     the contract) and fp32 (R6, the kernel's).  The cache state is compared with
@@ -64,8 +64,9 @@ def _run_case(ak, orc, sy, w, layer, kind=None, steps=4, units=None, check_every
     oracle's sampled inputs.  Worst errors and tie counts go to parity.MARGINS."""
     U = w.U
     us = list(range(U)) if units is None else list(units)
-    gcfg, _ = _configs(ak, orc, w, layer, U, kind, k_axis=k_axis)
-    ocfgs = [_configs(ak, orc, w, layer, len(us), kind, k_axis=k_axis, decide64=d)[1]
+    gcfg, _ = _configs(ak, orc, w, layer, U, kind, k_axis=k_axis, exact_r=exact_r)
+    ocfgs = [_configs(ak, orc, w, layer, len(us), kind, k_axis=k_axis, decide64=d,
+                      exact_r=exact_r)[1]
              for d in (1, 0)]
     rep64 = {} if report is None else report
     rep32 = {}
@@ -636,6 +637,47 @@ def test_paged_block_table(ak, orc, sy, name, layer):
         ak.akvq_rotate_quantize(c, torch.zeros((w.U, 1, w.d), dtype=torch.bfloat16, device="cuda"),
                                 torch.zeros((w.U, 1, w.d), dtype=torch.bfloat16, device="cuda"), 1)
     assert e.value.status == ak.AKVQ_ESTATE
+
+
+# ------------------------------------------ per-token K, exact residual window (R26)
+@pytest.mark.parametrize("options", [0, 1], ids=["layer-pages", "generic-pages"])
+@pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
+def test_tiny_exact_r(ak, orc, sy, kind, options):
+    """exact_r = 1 (R26): n_q = L - R after every step, one token quantized
+    as it leaves the window (partial last page), state and decode vs the oracle at
+    every step across page boundaries; view vs the oracle's view."""
+    lc, oc, _ = _run_case(ak, orc, sy, sy.TINY, 0, kind=kind, steps=16, options=options,
+                          k_axis=1, exact_r=1)
+    assert lc.n_q == lc.L - sy.TINY.R
+    K, V = lc.view()
+    Ko, Vo = oc.view()
+    for a, b in ((K, Ko), (V, Vo)):
+        a = a.double().cpu().numpy()
+        assert np.all(np.abs(a - b) <= 1e-6 * np.maximum(np.abs(b), np.abs(b).max(-1, keepdims=True)) + 1e-7)
+
+
+@pytest.mark.parametrize("layer", [0, 2], ids=["TSA-L0", "PSA-L2"])
+def test_llava7b_exact_r(ak, orc, sy, layer):
+    _run_case(ak, orc, sy, sy.LLAVA7B, layer, steps=6, units=[0, 13, 31], k_axis=1, exact_r=1)
+
+
+def test_full_size_exact_r_sampled(ak, orc, sy):
+    w = sy.get("sweep@b16")
+    _run_case(ak, orc, sy, w, 2, steps=3, units=[0, w.U // 2, w.U - 1], k_axis=1, exact_r=1)
+
+
+@pytest.mark.parametrize("g", [2, 7])
+def test_gqa_exact_r(ak, orc, sy, g):
+    import dataclasses
+    w = dataclasses.replace(sy.TINY, name=f"tiny_er_g{g}", hq=4 * g, hkv=4)
+    _run_case(ak, orc, sy, w, 0, kind=0, steps=16, k_axis=1, exact_r=1)
+
+
+def test_exact_r_errors(ak, sy):
+    w = sy.TINY
+    with pytest.raises(ak.AkvqError):     # exact R needs per-token K (EINVAL)
+        ak.LayerCache(ak.make_config(w.U, w.g, w.d, w.G, w.R, w.capacity, w.top_k, 1,
+                                     ak.AKVQ_BF16, k_axis=0, exact_r=1))
 
 
 @pytest.mark.parametrize("g", [3, 7])

@@ -1,7 +1,7 @@
 """Randomized operation sequences against the oracle (-m gpu; SPEC acceptance
 criterion 8, and prefill == incremental append): >= 10^4 prefill /
 append / decode / fused-step operations over many small caches with random
-shapes (d, G, R, g, layer kind, K axis, DEVICE_L), every decode output compared
+shapes (d, G, R, g, layer kind, K axis, exact residual window, DEVICE_L), every decode output compared
 with the oracle (fp32-decision mode, where the kernel's codes agree bit for
 bit) and the full cache state compared at the end of every cache's life and at
 random points; a twin cache built by appends alone must equal the prefilled one."""
@@ -46,18 +46,20 @@ def test_random_operation_sequences(ak, orc):
         kind = int(rng.integers(0, 2))
         k_axis = int(rng.integers(0, 2)) if g == 1 else 0
         top_k = int(rng.integers(0, 6))
-        dev_L = bool(rng.integers(0, 2))
+        exact_r = int(rng.integers(0, 2)) if k_axis == 1 else 0      # R26
+        dev_L = bool(rng.integers(0, 2)) and not exact_r
         fp16 = bool(rng.integers(0, 2))
         dt = torch.float16 if fp16 else torch.bfloat16
         cap = int(rng.integers(2 * G, 5 * G))
         L0 = int(rng.integers(0, cap // 2))
         gdt = ak.AKVQ_FP16 if fp16 else ak.AKVQ_BF16
-        cfg = ak.make_config(U, g, d, G, R, cap, top_k, kind, gdt, 0.8, 1.0, k_axis)
+        cfg = ak.make_config(U, g, d, G, R, cap, top_k, kind, gdt, 0.8, 1.0, k_axis,
+                             exact_r=exact_r)
         lc = ak.LayerCache(cfg, options=ak.AKVQ_OPT_DEVICE_L if dev_L else 0)
         twin = ak.LayerCache(cfg)                              # built by appends only
         oc = orc.OracleCache(orc.OracleConfig(U, g, d, G, R, cap, top_k, kind,
                                               orc.FP16 if fp16 else orc.BF16, k_axis=k_axis,
-                                              decide64=0))
+                                              decide64=0, exact_r=exact_r))
         outl = int(rng.integers(0, d))
         K, V = _rows(rng, L0, U, d, dt, outl), _rows(rng, L0, U, d, dt, outl)
         types = torch.from_numpy((rng.random((U, L0)) < 0.3).astype(np.uint8))
@@ -93,7 +95,8 @@ def test_random_operation_sequences(ak, orc):
             if op in ("step", "decode"):
                 ref = oc.decode(f16_bits(q))
                 err = np.abs(out.double().cpu().numpy() - ref).max()
-                assert err <= OUT_TOL, (cfg.n_units, g, d, G, R, kind, k_axis, dev_L, op, lc.L, err)
+                assert err <= OUT_TOL, (cfg.n_units, g, d, G, R, kind, k_axis, exact_r, dev_L, op,
+                                        lc.L, err)
             assert (lc.L, lc.n_q) == (oc.L, oc.nq)
             ops += 1
             if rng.random() < 0.01:
