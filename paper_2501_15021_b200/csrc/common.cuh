@@ -187,6 +187,27 @@ __device__ __forceinline__ uint32_t q_codes2(const float (&x)[N], const QMeta &m
   if (m.mode == 1) return 0x55555555u & ((N >= 16) ? 0xffffffffu : ((1u << (2 * N)) - 1u));
   uint32_t w = 0;
   bool near = false;
+#ifndef AKVQ_QCODES_V1
+  // |x rs - x / s| <= 2 ulp(|y|) < 2.4e-7 |y|: for |y| <= 99 the two round alike
+  // unless y is within 2.4e-5 of a half-integer, which |y - rint(y)| > 0.4999
+  // flags; |y| > 99 (a large zero point) always takes the IEEE path.  Codes are
+  // packed exactly in fp32 (8 per float, values < 2^16) instead of per-code
+  // conversions and shifts.
+  float acc[(N + 7) / 8];
+#pragma unroll
+  for (int i = 0; i < (N + 7) / 8; ++i) acc[i] = 0.f;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const float y = __fmul_rn(x[i], rs);
+    const float r = rintf(y);
+    near |= fabsf(__fsub_rn(y, r)) > 0.4999f;
+    near |= fabsf(y) > 99.f;
+    const float q = fminf(fmaxf(__fadd_rn(r, m.zf), 0.f), 3.f);
+    acc[i / 8] = __fmaf_rn(q, (float)(1u << (2 * (i % 8))), acc[i / 8]);
+  }
+#pragma unroll
+  for (int i = 0; i < (N + 7) / 8; ++i) w |= (uint32_t)acc[i] << (16 * i);
+#else
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     const float y = __fmul_rn(x[i], rs);
@@ -195,6 +216,7 @@ __device__ __forceinline__ uint32_t q_codes2(const float (&x)[N], const QMeta &m
     const float q = fminf(fmaxf(__fadd_rn(r, m.zf), 0.f), 3.f);
     w |= (uint32_t)q << (2 * i);
   }
+#endif
   if (near) {
     w = 0;
 #pragma unroll

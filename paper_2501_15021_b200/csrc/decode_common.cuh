@@ -10,6 +10,28 @@
 
 namespace akvq {
 
+// Single-instruction warp reductions (REDUX) for the per-page critical path;
+// AKVQ_REDUX=0 builds the shuffle-tree versions (A/B).
+#ifndef AKVQ_REDUX
+#define AKVQ_REDUX 0
+#endif
+// max over the warp of a float: the order-preserving map of IEEE bits to
+// signed integers (negative values: magnitude bits flipped) is an involution
+__device__ __forceinline__ float warp_max_fast(float v) {
+#if AKVQ_REDUX
+  int i = __float_as_int(v);
+  i ^= (i >> 31) & 0x7fffffff;
+  i = __reduce_max_sync(0xffffffffu, i);
+  i ^= (i >> 31) & 0x7fffffff;
+  return __int_as_float(i);
+#else
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+#endif
+}
+
+
 #ifndef AKVQ_LY_STAGES
 #define AKVQ_LY_STAGES 2
 #endif
@@ -194,6 +216,24 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// the same on precomputed shared-window addresses (no generic->shared conversion
+// in the pipeline loop)
+__device__ __forceinline__ void mbar_expect_tx(uint32_t b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {

@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   uint32_t *klimb = reinterpret_cast<uint32_t *>(wsm + S::kl_off(SB));
   uint32_t *vlimb = reinterpret_cast<uint32_t *>(wsm + S::vl_off(SB));
   uint64_t *bar = reinterpret_cast<uint64_t *>(wsm + S::bar_off(SB));
+  const uint32_t bar_s = smem_u32(bar), wsm_s = smem_u32(wsm);   // shared-window addresses
 
   // Programmatic dependent launch: q, k, v (and, after a flush or append, the
   // cache) come from the preceding grid.  When the host knows the preceding grid
@@ -151,11 +152,11 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   uint32_t pbits = 0u;
   const int pbw = (lane % (G / 4)) >> 3;
   auto produce = [&](int st) -> uint2 {
-    uint8_t *dst = wsm + (size_t)st * SB;
+    const uint32_t dst = wsm_s + (uint32_t)st * (uint32_t)SB, bst = bar_s + 8u * st;
     if (vsrc != nullptr) {                      // V half of the page whose K half went last
       if (lane == 0) {
-        mbar_expect_tx(&bar[st], vbytes);
-        bulk_g2s(dst, vsrc, vbytes, &bar[st]);
+        mbar_expect_tx(bst, vbytes);
+        bulk_g2s(dst, vsrc, vbytes, bst);
       }
       vsrc = nullptr;
       return vdesc;
@@ -214,8 +215,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           const uint8_t *pg = c.btab ? c.pages + (size_t)__ldg(c.btab + (size_t)sb.pu * c.n_pages + sb.a) * c.page_bytes
                                      : ub + (size_t)sb.a * c.page_bytes;
           if (lane == 0) {
-            mbar_expect_tx(&bar[st], kbytes);
-            bulk_g2s(dst, pg, kbytes, &bar[st]);
+            mbar_expect_tx(bst, kbytes);
+            bulk_g2s(dst, pg, kbytes, bst);
           }
           pbits = __ldg(c.bitmask + (size_t)sb.pu * c.bm_words + (size_t)a * (G / 32) + pbw);
           if constexpr (KT) {                     // exact R (R26): the last page is partial;
@@ -232,16 +233,16 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           const int n1 = min(sb.n, c.slots - s0);
           const uint32_t rowb = 4 * D;
           if (lane == 0) {
-            mbar_expect_tx(&bar[st], (uint32_t)sb.n * rowb);
-            bulk_g2s(dst, ring_row(c, sb.pu, s0), (uint32_t)n1 * rowb, &bar[st]);
+            mbar_expect_tx(bst, (uint32_t)sb.n * rowb);
+            bulk_g2s(dst, ring_row(c, sb.pu, s0), (uint32_t)n1 * rowb, bst);
             if (n1 < sb.n)
-              bulk_g2s(dst + (size_t)n1 * rowb, ring_row(c, sb.pu, 0), (uint32_t)(sb.n - n1) * rowb, &bar[st]);
+              bulk_g2s(dst + (uint32_t)n1 * rowb, ring_row(c, sb.pu, 0), (uint32_t)(sb.n - n1) * rowb, bst);
           }
         } else {
           const uint32_t eb = c.side_entry;
           if (lane == 0) {
-            mbar_expect_tx(&bar[st], (uint32_t)sb.n * eb);
-            bulk_g2s(dst, side_ptr(c, sb.pu, sb.a), (uint32_t)sb.n * eb, &bar[st]);
+            mbar_expect_tx(bst, (uint32_t)sb.n * eb);
+            bulk_g2s(dst, side_ptr(c, sb.pu, sb.a), (uint32_t)sb.n * eb, bst);
           }
         }
         break;
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         // writes the (empty) partial the unit's merge ticket counts on
         eu = sb.u;
         sb.kind = 4;
-        if (lane == 0) mbar_expect_tx(&bar[st], 0u);
+        if (lane == 0) mbar_expect_tx(bst, 0u);
         break;
       }
       sb.kind = -1;
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     if (s.kind < 0) break;
     uint8_t *B = wsm + (size_t)st * SB;
     if constexpr (SO) {                             // profiling: pipeline only
-      mbar_wait(&bar[st], par);
+      mbar_wait(bar_s + 8u * st, par);
       __syncwarp();
       if (st) { dsc1 = produce(st); bits1 = pbits; } else { dsc0 = produce(st); bits0 = pbits; }
       if (++st == kLyStages) { st = 0; par ^= 1u; }
@@ -579,7 +580,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     if (s.kind == 0) {
       // ================= page K half: logits of the page's G tokens
       const uint32_t sbits = ((st ? bits1 : bits0) >> (4 * (ktq & 7))) & 15u;
-      mbar_wait(&bar[st], par);
+      mbar_wait(bar_s + 8u * st, par);
       const float4 *ks4 = reinterpret_cast<const float4 *>(B + c.pg_kscale);
       const int4 *kz4 = reinterpret_cast<const int4 *>(B + c.pg_kzero);
       if constexpr (KT) {                      // per-token K variant (compile time)
@@ -650,6 +651,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       } else {
       float dA[NH];
       int bA[NH][3];
+      bool sat = false;                  // REDUX bias: a lane partial out of range
 #pragma unroll
       for (int h = 0; h < NH; ++h) {      // Q_c = rn(q~_c s^K_c inv): lane = channel quad
         float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -666,11 +668,27 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         // with |z| < 2^14)
         long long bz = (long long)(int)(x[0] - kQOff) * zq.x + (long long)(int)(x[1] - kQOff) * zq.y +
                        (long long)(int)(x[2] - kQOff) * zq.z + (long long)(int)(x[3] - kQOff) * zq.w;
+#if AKVQ_REDUX
+        // two 32-bit REDUX sums: lane partial = hi 65536 + lo, lo in [0, 65535]
+        // (sum < 2^21), hi saturated at +-2^26 (sum < 2^31); a saturated lane
+        // sends the page to the fp32 path (its bias is beyond the MMA range anyway)
+        {
+          const long long hl = bz >> 16;
+          const int hi = (int)(hl > (1LL << 26) ? (1LL << 26) : (hl < -(1LL << 26) ? -(1LL << 26) : hl));
+          sat |= hi == (1 << 26) || hi == -(1 << 26);
+          const unsigned slo = __reduce_add_sync(0xffffffffu, (unsigned)(bz & 0xffff));
+          const int shi = __reduce_add_sync(0xffffffffu, hi);
+          bA[h][0] = (int)(slo & 255u);
+          bA[h][1] = (int)((slo >> 8) & 255u);
+          bA[h][2] = shi + (int)(slo >> 16);
+        }
+#else
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) bz += __shfl_xor_sync(0xffffffffu, bz, o);
         bA[h][0] = (int)(bz & 255);
         bA[h][1] = (int)((bz >> 8) & 255);
         bA[h][2] = (int)(bz >> 16);
+#endif
         dA[h] = dAu[h];
         if (lane < CQ) {
           qlimb[(4 * h) * CQ + lane] = prmt(prmt(x[0], x[1], 0x0040), prmt(x[2], x[3], 0x0040), 0x5410) ^ 0x80808080u;
@@ -683,7 +701,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       // ~1000 in magnitude).  A page beyond that (a near-constant channel with a
       // large offset: tiny range, huge zero point) takes the plain fp32 path:
       // logit_t = alpha_k sum_c q~_c s_c (code_tc - z_c), each (code - z) exact.
-      bool slow = lp.exact_logits != 0;
+      bool slow = lp.exact_logits != 0 || __any_sync(0xffffffffu, sat);
 #pragma unroll
       for (int h = 0; h < NH; ++h) slow |= bA[h][2] >= (1 << 24) || bA[h][2] <= -(1 << 24);
       if (slow) {
@@ -725,7 +743,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       for (int h = 1; h < NH; ++h)
         if (hsel == h) { ba = bA[h][0]; bb = bA[h][1]; b2 = bA[h][2]; }
       if (rodd) { ba = b2; bb = 0; }
-      const float wB = rodd ? 0.f : 256.f;
+      const int wBi = rodd ? 0 : 256;
       float *lgw = lgs + ((rodd ? NH + 1 : 0) + min(rhead, NH)) * S::LP;
       const uint32_t *kcw = reinterpret_cast<const uint32_t *>(B + c.pg_kcodes);
       AKVQ_UNROLL(AKVQ_KU)
@@ -738,9 +756,10 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           mma_u8s8(c01, fmask(w.x, 0), fmask(w.x, 1), fmask(w.y, 0), fmask(w.y, 1), bq[cc][0], bq[cc][1]);
           mma_u8s8(c23, fmask(w.x, 2), fmask(w.x, 3), fmask(w.y, 2), fmask(w.y, 3), bq[cc][0], bq[cc][1]);
         }
+        // limb 0 + 256 limb 1 combined in int32 (|sum| < 2^30), one rounding like fmaf
         reinterpret_cast<float4 *>(lgw)[tq] =
-              make_float4(fmaf(wB, (float)c01[1], (float)c01[0]), fmaf(wB, (float)c01[3], (float)c01[2]),
-                          fmaf(wB, (float)c23[1], (float)c23[0]), fmaf(wB, (float)c23[3], (float)c23[2]));
+              make_float4((float)(c01[0] + wBi * c01[1]), (float)(c01[2] + wBi * c01[3]),
+                          (float)(c23[0] + wBi * c23[1]), (float)(c23[2] + wBi * c23[3]));
       }
       __syncwarp();
 #pragma unroll
@@ -757,7 +776,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       }   // per-channel K
     } else if (s.kind == 1) {
       // ================= page V half: softmax update, value accumulation
-      mbar_wait(&bar[st], par);
+      mbar_wait(bar_s + 8u * st, par);
       const float *vs = reinterpret_cast<const float *>(B);
       const int32_t *vz = reinterpret_cast<const int32_t *>(B + (c.pg_vzero - c.pg_vscale));
       const uint4 *vc4 = reinterpret_cast<const uint4 *>(B + (c.pg_vcodes - c.pg_vscale));
@@ -781,7 +800,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       }
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
-        const float mloc = warp_max(fmaxf(fmaxf(lg[h][0], lg[h][1]), fmaxf(lg[h][2], lg[h][3])));
+        const float mloc = warp_max_fast(fmaxf(fmaxf(lg[h][0], lg[h][1]), fmaxf(lg[h][2], lg[h][3])));
         const float m_new = fmaxf(m_run[h], mloc);
         live[h] = m_new != -INFINITY;                 // warp-uniform
 #pragma unroll
@@ -825,7 +844,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       // smem to the lane layout of o_rot (lane vcq: channels 4 vcq ..).
       constexpr int TC = G / 32;
       const uint32_t *vcw = reinterpret_cast<const uint32_t *>(vc4);
-      const float wBv = rodd ? 0.f : 256.f;
+      const int wBv = rodd ? 0 : 256;
       float *lvw = lgs + ((rodd ? NH + 1 : 0) + min(rhead, NH)) * S::LP;
       AKVQ_UNROLL(AKVQ_VU)
       for (int cb = 0; cb < D / 32; ++cb) {
@@ -841,8 +860,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         // per limb column: <= G tokens x 192 x 255 < 2^31 (exact); even lanes
         // store limb 0 + 256 limb 1, odd lanes limb 2 (x 65536 in the reader)
         reinterpret_cast<float4 *>(lvw)[cq] =
-              make_float4(fmaf(wBv, (float)c01[1], (float)c01[0]), fmaf(wBv, (float)c01[3], (float)c01[2]),
-                          fmaf(wBv, (float)c23[1], (float)c23[0]), fmaf(wBv, (float)c23[3], (float)c23[2]));
+              make_float4((float)(c01[0] + wBv * c01[1]), (float)(c01[2] + wBv * c01[3]),
+                          (float)(c23[0] + wBv * c23[1]), (float)(c23[2] + wBv * c23[3]));
       }
       __syncwarp();
       if (vts == 0) {
@@ -862,11 +881,11 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
         }
       }
     } else if (s.kind == 4) {
-      mbar_wait(&bar[st], par);                       // empty unit marker (no data)
+      mbar_wait(bar_s + 8u * st, par);                       // empty unit marker (no data)
     } else {
       // ================= rows: 16-bit (ring / PSA side, original basis) or
       //                   4-bit (TSA side, rotated basis), in groups of kRows
-      mbar_wait(&bar[st], par);
+      mbar_wait(bar_s + 8u * st, par);
       const bool r16 = s.kind == 2;
       if (s.ring && app_k != nullptr) {
         // the newest token (Eq. 2): the stale ring slot was staged -- patch in

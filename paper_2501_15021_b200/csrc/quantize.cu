@@ -91,6 +91,13 @@ __global__ void __launch_bounds__(1024) k_salient_psa(DevCache c, const float *_
 //      and V (common.cuh kword_idx / vword_idx) with coalesced stores.
 // Source rows come from the prefill inputs or, for a flush, from the ring.
 constexpr int kQThreads = 256;
+// packed fp32x2 FWHT and cheaper code rounding (A/B knob; results are identical)
+#ifndef AKVQ_QPACKED
+#define AKVQ_QPACKED 1
+#endif
+#ifndef AKVQ_QPREFETCH
+#define AKVQ_QPREFETCH 1
+#endif
 
 // Staged K rows xs[t][P]: 16-byte chunk c of a row is stored at chunk
 // c ^ ((c >> 2) & 7), so the 8 lanes of a row (16 consecutive channels each)
@@ -100,6 +107,37 @@ __device__ __forceinline__ int xs_col(int ch) { return ((((ch >> 2) ^ (ch >> 4))
 
 template <int CPL>
 __device__ __forceinline__ void fwht_lanes8(float (&x)[CPL], int cl) {
+#if AKVQ_QPACKED
+  // stage h = 1 scalar; stages h >= 2 pair the adjacent lower elements (j, j+1)
+  // with (j+h, j+h+1) as packed fp32x2 (FADD2 / FFMA2); a - b is fma(b, -1, a),
+  // one rounding like the scalar subtraction: bit-identical results
+#pragma unroll
+  for (int i = 0; i < CPL; i += 2) {
+    const float a = x[i], b = x[i + 1];
+    x[i] = __fadd_rn(a, b);
+    x[i + 1] = __fsub_rn(a, b);
+  }
+#pragma unroll
+  for (int h = 2; h < CPL; h <<= 1)
+#pragma unroll
+    for (int i = 0; i < CPL; i += 2 * h)
+#pragma unroll
+      for (int j = i; j < i + h; j += 2) {
+        const float2 a = make_float2(x[j], x[j + 1]), b = make_float2(x[j + h], x[j + h + 1]);
+        const float2 sm = __fadd2_rn(a, b), df = __ffma2_rn(b, make_float2(-1.f, -1.f), a);
+        x[j] = sm.x; x[j + 1] = sm.y; x[j + h] = df.x; x[j + h + 1] = df.y;
+      }
+#pragma unroll
+  for (int lm = 1; lm < 8; lm <<= 1) {
+    const float sg = (cl & lm) ? -1.f : 1.f;     // upper: partner - own; lower: own + partner
+#pragma unroll
+    for (int k = 0; k < CPL; k += 2) {
+      const float2 pr = make_float2(__shfl_xor_sync(0xffffffffu, x[k], lm), __shfl_xor_sync(0xffffffffu, x[k + 1], lm));
+      const float2 r = __ffma2_rn(make_float2(sg, sg), make_float2(x[k], x[k + 1]), pr);
+      x[k] = r.x; x[k + 1] = r.y;
+    }
+  }
+#else
 #pragma unroll
   for (int h = 1; h < CPL; h <<= 1)
 #pragma unroll
@@ -116,6 +154,7 @@ __device__ __forceinline__ void fwht_lanes8(float (&x)[CPL], int cl) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k) x[k] = __fmaf_rn(sg, x[k], __shfl_xor_sync(0xffffffffu, x[k], lm));
   }
+#endif
 }
 
 // min / max over the lanes of a channel group of GL lanes (within the 8-lane row group)
@@ -129,7 +168,7 @@ __device__ __forceinline__ void group_minmax(float &mn, float &mx) {
 }
 
 template <int D, int G, int DT, bool KT>
-__global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, QuantSrc src, int block0,
+__global__ void __launch_bounds__(kQThreads, 2) k_quantize_blocks(DevCache c, QuantSrc src, int block0,
                                                                int last_block) {
   constexpr int CPL = D / 8;                 // channels per lane
   constexpr int GL = G / CPL;                // lanes per V channel group
@@ -163,17 +202,49 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_blocks(DevCache c, Quant
 
   // ---------------- rows: FWHT of K and V, V quantization, side entries
   unsigned kmax_l = 0u, vmax_l = 0u;          // this lane's largest |stored scale| (bits)
+  auto row_off = [&](int t) -> size_t {     // element offset of token t's row
+    const int tok = j * G + t;
+    return (size_t)u * src.unit_stride +
+           (size_t)(src.ring_slots ? tok % src.ring_slots : tok) * src.tok_stride + cl * CPL;
+  };
+#if AKVQ_QPREFETCH
+  // the next row group's loads are issued before this one is processed
+  uint4 knx[CPL / 8], vnx[CPL / 8];
+  {
+    const size_t o = row_off(warp * 4 + rg);
+#pragma unroll
+    for (int i = 0; i < CPL / 8; ++i) {
+      knx[i] = reinterpret_cast<const uint4 *>(src.K + o)[i];
+      vnx[i] = reinterpret_cast<const uint4 *>(src.V + o)[i];
+    }
+  }
+#endif
   for (int r0 = warp * 4; r0 < G; r0 += NW * 4) {
     const int t = r0 + rg;                   // token within the block
     const int tok = j * G + t;
     const bool sal = (s_bits[t >> 5] >> (t & 31)) & 1u;
-    const size_t roff = (size_t)u * src.unit_stride +
-                        (size_t)(src.ring_slots ? tok % src.ring_slots : tok) * src.tok_stride;
-    const uint4 *kr = reinterpret_cast<const uint4 *>(src.K + roff + cl * CPL);
-    const uint4 *vr = reinterpret_cast<const uint4 *>(src.V + roff + cl * CPL);
     uint4 kraw[CPL / 8], vraw[CPL / 8];
+#if AKVQ_QPREFETCH
 #pragma unroll
-    for (int i = 0; i < CPL / 8; ++i) { kraw[i] = kr[i]; vraw[i] = vr[i]; }
+    for (int i = 0; i < CPL / 8; ++i) { kraw[i] = knx[i]; vraw[i] = vnx[i]; }
+    if (r0 + NW * 4 < G) {
+      const size_t o = row_off(t + NW * 4);
+#pragma unroll
+      for (int i = 0; i < CPL / 8; ++i) {
+        knx[i] = reinterpret_cast<const uint4 *>(src.K + o)[i];
+        vnx[i] = reinterpret_cast<const uint4 *>(src.V + o)[i];
+      }
+    }
+#else
+    {
+      const size_t o = row_off(t);
+#pragma unroll
+      for (int i = 0; i < CPL / 8; ++i) {
+        kraw[i] = reinterpret_cast<const uint4 *>(src.K + o)[i];
+        vraw[i] = reinterpret_cast<const uint4 *>(src.V + o)[i];
+      }
+    }
+#endif
     float k[CPL], v[CPL];
 #pragma unroll
     for (int i = 0; i < CPL / 8; ++i) { cvt8<DT>(kraw[i], k + 8 * i); cvt8<DT>(vraw[i], v + 8 * i); }

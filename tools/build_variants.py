@@ -17,11 +17,12 @@ def one(spec):
     out = os.path.join(ROOT, "build_exp", f"var_{name}")
     os.makedirs(out, exist_ok=True)
     objs = []
+    qflag = "AKVQ_Q" in flags
     for s in b.SOURCES:
         o = os.path.join(b.BUILD, s.replace(".cu", ".o"))
         api_only = "AKVQ_C" in flags and "AKVQ_MAX_TAB" not in flags
-        if (s == "decode_layer.cu" and not api_only) or (s == "api.cu" and ("AKVQ_MAX_TAB" in flags or api_only)) \
-                or (s == "decode_gqa.cu" and "AKVQ_GQ" in flags):
+        if (s == "decode_layer.cu" and not api_only and not qflag) or (s == "api.cu" and ("AKVQ_MAX_TAB" in flags or api_only)) \
+                or (s == "decode_gqa.cu" and "AKVQ_GQ" in flags) or (s == "quantize.cu" and qflag):
             o = os.path.join(out, s.replace(".cu", ".o"))
             subprocess.run([b.NVCC, *b.FLAGS, *flags.split(), "-c", os.path.join(b.CSRC, s), "-o", o], check=True)
         objs.append(o)
