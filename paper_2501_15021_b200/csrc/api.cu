@@ -185,7 +185,10 @@ DecodePlan plan_decode(const akvq_cache *c, int L, int n_q, bool build_tab = tru
     if (f.kind == AKVQ_PSA) {
       lp.Sc = (f.top_k > 0 && n_q > 0) ? (f.top_k + rows - 1) / rows : 0;   // <= rows each
     } else {
-      lp.Sc = n_q > 0 ? (n_q + 255) / 256 : 0;                              // text rows <= n_q
+#ifndef AKVQ_CSIDE_DIV
+#define AKVQ_CSIDE_DIV 1024   // side splits of a TSA layer: one per 1024 tokens of n_q (measured, r02z3)
+#endif
+      lp.Sc = n_q > 0 ? (n_q + AKVQ_CSIDE_DIV - 1) / AKVQ_CSIDE_DIV : 0;    // text rows <= n_q
       if (lp.Sc > 8) lp.Sc = 8;
       // the GQA kernel takes its rows one at a time for all heads (~ a page's work
       // per dozen rows): many small splits keep the long text tiers balanced

@@ -43,6 +43,9 @@
 namespace akvq {
 
 constexpr int kLyWarps = 4;        // warps per CTA
+#ifndef AKVQ_SIDE_RR
+#define AKVQ_SIDE_RR 1             // side splits take round-robin sub-loads (A/B knob)
+#endif
 constexpr int kLimbCols = 4;
 #ifndef AKVQ_LY_CTAS
 #define AKVQ_LY_CTAS 4
@@ -190,11 +193,19 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
           qd -= qd * lp.Sc > x;
           return qd;
         };
-        const int lo = fdiv(a * cnt), hi = fdiv((a + 1) * cnt);
         const int per = tsa ? kRows4 : kRows;
         sb.kind = tsa ? 3 : 2;
+#if AKVQ_SIDE_RR
+        // round-robin: split a takes the per-row sub-loads a, a + Sc, a + 2 Sc, ...
+        // (full sub-loads whatever the runtime count; splits past it are empty)
+        (void)fdiv;
+        sb.a = (a + part_i * lp.Sc) * per;
+        sb.n = min(per, cnt - sb.a);
+#else
+        const int lo = fdiv(a * cnt), hi = fdiv((a + 1) * cnt);
         sb.a = lo + part_i * per;
         sb.n = min(per, hi - sb.a);
+#endif
         ok = sb.n > 0;
         next = !ok;
         part_i = ok ? part_i + 1 : 0;
