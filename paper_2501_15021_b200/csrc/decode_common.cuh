@@ -280,6 +280,8 @@ __device__ __forceinline__ int ly_first_item(const LayerPlan &lp, int w) {
   if (lo == lp.per_u) { ++u; lo = 0; }
   return u * lp.per_u + lo;
 }
+// out-of-line copy (the 64-bit divisions are large; called twice per warp)
+static __device__ __noinline__ int ly_first_item_p(const LayerPlan *lp, int w) { return ly_first_item(*lp, w); }
 // unit of warp w's first item (O(1): c0 falls in unit c0 / cu unless past its last start)
 __device__ __forceinline__ int ly_first_unit(const LayerPlan &lp, int w) {
   const unsigned long long c0 = ly_first_cost(lp, w);

@@ -121,8 +121,8 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   }
   const int gw = blockIdx.x * kLyWarps + warp;
   if (gw >= lp.W) { if constexpr (DL) ly_exit(c, lp, lane, &cta_done); return; }
-  const int ib = ly_first_item(lp, gw);
-  const int ie = gw + 1 < lp.W ? ly_first_item(lp, gw + 1) : lp.T;
+  const int ib = ly_first_item_p(&lp, gw);       // (one out-of-line copy: code size)
+  const int ie = gw + 1 < lp.W ? ly_first_item_p(&lp, gw + 1) : lp.T;
   if (ib >= ie) { if constexpr (DL) ly_exit(c, lp, lane, &cta_done); return; }
   // this launch's token count, the new token included when it appends (DEVICE_L
   // launches have no prologue: the griddepcontrol.wait above has been passed)
@@ -271,18 +271,11 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
     }
     return pack_sub(sb);
   };
-  uint2 dsc0 = produce(0);
-  uint32_t bits0 = pbits;
-  uint2 dsc1 = produce(1);
-  uint32_t bits1 = pbits;
+  // stage descriptors; both stages are primed by the loop's (single) producer
+  // call site before the first consume (one inlined copy of produce)
+  uint2 dsc0 = make_uint2(0u, 0u), dsc1 = make_uint2(0u, 0u);
+  uint32_t bits0 = 0u, bits1 = 0u;
   static_assert(kLyStages == 2, "two stages: descriptors dsc0 / dsc1");
-  if (lp.prologue) {                            // inputs from the preceding grid from here on
-    pdl_wait();
-    pdl_launch_dependents();
-  }
-  // host-L mode: keep the device copy current (a later DEVICE_L launch reads it)
-  if constexpr (!DL)
-    if (lp.appends && blockIdx.x == 0 && threadIdx.x == 0) c.dstate->L = lp.L;
 
   // lane roles
   const int ktq = lane % TQ, kcs = lane / TQ;         // page K phase
@@ -446,19 +439,38 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
   int st = 0;
   uint32_t par = 0;
   bool unit_fresh = false;                          // KT: q limbs of the new unit pending
+  int rf = 0, nrf = kLyStages;                      // stages to (re)fill: both at first
+  bool first = true;
   for (;;) {
+#pragma unroll 1
+    for (; nrf > 0; --nrf, rf ^= 1) {               // the only producer call site
+      const uint2 d = produce(rf);
+      if (rf) { dsc1 = d; bits1 = pbits; } else { dsc0 = d; bits0 = pbits; }
+    }
+    if (first) {
+      first = false;
+      if (lp.prologue) {                          // inputs from the preceding grid from here on
+        pdl_wait();
+        pdl_launch_dependents();
+      }
+      // host-L mode: keep the device copy current (a later DEVICE_L launch reads it)
+      if constexpr (!DL)
+        if (lp.appends && blockIdx.x == 0 && threadIdx.x == 0) c.dstate->L = lp.L;
+    }
     const LySub s = unpack_sub(st ? dsc1 : dsc0);
-    if (s.kind < 0) break;
-    uint8_t *B = wsm + (size_t)st * SB;
     if constexpr (SO) {                             // profiling: pipeline only
+      if (s.kind < 0) break;
       mbar_wait(bar_s + 8u * st, par);
       __syncwarp();
-      if (st) { dsc1 = produce(st); bits1 = pbits; } else { dsc0 = produce(st); bits0 = pbits; }
+      rf = st;
+      nrf = 1;
       if (++st == kLyStages) { st = 0; par ^= 1u; }
       continue;
     }
-    if (s.u != cur_u) {
+    uint8_t *B = wsm + (size_t)st * SB;
+    if (s.kind < 0 || s.u != cur_u) {               // segment boundary (one flush site)
       if (cur_u >= 0) flush(cur_u);
+      if (s.kind < 0) break;
       cur_u = s.u;
       unit_fresh = true;
       cur_pu = s.u / HG;
@@ -937,11 +949,10 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       }
     }
     __syncwarp();                                   // every lane is done with stage st
-    if (st) { dsc1 = produce(st); bits1 = pbits; } else { dsc0 = produce(st); bits0 = pbits; }   // refill it
+    rf = st;                                        // refill it at the loop top
+    nrf = 1;
     if (++st == kLyStages) { st = 0; par ^= 1u; }
   }
-  if constexpr (!SO)
-    if (cur_u >= 0) flush(cur_u);
   if constexpr (DL) ly_exit(c, lp, lane, &cta_done);
 }
 
