@@ -282,6 +282,10 @@ __device__ __forceinline__ int ly_first_item(const LayerPlan &lp, int w) {
 }
 // out-of-line copy (the 64-bit divisions are large; called twice per warp)
 static __device__ __noinline__ int ly_first_item_p(const LayerPlan *lp, int w) { return ly_first_item(*lp, w); }
+// out-of-line: warps owning unit u's first and last items (segment flush)
+static __device__ __noinline__ int2 ly_warp_span_p(const LayerPlan *lp, int u) {
+  return make_int2(ly_warp_of(*lp, u, 0), ly_warp_of(*lp, u, lp->per_u - 1));
+}
 // unit of warp w's first item (O(1): c0 falls in unit c0 / cu unless past its last start)
 __device__ __forceinline__ int ly_first_unit(const LayerPlan &lp, int w) {
   const unsigned long long c0 = ly_first_cost(lp, w);

@@ -196,8 +196,8 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
   }
   const int gw = blockIdx.x * kGqWarps + warp;
   if (gw >= lp.W) { ly_exit(c, lp, lane, &cta_done); return; }
-  const int ib = ly_first_item(lp, gw);
-  const int ie = gw + 1 < lp.W ? ly_first_item(lp, gw + 1) : lp.T;
+  const int ib = ly_first_item_p(&lp, gw);       // (out of line: code size)
+  const int ie = gw + 1 < lp.W ? ly_first_item_p(&lp, gw + 1) : lp.T;
   if (ib >= ie) { ly_exit(c, lp, lane, &cta_done); return; }
   // this launch's token count, the new token included when it appends (DEVICE_L
   // launches have no prologue: the griddepcontrol.wait above has been passed)
@@ -322,14 +322,8 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
     }
     return pack_sub(sb);
   };
-  uint2 dsc0 = produce(0);
-  uint2 dsc1 = produce(1);
-  if (lp.prologue) {
-    pdl_wait();
-    pdl_launch_dependents();
-  }
-  // host-L mode: keep the device copy current (a later DEVICE_L launch reads it)
-  if (!lp.dev_L && lp.appends && blockIdx.x == 0 && threadIdx.x == 0) c.dstate->L = lp.L;
+  // stage descriptors, primed by the loop's single producer call site (code size)
+  uint2 dsc0 = make_uint2(0u, 0u), dsc1 = make_uint2(0u, 0u);
 
   // lane roles
   const int mg = lane >> 2, mt = lane & 3;            // MMA fragment group / thread in group
@@ -391,7 +385,8 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
       }
       if (mg == 0 && h < nh) { rec[D] = m; rec[D + 1] = fmaf(lp_t, fp, lr * fr); }
     }
-    const int w_lo = ly_warp_of(lp, u, 0), w_hi = ly_warp_of(lp, u, lp.per_u - 1);
+    const int2 wsp = ly_warp_span_p(&lp, u);      // (out of line: code size)
+    const int w_lo = wsp.x, w_hi = wsp.y;
     if (take_ticket(c, u, w_hi - w_lo + 1, lane)) {
       merge_gqa_unit<D, NH>(c, lp, part, u, out + ((size_t)(u / HG) * c.g + hg * NH) * D, nh, flags, lane);
       if (lane == 0) c.ticket[u] = 0u;
@@ -427,12 +422,28 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
 
   int st = 0;
   uint32_t par = 0;
+  int rf = 0, nrf = kLyStages;                      // stages to (re)fill: both at first
+  bool first = true;
   for (;;) {
+#pragma unroll 1
+    for (; nrf > 0; --nrf, rf ^= 1) {               // the only producer call site
+      const uint2 d = produce(rf);
+      if (rf) dsc1 = d; else dsc0 = d;
+    }
+    if (first) {
+      first = false;
+      if (lp.prologue) {
+        pdl_wait();
+        pdl_launch_dependents();
+      }
+      // host-L mode: keep the device copy current (a later DEVICE_L launch reads it)
+      if (!lp.dev_L && lp.appends && blockIdx.x == 0 && threadIdx.x == 0) c.dstate->L = lp.L;
+    }
     const LySub s = unpack_sub(st ? dsc1 : dsc0);
-    if (s.kind < 0) break;
     uint8_t *B = wsm + (size_t)st * SB;
-    if (s.u != cur_u) {
+    if (s.kind < 0 || s.u != cur_u) {               // segment boundary (one flush site)
       if (cur_u >= 0) flush(cur_u);
+      if (s.kind < 0) break;
       cur_u = s.u;
       cur_pu = s.u / HG;
       cur_hg = s.u - cur_pu * HG;
@@ -453,8 +464,8 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
         { const float a = x[2], b = x[3]; x[2] = a + b; x[3] = a - b; }
         { const float a = x[0], b = x[2]; x[0] = a + b; x[2] = a - b; }
         { const float a = x[1], b = x[3]; x[1] = a + b; x[3] = a - b; }
-#pragma unroll
-        for (int lm = 1; lm < CQ; lm <<= 1) {
+#pragma unroll 1
+        for (int lm = 1; lm < CQ; lm <<= 1) {     // (not unrolled: once per unit, code size)
           const bool upper = lane & lm;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -568,7 +579,8 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               float acc = 0.f;
-              for (int ch = 0; ch < D; ++ch)
+#pragma unroll 1
+              for (int ch = 0; ch < D; ++ch)              // (rare fp32 path: not unrolled)
                 acc = fmaf(qf[h * D + ch] * ksf[ch], (float)kcode_at(kcb, 4 * tq + k, ch, G) - (float)kzf[ch], acc);
               lgv[t][blk][k] = ((sw[blk] >> k) & 1u) ? -INFINITY : acc;   // q~ alpha_k . K^
             }
@@ -861,10 +873,10 @@ __global__ void __maxnreg__(AKVQ_GQ_REGS)
       }
     }
     __syncwarp();
-    if (st) dsc1 = produce(st); else dsc0 = produce(st);
+    rf = st;                                        // refill it at the loop top
+    nrf = 1;
     if (++st == kLyStages) { st = 0; par ^= 1u; }
   }
-  if (cur_u >= 0) flush(cur_u);
   ly_exit(c, lp, lane, &cta_done);
 }
 
