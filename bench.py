@@ -311,8 +311,9 @@ def main():
     ap.add_argument("--pivots", default="colsum", choices=["colsum", "massive"],
                     help="PSA saliency: column-sum top-k (BJ:5, graded) or massive-activation "
                          "pivots from a synthetic residual stream (P:209-213, NEXT-2)")
-    ap.add_argument("--k-axis", default="channel", choices=["channel", "token"],
-                    help="K quantization axis: per channel (R1, graded) or per token (P:246)")
+    ap.add_argument("--k-axis", default="channel", choices=["channel", "token", "token-exact"],
+                    help="K quantization axis: per channel (R1, graded), per token (P:246), or "
+                         "per token with the exact residual window (R26, NEXT-1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-strong-emulation", action="store_true",
                     help="skip the 1-GPU emulation of the strong-scaling per-rank shapes")
@@ -376,7 +377,8 @@ def main():
     for layer in range(n_layers):
         kind = w.kind(layer)
         cfg = ak.make_config(Ul, w.g, w.d, w.G, w.R, cap, w.top_k, kind, dt, w.clip2, w.clip4,
-                             1 if args.k_axis == "token" else 0)
+                             1 if args.k_axis.startswith("token") else 0,
+                             exact_r=1 if args.k_axis == "token-exact" else 0)
         lc = ak.LayerCache(cfg, device=dev)
         lc.handle.options = ((ak.AKVQ_OPT_STREAM_ONLY if args.stream_only else 0) |
                              (ak.AKVQ_OPT_SKIP_ROWS if args.skip_rows else 0) |
@@ -604,10 +606,14 @@ def main():
 
     flush = None
     st = args.warmup + 2 * args.steps
-    while caches[0].L - w.R - caches[0].n_q < w.G - 1 and caches[0].L < cap - 1:
+    # (exact residual window, R26: every step quantizes one token inside the timed
+    # region, there is no block flush to time separately)
+    while args.k_axis != "token-exact" and caches[0].L - w.R - caches[0].n_q < w.G - 1 \
+            and caches[0].L < cap - 1:
         one_step(*sync_inputs(st)); st += 1             # plain steps up to the boundary
     drain()
-    if caches[0].L - w.R - caches[0].n_q == w.G - 1 and caches[0].L < cap:
+    if args.k_axis != "token-exact" and caches[0].L - w.R - caches[0].n_q == w.G - 1 \
+            and caches[0].L < cap:
         fin = sync_inputs(st)
         torch.cuda.synchronize()
         if dist:
@@ -636,7 +642,8 @@ def main():
     # ---------------- 1-GPU emulation of the per-rank shapes of strong scaling
     # (the BJ:9 global batch split over 2 / 4 / 8 GPUs = batch 32 / 16 / 8 per rank)
     emul = None
-    if world == 1 and w1.name.startswith("sweep@b") and not args.no_strong_emulation:
+    if world == 1 and w1.name.startswith("sweep@b") and not args.no_strong_emulation \
+            and args.k_axis != "token-exact":
         del caches
         inputs.clear()
         torch.cuda.synchronize()

@@ -224,7 +224,8 @@ akvq_status akvq_cache_init(akvq_cache *c, const akvq_config *cfg, void *dev_buf
  * i32 [U][n_pages], entry (u, p) = index of the pool page holding logical page
  * p (tokens [pG, (p+1)G)) of unit u.  The caller owns both, fills the entries
  * of every page the cache will quantize before that happens (pages fill in
- * order: page p is written when n_q passes (p+1) G), and never maps one pool
+ * order: page p is written when n_q passes (p+1) G, or pG with cfg.exact_r,
+ * whose first token zeroes the page), and never maps one pool
  * page to two live logical pages.  Host call; no work is enqueued.
  * Errors: EINVAL (NULL, or a cache that is not paged).  Every other call on a
  * paged cache without attached pages returns ESTATE. */

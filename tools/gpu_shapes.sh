@@ -11,3 +11,4 @@ run video13b --workload video13b
 run qwen --workload qwen_gqa
 run ktoken --k-axis token
 run massive --pivots massive
+run ktoken_exact --k-axis token-exact

@@ -3,7 +3,8 @@
 
 For a workload's layer (synthetic LLaVA-shaped inputs with K outlier channels),
 runs prefill + decode steps through libakvq.so for both K axes -- per channel
-over G-token blocks (R1, graded) and per token over G-channel groups --
+over G-token blocks (R1, graded) and per token over G-channel groups,
+the latter also with the exact residual window (R26: exactly R 16-bit rows) --
 and compares each decode output with plain unquantized attention computed in
 fp64 by torch on the CPU over the same 16-bit rows (q.K^T/sqrt d, softmax, .V).
 Reports cosine similarity and relative L2 error per layer kind (mean / min
@@ -38,10 +39,10 @@ def reference(Kall, Vall, q):
     return torch.einsum("ngl,nld->ngd", torch.softmax(s, -1), Vall)
 
 
-def run(w, layer, k_axis, steps, units, wht=True):
+def run(w, layer, k_axis, steps, units, wht=True, exact_r=0):
     dt = ak.AKVQ_BF16 if w.dtype == "bf16" else ak.AKVQ_FP16
     cfg = ak.make_config(w.U, w.g, w.d, w.G, w.R, w.L0 + steps, w.top_k, w.kind(layer), dt,
-                         w.clip2, w.clip4, k_axis)
+                         w.clip2, w.clip4, k_axis, exact_r=exact_r)
     lc = ak.LayerCache(cfg)
     inp = synth.layer_inputs(w, layer, device="cuda")
     tdt = inp["K"].dtype
@@ -83,8 +84,9 @@ def main():
     rows = []
     for layer in [l for l in (tsa, psa) if l is not None]:
         for wht in (True, False):
-            for k_axis, name in ((0, "per-channel K (R1)"), (1, "per-token K (P:246)")):
-                r = run(w, layer, k_axis, a.steps, units, wht)
+            for k_axis, ex, name in ((0, 0, "per-channel K (R1)"), (1, 0, "per-token K (P:246)"),
+                                     (1, 1, "per-token K, exact R (R26)")):
+                r = run(w, layer, k_axis, a.steps, units, wht, ex)
                 r.update(layer=layer, kind="TSA" if w.kind(layer) == 0 else "PSA", k_axis=name,
                          wht="on" if wht else "off")
                 rows.append(r)
