@@ -574,10 +574,13 @@ akvq_status akvq_decode_step(akvq_cache *c, const void *k, const void *v, const 
   const int L1 = c->L + 1;
   if ((c->options & AKVQ_OPT_DEVICE_L) && f.exact_r) return AKVQ_EUNSUPPORTED;
   // exact R (R26): token n_q leaves the window at this step; it is quantized
-  // from the ring before the fused launch (it does not depend on the new token)
-  const bool leave1 = f.exact_r && L1 - f.residual > c->n_q;
-  const bool flush = !f.exact_r && L1 - f.residual - c->n_q >= f.group;
-  DecodePlan p = plan_decode(c, L1, flush ? c->n_q + f.group : c->n_q + (leave1 ? 1 : 0));
+  // from the ring before the fused launch (it does not depend on the new token).
+  // With R = 0 the leaving token IS the new one (not in the ring yet): that step
+  // takes the unfused path (append, then quantize it from the ring, then decode).
+  const bool ex0 = f.exact_r && f.residual == 0;
+  const bool leave1 = f.exact_r && !ex0 && L1 - f.residual > c->n_q;
+  const bool flush = (!f.exact_r && L1 - f.residual - c->n_q >= f.group) || ex0;
+  DecodePlan p = plan_decode(c, L1, flush ? c->n_q + (ex0 ? 1 : f.group) : c->n_q + (leave1 ? 1 : 0));
   if (ws_bytes < ws_bytes_for(c, p)) return AKVQ_ECAPACITY;
   if (leave1) {
     const DevCache d = make_dev(c);

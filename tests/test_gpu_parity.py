@@ -656,6 +656,18 @@ def test_tiny_exact_r(ak, orc, sy, kind, options):
         assert np.all(np.abs(a - b) <= 1e-6 * np.maximum(np.abs(b), np.abs(b).max(-1, keepdims=True)) + 1e-7)
 
 
+@pytest.mark.parametrize("R", [0, 1])
+@pytest.mark.parametrize("kind", [1, 0], ids=["PSA", "TSA"])
+def test_exact_r_small_window(ak, orc, sy, kind, R):
+    """Exact R with R = 0 (the new token itself leaves the window at once: the
+    fused step must append before quantizing it) and R = 1, fused and split
+    calls alternating, state and outputs vs the oracle at every step."""
+    import dataclasses
+    w = dataclasses.replace(sy.TINY, name=f"tiny_er_r{R}", R=R)
+    lc, oc, _ = _run_case(ak, orc, sy, w, 0, kind=kind, steps=16, k_axis=1, exact_r=1)
+    assert lc.n_q == lc.L - R
+
+
 @pytest.mark.parametrize("layer", [0, 2], ids=["TSA-L0", "PSA-L2"])
 def test_llava7b_exact_r(ak, orc, sy, layer):
     _run_case(ak, orc, sy, sy.LLAVA7B, layer, steps=6, units=[0, 13, 31], k_axis=1, exact_r=1)

@@ -95,8 +95,9 @@ def test_random_operation_sequences(ak, orc):
             if op in ("step", "decode"):
                 ref = oc.decode(f16_bits(q))
                 err = np.abs(out.double().cpu().numpy() - ref).max()
-                assert err <= OUT_TOL, (cfg.n_units, g, d, G, R, kind, k_axis, exact_r, dev_L, op,
-                                        lc.L, err)
+                assert err <= OUT_TOL, (f"U {cfg.n_units} g {g} d {d} G {G} R {R} kind {kind} "
+                                        f"k_axis {k_axis} exact_r {exact_r} dev_L {dev_L} op {op} "
+                                        f"L {lc.L} n_q {lc.n_q} err {err}")
             assert (lc.L, lc.n_q) == (oc.L, oc.nq)
             ops += 1
             if rng.random() < 0.01:
