@@ -43,6 +43,9 @@
 namespace akvq {
 
 constexpr int kLyWarps = 4;        // warps per CTA
+#ifndef AKVQ_R4U
+#define AKVQ_R4U 2
+#endif
 #ifndef AKVQ_SIDE_RR
 #define AKVQ_SIDE_RR 1             // side splits take round-robin sub-loads (A/B knob)
 #endif
@@ -419,7 +422,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k) { o_rot[h][k] *= sc; o_org[h][k] *= sc; }
-#pragma unroll
+        AKVQ_UNROLL(AKVQ_R4U)                 // 4-bit rows (TSA only): code size knob
         for (int i = 0; i < NV; ++i) {
           const int row = vts + VTS * i;
           const float pr = __shfl_sync(0xffffffffu, p, (lane & (BFLY - 1)) | rs_enc<NV, CQ>(i) | (vts * CQ));
