@@ -43,6 +43,9 @@
 namespace akvq {
 
 constexpr int kLyWarps = 4;        // warps per CTA
+#ifndef AKVQ_R16U
+#define AKVQ_R16U 8
+#endif
 #ifndef AKVQ_R4U
 #define AKVQ_R4U 2
 #endif
@@ -405,7 +408,7 @@ __global__ void __launch_bounds__(kLyWarps * 32, ly_ctas_per_sm(NH))
       if (r16) {
         float2 oa = __fmul2_rn(make_float2(o_org[h][0], o_org[h][1]), make_float2(sc, sc));
         float2 ob = __fmul2_rn(make_float2(o_org[h][2], o_org[h][3]), make_float2(sc, sc));
-#pragma unroll
+        AKVQ_UNROLL(AKVQ_R16U)                // 16-bit rows: code size knob
         for (int i = 0; i < NV; ++i) {
           const int row = vts + VTS * i;
           const float pr = __shfl_sync(0xffffffffu, p, (lane & (BFLY - 1)) | rs_enc<NV, CQ>(i) | (vts * CQ));

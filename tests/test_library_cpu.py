@@ -131,3 +131,15 @@ def test_ticket_region_covers_every_head_group(ak, g):
     decode kernel for every supported q_per_kv (g up to 16)."""
     y = ak.akvq_cache_layout(_cfg(ak, g=g))
     assert y.total_bytes - y.ticket_off >= 4 * 4 * max(1, g)      # U = 4 units, <= g groups
+
+
+def test_exact_r_config(ak):
+    """exact_r (R26) needs per-token K and is 0 / 1; the layout does not change."""
+    def mk(k_axis, exact_r):
+        return ak.make_config(4, 1, 128, 128, 32, 800, 15, ak.AKVQ_PSA, ak.AKVQ_BF16, 0.8, 1.0,
+                              k_axis, exact_r=exact_r)
+    for k_axis, ex in ((0, 1), (1, 2), (1, -1)):
+        with pytest.raises(ak.AkvqError) as e:
+            ak.akvq_cache_layout(mk(k_axis, ex))
+        assert e.value.status == ak.AKVQ_EINVAL, (k_axis, ex)
+    assert ak.akvq_cache_bytes(mk(1, 1)) == ak.akvq_cache_bytes(mk(1, 0)) > 0
