@@ -11,10 +11,11 @@ import re
 import subprocess
 
 KERNELS = [
-    ("k_decode_layer<128,128,bf16,NH=1,PSA,per-channel>", "_ZN4akvq14k_decode_layerILi128ELi128ELi0ELi1ELb0ELi0EEEvNS_8DevCacheENS_9LayerPlanEPKtS4_S4_PKhPfS7_j"),
-    ("k_decode_layer<128,128,bf16,NH=1,TSA,per-channel>", "_ZN4akvq14k_decode_layerILi128ELi128ELi0ELi1ELb1ELi0EEEvNS_8DevCacheENS_9LayerPlanEPKtS4_S4_PKhPfS7_j"),
+    ("k_decode_layer<128,128,bf16,NH=1,PSA,per-channel>", "_ZN4akvq14k_decode_layerILi128ELi128ELi0ELi1ELb0ELi0ELb0EEEvNS_8DevCacheENS_9LayerPlanEPKtS4_S4_PKhPfS7_j"),
+    ("k_decode_layer<128,128,bf16,NH=1,TSA,per-channel>", "_ZN4akvq14k_decode_layerILi128ELi128ELi0ELi1ELb1ELi0ELb0EEEvNS_8DevCacheENS_9LayerPlanEPKtS4_S4_PKhPfS7_j"),
     ("k_decode_gqa<128,128,bf16,NH=8,PSA>", "_ZN4akvq12k_decode_gqaILi128ELi128ELi0ELi8ELb0EEEvNS_8DevCacheENS_9LayerPlanEPKtS4_S4_PKhPfS7_j"),
     ("k_quantize_blocks<128,128,bf16,per-channel>", "_ZN4akvq17k_quantize_blocksILi128ELi128ELi0ELb0EEEvNS_8DevCacheENS_8QuantSrcEii"),
+    ("k_quantize_tokens<128,128,bf16> (exact R, R26)", "_ZN4akvq17k_quantize_tokensILi128ELi128ELi0EEEvNS_8DevCacheENS_8QuantSrcEii"),
 ]
 WATCH = ["IMMA", "HMMA", "UTCMMA", "UBLKCP", "UTMALDG", "SYNCS", "ACQBULK", "SHFL", "LOP3", "PRMT",
          "I2FP", "F2I", "MUFU", "FFMA", "FFMA2", "FMUL2", "LDS", "STS", "LDG", "STG", "ATOM", "RED",
